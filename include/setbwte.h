@@ -1,0 +1,185 @@
+/*
+ * setbwte.h -- C-ABI of libsetbwte.so, a B200-native (sm_100a) implementation
+ * of the per-block insertion step of set-bwte (arXiv 1410.0562).
+ *
+ * Citations: "P:<line>" is a line of /root/reference/PAPER.md, with the
+ * section / equation / algorithm it falls in.  Readings of the paper that the
+ * library takes where the paper is silent or inconsistent are numbered R1..R16
+ * in DESIGN.md ("Readings").
+ *
+ * What the library computes
+ * -------------------------
+ * The BWT of a string set S_0..S_{m-1} over an ordered alphabet
+ * c_1 < ... < c_sigma (Sec.2) is the BWT of
+ *     T = S_0 $_0 S_1 $_1 ... S_{m-1} $_{m-1},  $_0 < ... < $_{m-1} < c_1
+ * (P:36-37), B[i] = T[(SA[i]-1) mod n] (Eq.(1)).  Strings are added
+ * block by block (Algorithm 1): each block is suffix sorted
+ * (ConstructSA, Sec.3), its BWT symbols B_int are extracted,
+ * its suffixes are ranked in the existing BWT B_ext (ComputeRanks, Lemma 1
+ * P:95-100 / Algorithm 2), the ranks are reordered by suffix order
+ * (g -> g_sa) and B_int is inserted into B_ext (Insert, Sec.5
+ * P:127-165).  All of it runs as CUDA kernels on the device the handle is
+ * bound to; there is no CPU fallback.
+ *
+ * Conventions (all calls)
+ * -----------------------
+ * - A handle is bound to the CUDA device current at setbwte_create and is not
+ *   thread-safe.  The library owns all device state; the caller owns every
+ *   buffer it passes.  Host pointers are borrowed for the duration of the
+ *   call only.  "Device" pointers must be CUDA device (or managed) memory on
+ *   the handle's device.
+ * - Every call is synchronous with respect to the host (it returns after its
+ *   device work has completed on the handle's stream), unless stated.
+ * - No call aborts the process.  A CUDA error inside a call returns
+ *   SETBWTE_E_CUDA and makes the handle sticky-failed: later calls return
+ *   SETBWTE_E_STATE.
+ * - Terminators are written '$' (every $_j collapses to '$', reading R5);
+ *   row order still identifies them: rows 0..m-1 are $_0..$_{m-1}.
+ * - The empty index has n = 0 and rank(c, 0) = 0.
+ */
+#ifndef SETBWTE_H
+#define SETBWTE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct setbwte_s* setbwte_t;
+
+typedef enum {
+    SETBWTE_OK = 0,
+    SETBWTE_E_INVALID_ARG = 1,   /* bad pointer, size, option key/value, offsets not CSR */
+    SETBWTE_E_INVALID_CHAR = 2,  /* a string byte outside the alphabet; see setbwte_last_error */
+    SETBWTE_E_OUT_OF_RANGE = 3,  /* rank position k > n */
+    SETBWTE_E_NOMEM = 4,         /* device or pinned-host allocation failed */
+    SETBWTE_E_CUDA = 5,          /* a CUDA runtime/kernel error (handle becomes sticky-failed) */
+    SETBWTE_E_UNSUPPORTED = 6,   /* e.g. sigma > 4 on the 2-bit path, block too large */
+    SETBWTE_E_STATE = 7          /* handle previously failed, or call not valid now */
+} setbwte_status;
+
+/* Create an empty index.  alphabet: NUL-terminated, 1..4 distinct bytes in
+ * increasing symbol order c_1 < ... < c_sigma (Sec.2), e.g. "ACGT";
+ * '$' is reserved.  Matching is case-insensitive (reading R10).  sigma > 4 ->
+ * SETBWTE_E_UNSUPPORTED (2-bit packed path).  Binds the current CUDA device
+ * and creates a private non-blocking stream.  *out receives the handle. */
+setbwte_status setbwte_create(const char* alphabet, setbwte_t* out);
+
+/* Release all device and host resources of h (NULL is a no-op). */
+void setbwte_destroy(setbwte_t h);
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* setbwte_strerror(setbwte_status s);
+
+/* Append m strings, in order, to the index (Algorithm 1 P:54-76 run over the
+ * blocks the strings are partitioned into; "adding new strings at
+ * any time").
+ *   strings : HOST bytes; string j is strings[offsets[j] .. offsets[j+1]).
+ *             No terminators in the input; empty strings are allowed
+ *             (reading R11).
+ *   offsets : HOST array of m+1 non-decreasing u64, offsets[0] = 0.
+ *   m       : number of strings (0 is a no-op).
+ * The input is copied to the device, validated and packed before the index
+ * is touched: all-or-nothing -- on any error the index is unchanged.  A byte
+ * outside the alphabet returns SETBWTE_E_INVALID_CHAR; setbwte_last_error
+ * then reports the lowest offending byte position.
+ * Post: setbwte_bwt() == the one-shot BWT (Eq.(1)) of every string appended
+ * so far, in append order; the result does not depend on the block size
+ * (reading R8). */
+setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                              uint64_t m);
+
+/* Same as setbwte_append with DEVICE-resident inputs (d_strings, d_offsets on
+ * the handle's device; same layout).  No host<->device copy of the strings. */
+setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,
+                                     const uint64_t* d_offsets, uint64_t m);
+
+/* Remove every string (n = m = 0) but keep device allocations for reuse. */
+setbwte_status setbwte_clear(setbwte_t h);
+
+/* Current size: *n = sum(|S_j|+1) symbols of B, *m = number of strings. */
+setbwte_status setbwte_size(setbwte_t h, uint64_t* n, uint64_t* m);
+
+/* Write the BWT B[0..n) as ASCII ('$' for every terminator) into HOST buffer
+ * out of capacity cap bytes.  out == NULL -> size query: *n set, OK.
+ * cap < n -> SETBWTE_E_INVALID_ARG. */
+setbwte_status setbwte_bwt(setbwte_t h, uint8_t* out, uint64_t cap, uint64_t* n);
+
+/* Same as setbwte_bwt into a DEVICE buffer d_out. */
+setbwte_status setbwte_bwt_device(setbwte_t h, uint8_t* d_out, uint64_t cap, uint64_t* n);
+
+/* Eq.(2): *out = rank(c, k, B) = |{ i < k : B[i] = c }|.
+ * c: a byte of the alphabet (either case) or '$' (rank of '$' is
+ * k - sum_c rank(c,k), reading R12).  k > n -> SETBWTE_E_OUT_OF_RANGE;
+ * unknown c -> SETBWTE_E_INVALID_ARG. */
+setbwte_status setbwte_rank(setbwte_t h, uint8_t c, uint64_t k, uint64_t* out);
+
+/* Batched Eq.(2) on the device: out_dev[i] = rank(c_dev[i], k_dev[i]) for
+ * i < q.  All three arrays are DEVICE pointers.  A query with an unknown c or
+ * k > n yields UINT64_MAX in its slot (no error is raised for it). */
+setbwte_status setbwte_rank_batch(setbwte_t h, const uint8_t* c_dev, const uint64_t* k_dev,
+                                  uint64_t q, uint64_t* out_dev);
+
+/* ConstructSA + B_int of ONE block, without touching the index (Alg.1
+ * P:60-63; Sec.3).  Inputs as setbwte_append (HOST).  The block must
+ * hold fewer than 2^31 suffixes.  Outputs (HOST, each n_suf = offsets[m]+m
+ * entries, either may be NULL):
+ *   sa_out   : SA_int as block slot ids, slot(j,k) = offsets[j] + j + k
+ *              (string-major layout, reading R2); terminator ties ordered by
+ *              string index.
+ *   bint_out : B_int as ASCII, '$' where k = 0. */
+setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                                    uint64_t m, uint32_t* sa_out, uint8_t* bint_out);
+
+/* ComputeRanks of ONE block against the current index, without modifying it
+ * (Lemma 1, Algorithm 2 P:106-123 with i := m_ext, reading R1).
+ * g_out (HOST, n_suf u64) receives, per slot (layout as above), the number of
+ * suffixes in the index smaller than that suffix of the block, the block's
+ * strings taking global indices m_ext, m_ext+1, ... */
+setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                                     uint64_t m, uint64_t* g_out);
+
+/* Options (integer valued).  Unknown key or invalid value ->
+ * SETBWTE_E_INVALID_ARG.  Keys:
+ *   "block_suffixes"  M, target suffixes per block (emit a block when
+ *                     it reaches >= M, reading R8).  1 <= M <= 2^30.
+ *                     Default 2^24.
+ *   "profile"         1: time every kernel launch with CUDA events on the
+ *                     handle's stream (reported by setbwte_stats); 0: off.
+ *   "rank_ilp"        strings per thread in the ComputeRanks kernel (1..4). */
+setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value);
+
+/* Use cuda_stream (a cudaStream_t on the handle's device) for all further
+ * work instead of the private stream; NULL restores the private stream. */
+setbwte_status setbwte_set_stream(setbwte_t h, void* cuda_stream);
+
+/* Multi-process data parallelism over strings (Sec.8(e) of SURVEY.md):
+ * ComputeRanks of every block runs only on this rank's contiguous slice of
+ * the block's strings (balanced by suffix count), then `allgather` is called
+ * to assemble the full g on every rank.  allgather(buf, bytes_per_rank, world,
+ * stream, ctx): buf is a DEVICE buffer holding the concatenation of all
+ * ranks' slices; this rank's slice is already filled; on return (work queued
+ * on `stream` is allowed) every slice must be filled.  bytes_per_rank has
+ * `world` entries.  world == 1 (the default) disables the exchange. */
+typedef int (*setbwte_allgather_fn)(void* buf, const uint64_t* bytes_per_rank, int world,
+                                    void* stream, void* ctx);
+setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,
+                                     setbwte_allgather_fn allgather, void* ctx);
+
+/* Per-stage statistics of the last append as a NUL-terminated JSON object
+ * written into HOST buffer out (cap bytes); *n receives the length needed
+ * (including NUL).  out == NULL -> size query.  Includes per-kernel launch
+ * counts, and (when "profile" is on) per-kernel CUDA-event time and
+ * algorithmic bytes. */
+setbwte_status setbwte_stats(setbwte_t h, char* out, uint64_t cap, uint64_t* n);
+
+/* Details of the last SETBWTE_E_INVALID_CHAR: the byte position (in the
+ * strings buffer of that call) and the byte. */
+setbwte_status setbwte_last_error(setbwte_t h, uint64_t* pos, uint8_t* byte);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SETBWTE_H */

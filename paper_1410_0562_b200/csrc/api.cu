@@ -1,0 +1,705 @@
+// api.cu -- the host runtime behind include/setbwte.h: the handle, the
+// per-append stage sequence of Algorithm 1 on one CUDA stream, the
+// ping-pong B_ext dictionary, error state and statistics.
+#include <ctype.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "setbwte.h"
+
+using namespace setbwte;
+
+// ---------------------------------------------------------------------------
+// DevBuf / Profiler
+// ---------------------------------------------------------------------------
+namespace setbwte {
+
+cudaError_t ensure_bytes(DevBuf& b, size_t bytes) {
+    if (bytes <= b.cap && b.p) return cudaSuccess;
+    if (b.p) {
+        cudaError_t e = cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        if (e != cudaSuccess) return e;
+    }
+    size_t cap = bytes + bytes / 4;  // 1.25x headroom against regrowth
+    cudaError_t e = cudaMalloc(&b.p, cap);
+    if (e != cudaSuccess) {
+        b.p = nullptr;
+        return e;
+    }
+    b.cap = cap;
+    return cudaSuccess;
+}
+
+static void free_buf(DevBuf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+cudaEvent_t Profiler::get_event() {
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void Profiler::begin(const char* name, cudaStream_t s, double bytes, uint64_t units,
+                     cudaEvent_t* ev) {
+    KStat& ks = k[name];
+    ks.launches++;
+    ks.bytes += bytes;
+    ks.units += units;
+    total_launches++;
+    if (on) {
+        *ev = get_event();
+        cudaEventRecord(*ev, s);
+    }
+}
+
+void Profiler::end(const char* name, cudaStream_t s, cudaEvent_t a) {
+    if (on && a) {
+        cudaEvent_t b = get_event();
+        cudaEventRecord(b, s);
+        pending.push_back(Rec{name, a, b});
+    }
+}
+
+cudaError_t Profiler::resolve() {
+    cudaError_t err = cudaSuccess;
+    for (Rec& r : pending) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e == cudaSuccess) k[r.name].ms += ms; else err = e;
+        pool.push_back(r.a);
+        pool.push_back(r.b);
+    }
+    pending.clear();
+    return err;
+}
+
+void Profiler::reset() {
+    for (Rec& r : pending) {
+        pool.push_back(r.a);
+        pool.push_back(r.b);
+    }
+    pending.clear();
+    k.clear();
+    total_launches = 0;
+}
+
+Profiler::~Profiler() {
+    for (Rec& r : pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
+}  // namespace setbwte
+
+// ---------------------------------------------------------------------------
+// Handle
+// ---------------------------------------------------------------------------
+struct DevErr {
+    unsigned long long err_pos;
+    int bad_offsets;
+    int pad;
+};
+
+struct setbwte_s {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    Profiler prof;
+    bool failed = false;
+
+    // alphabet
+    char alpha[5] = {0};
+    int sigma = 0;
+    uint8_t code_of[256];
+    DevBuf d_code_of, d_sym;
+
+    // the index: B_ext as a rank dictionary, ping-pong (reading: Sec.5)
+    uint64_t n = 0, m = 0;
+    DevBuf blk[2], sb[2];
+    int cur = 0;
+    DevBuf d_C, sb_tot;
+
+    // append scratch
+    DevBuf in_bytes, in_off, text, term, slot_off, bounds, err, small;
+    DevBuf saf, g, pos, bint, outbuf;
+    SortScratch sort;
+
+    // options
+    uint64_t M = 1ull << 24;
+    int rank_ilp = 1;
+
+    // data-parallel ComputeRanks
+    int rank = 0, world = 1;
+    setbwte_allgather_fn allgather = nullptr;
+    void* allgather_ctx = nullptr;
+
+    // diagnostics
+    uint64_t err_pos = 0;
+    uint8_t err_byte = 0;
+    uint64_t last_blocks = 0, last_bases = 0, last_m = 0;
+    SortStats sstats;
+    std::string stats_json;
+};
+
+namespace {
+
+setbwte_status from_cuda(setbwte_t h, cudaError_t e) {
+    if (e == cudaSuccess) return SETBWTE_OK;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) return SETBWTE_E_NOMEM;
+    if (h) h->failed = true;
+    return SETBWTE_E_CUDA;
+}
+
+#define API_CHECK(h, expr)                                    \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return from_cuda((h), _e);     \
+    } while (0)
+
+#define API_ENTER(h)                                          \
+    do {                                                      \
+        if (!(h)) return SETBWTE_E_INVALID_ARG;               \
+        if ((h)->failed) return SETBWTE_E_STATE;              \
+        cudaError_t _d = cudaSetDevice((h)->device);          \
+        if (_d != cudaSuccess) return from_cuda((h), _d);     \
+    } while (0)
+
+struct PackOut {
+    Packed pk;
+    uint64_t n_bytes = 0;
+};
+
+// Validate + pack an append whose inputs are already on the device.
+setbwte_status pack_input(setbwte_t h, const uint8_t* d_bytes, const uint64_t* d_off, uint64_t m,
+                          PackOut* out) {
+    uint64_t n_bytes = 0;
+    API_CHECK(h, cudaMemcpyAsync(&n_bytes, d_off + m, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                 h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    const uint64_t n_slots = n_bytes + m;
+    const uint64_t n_groups = (n_slots + 31) / 32;
+    Packed pk;
+    pk.n_slots = n_slots;
+    API_CHECK(h, ensure(h->text, 2 * n_groups + 8, &pk.text));
+    API_CHECK(h, ensure(h->term, n_groups + 8, &pk.term));
+    API_CHECK(h, ensure(h->slot_off, m + 2, &pk.slot_off));
+    DevErr* derr;
+    API_CHECK(h, ensure(h->err, 1, &derr));
+    DevErr init{~0ull, 0, 0};
+    API_CHECK(h, cudaMemcpyAsync(derr, &init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, launch_pack(h->prof, h->stream, d_bytes, d_off, m, n_bytes,
+                             (const uint8_t*)h->d_code_of.p, pk, &derr->err_pos,
+                             &derr->bad_offsets));
+    DevErr res;
+    API_CHECK(h, cudaMemcpyAsync(&res, derr, sizeof(res), cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    if (res.bad_offsets) return SETBWTE_E_INVALID_ARG;
+    if (res.err_pos != ~0ull) {
+        h->err_pos = res.err_pos;
+        uint8_t b = 0;
+        API_CHECK(h, cudaMemcpy(&b, d_bytes + res.err_pos, 1, cudaMemcpyDeviceToHost));
+        h->err_byte = b;
+        return SETBWTE_E_INVALID_CHAR;
+    }
+    out->pk = pk;
+    out->n_bytes = n_bytes;
+    return SETBWTE_OK;
+}
+
+// Dictionary accessors for the current B_ext.
+inline const Blk* cur_blk(setbwte_t h) { return (const Blk*)h->blk[h->cur].p; }
+inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cur].p; }
+
+// ComputeRanks for strings [j0, j1) of a packed append, into g (block-local
+// slots starting at slot_base).  With world > 1, only this rank's slice is
+// computed and the slices are exchanged by the allgather callback.
+setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1,
+                                 uint64_t slot_base, uint64_t n_suf, uint64_t* g) {
+    if (h->n == 0) {
+        // empty B_ext: every suffix has rank 0
+        API_CHECK(h, cudaMemsetAsync(g, 0, n_suf * sizeof(uint64_t), h->stream));
+        return SETBWTE_OK;
+    }
+    if (h->world <= 1) {
+        API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
+                                          slot_base, cur_blk(h), cur_sb(h),
+                                          (const uint64_t*)h->d_C.p, h->m, n_suf - (j1 - j0), g,
+                                          h->rank_ilp));
+        return SETBWTE_OK;
+    }
+    // data-parallel over strings: balanced slices by suffix count
+    uint64_t* d_sl;
+    API_CHECK(h, ensure(h->small, 2 * (size_t)h->world + 8, &d_sl));
+    API_CHECK(h, launch_slices(h->prof, h->stream, pk.slot_off, j0, j1, h->world, d_sl));
+    std::vector<uint64_t> sl(h->world + 1), so(h->world + 1);
+    API_CHECK(h, cudaMemcpyAsync(sl.data(), d_sl, sizeof(uint64_t) * (h->world + 1),
+                                 cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    std::vector<uint64_t> slot_of(h->world + 1);
+    for (int r = 0; r <= h->world; ++r) {
+        API_CHECK(h, cudaMemcpyAsync(&slot_of[r], pk.slot_off + sl[r], sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, h->stream));
+    }
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    const uint64_t a = sl[h->rank], b = sl[h->rank + 1];
+    const uint64_t steps = (slot_of[h->rank + 1] - slot_of[h->rank]) - (b - a);
+    API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
+                                      cur_blk(h), cur_sb(h), (const uint64_t*)h->d_C.p, h->m,
+                                      steps, g, h->rank_ilp));
+    std::vector<uint64_t> bytes(h->world);
+    for (int r = 0; r < h->world; ++r) bytes[r] = 8 * (slot_of[r + 1] - slot_of[r]);
+    if (!h->allgather) return SETBWTE_E_STATE;
+    int rc = h->allgather(g, bytes.data(), h->world, (void*)h->stream, h->allgather_ctx);
+    if (rc != 0) return SETBWTE_E_STATE;
+    return SETBWTE_OK;
+}
+
+// One iteration of Algorithm 1 for the block of strings [j0, j1)
+// occupying slots [S0, S1) of the packed append.
+setbwte_status process_block(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1, uint64_t S0,
+                             uint64_t S1) {
+    const uint64_t n_suf = S1 - S0;
+    uint32_t* saf;
+    uint64_t *g, *pos;
+    uint8_t* bint;
+    API_CHECK(h, ensure(h->saf, n_suf, &saf));
+    API_CHECK(h, ensure(h->g, n_suf, &g));
+    API_CHECK(h, ensure(h->pos, n_suf, &pos));
+    API_CHECK(h, ensure(h->bint, n_suf, &bint));
+    // SA_int := ConstructSA(S_jk) -- fused sieving
+    API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, S0, (uint32_t)n_suf,
+                            saf, &h->sstats));
+    // g := ComputeRanks(S_jk, B_ext)
+    setbwte_status st = compute_ranks_for(h, pk, j0, j1, S0, n_suf, g);
+    if (st != SETBWTE_OK) return st;
+    // B_int := B(S_jk, SA_int) and g_sa / pos, fused
+    API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, S0, saf, g, (uint32_t)n_suf,
+                               pos, bint));
+    // B_ext := Insert(B_int, g_sa, B_ext)
+    const uint64_t n_out = h->n + n_suf;
+    const uint64_t nblk = (n_out >> 6) + 1;
+    const uint64_t nsb = (n_out >> kSbShift) + 1;
+    const int nxt = 1 - h->cur;
+    Blk* ob;
+    uint64_t *osb, *tot;
+    API_CHECK(h, ensure(h->blk[nxt], nblk, &ob));
+    API_CHECK(h, ensure(h->sb[nxt], nsb * 4, &osb));
+    API_CHECK(h, ensure(h->sb_tot, nsb * 4, &tot));
+    const uint64_t m_new = h->m + (j1 - j0);
+    API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, bint, n_suf, ob, osb,
+                               tot, m_new, (uint64_t*)h->d_C.p));
+    h->cur = nxt;
+    h->n = n_out;
+    h->m = m_new;
+    return SETBWTE_OK;
+}
+
+void build_stats(setbwte_t h) {
+    std::string s = "{";
+    char buf[512];
+    snprintf(buf, sizeof(buf),
+             "\"n\": %llu, \"m\": %llu, \"blocks\": %llu, \"bases\": %llu, \"strings\": %llu, "
+             "\"launches\": %llu, \"profile\": %d, \"block_suffixes\": %llu, ",
+             (unsigned long long)h->n, (unsigned long long)h->m,
+             (unsigned long long)h->last_blocks, (unsigned long long)h->last_bases,
+             (unsigned long long)h->last_m, (unsigned long long)h->prof.total_launches,
+             h->prof.on ? 1 : 0, (unsigned long long)h->M);
+    s += buf;
+    s += "\"sort\": {\"digit_passes\": " + std::to_string(h->sstats.digit_passes) +
+         ", \"active_per_pass\": [";
+    for (size_t i = 0; i < h->sstats.active_per_pass.size(); ++i) {
+        if (i) s += ", ";
+        s += std::to_string(h->sstats.active_per_pass[i]);
+    }
+    s += "]}, \"kernels\": {";
+    bool first = true;
+    for (auto& kv : h->prof.k) {
+        if (!first) s += ", ";
+        first = false;
+        snprintf(buf, sizeof(buf),
+                 "\"%s\": {\"launches\": %llu, \"ms\": %.6f, \"bytes\": %.1f, \"units\": %llu}",
+                 kv.first.c_str(), (unsigned long long)kv.second.launches, kv.second.ms,
+                 kv.second.bytes, (unsigned long long)kv.second.units);
+        s += buf;
+    }
+    s += "}}";
+    h->stats_json = s;
+}
+
+setbwte_status append_impl(setbwte_t h, const uint8_t* d_bytes, const uint64_t* d_off,
+                           uint64_t m) {
+    h->prof.reset();
+    h->sstats = SortStats();
+    h->last_blocks = 0;
+    h->last_bases = 0;
+    h->last_m = m;
+    if (m == 0) {
+        build_stats(h);
+        return SETBWTE_OK;
+    }
+    PackOut po;
+    setbwte_status st = pack_input(h, d_bytes, d_off, m, &po);
+    if (st != SETBWTE_OK) return st;
+    h->last_bases = po.n_bytes;
+    // partition into blocks of >= M suffixes
+    uint64_t* d_bounds;
+    API_CHECK(h, ensure(h->bounds, 2 * (m + 2) + 2, &d_bounds));
+    uint64_t* d_k = d_bounds + 2 * (m + 2);
+    API_CHECK(h, launch_partition(h->prof, h->stream, po.pk.slot_off, m, h->M, d_bounds, d_k));
+    uint64_t K = 0;
+    API_CHECK(h, cudaMemcpyAsync(&K, d_k, sizeof(K), cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    std::vector<uint64_t> bounds(2 * (K + 1));
+    API_CHECK(h, cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(uint64_t) * 2 * (K + 1),
+                                 cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    // validate every block before touching the index (all-or-nothing)
+    for (uint64_t b = 0; b < K; ++b) {
+        if (bounds[2 * b + 3] - bounds[2 * b + 1] >= (1ull << 31)) return SETBWTE_E_UNSUPPORTED;
+    }
+    h->last_blocks = K;
+    for (uint64_t b = 0; b < K; ++b) {
+        st = process_block(h, po.pk, bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1],
+                           bounds[2 * b + 3]);
+        if (st != SETBWTE_OK) {
+            if (b > 0) h->failed = true;  // a partially applied append cannot be rolled back
+            return st;
+        }
+    }
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    API_CHECK(h, h->prof.resolve());
+    build_stats(h);
+    return SETBWTE_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* setbwte_strerror(setbwte_status s) {
+    switch (s) {
+        case SETBWTE_OK: return "ok";
+        case SETBWTE_E_INVALID_ARG: return "invalid argument";
+        case SETBWTE_E_INVALID_CHAR: return "invalid character";
+        case SETBWTE_E_OUT_OF_RANGE: return "position out of range";
+        case SETBWTE_E_NOMEM: return "out of memory";
+        case SETBWTE_E_CUDA: return "CUDA error";
+        case SETBWTE_E_UNSUPPORTED: return "unsupported";
+        case SETBWTE_E_STATE: return "handle in failed state";
+    }
+    return "unknown status";
+}
+
+setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
+    if (!alphabet || !out) return SETBWTE_E_INVALID_ARG;
+    *out = nullptr;
+    const size_t sigma = strlen(alphabet);
+    if (sigma < 1) return SETBWTE_E_INVALID_ARG;
+    if (sigma > 4) return SETBWTE_E_UNSUPPORTED;
+    setbwte_t h = new (std::nothrow) setbwte_s();
+    if (!h) return SETBWTE_E_NOMEM;
+    memset(h->code_of, 0xFF, sizeof(h->code_of));
+    for (size_t i = 0; i < sigma; ++i) {
+        const unsigned char c = (unsigned char)alphabet[i];
+        if (c == '$' || h->code_of[toupper(c)] != 0xFF || h->code_of[tolower(c)] != 0xFF) {
+            delete h;
+            return SETBWTE_E_INVALID_ARG;
+        }
+        h->code_of[toupper(c)] = (uint8_t)i;
+        h->code_of[tolower(c)] = (uint8_t)i;
+        h->alpha[i] = (char)c;
+    }
+    h->sigma = (int)sigma;
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+    h->stream = h->own_stream;
+    uint8_t* dc = nullptr;
+    uint8_t* ds = nullptr;
+    uint64_t* dC = nullptr;
+    if (e == cudaSuccess) e = ensure(h->d_code_of, 256, &dc);
+    if (e == cudaSuccess) e = ensure(h->d_sym, 4, &ds);
+    if (e == cudaSuccess) e = ensure(h->d_C, 8, &dC);
+    uint8_t sym[4] = {0, 0, 0, 0};
+    for (size_t i = 0; i < sigma; ++i) sym[i] = (uint8_t)alphabet[i];
+    if (e == cudaSuccess) e = cudaMemcpy(dc, h->code_of, 256, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(ds, sym, 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(dC, 0, 8 * sizeof(uint64_t));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        setbwte_destroy(h);
+        return e == cudaErrorMemoryAllocation ? SETBWTE_E_NOMEM : SETBWTE_E_CUDA;
+    }
+    build_stats(h);
+    *out = h;
+    return SETBWTE_OK;
+}
+
+void setbwte_destroy(setbwte_t h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    DevBuf* bufs[] = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0], &h->sb[1],
+                      &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term,
+                      &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos,
+                      &h->bint, &h->outbuf, &h->sort.sa0, &h->sort.sa1, &h->sort.k0,
+                      &h->sort.k1, &h->sort.segs_a, &h->sort.segs_b, &h->sort.small_a,
+                      &h->sort.small_b, &h->sort.chunks, &h->sort.hist, &h->sort.ctr};
+    for (DevBuf* b : bufs) free_buf(*b);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    delete h;
+}
+
+setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,
+                                     const uint64_t* d_offsets, uint64_t m) {
+    API_ENTER(h);
+    if (m > 0 && !d_offsets) return SETBWTE_E_INVALID_ARG;
+    return append_impl(h, d_strings, d_offsets, m);
+}
+
+setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                              uint64_t m) {
+    API_ENTER(h);
+    if (m == 0) return append_impl(h, nullptr, nullptr, 0);
+    if (!offsets) return SETBWTE_E_INVALID_ARG;
+    const uint64_t nb = offsets[m];
+    if (nb > 0 && !strings) return SETBWTE_E_INVALID_ARG;
+    uint8_t* db;
+    uint64_t* dof;
+    API_CHECK(h, ensure(h->in_bytes, nb + 16, &db));
+    API_CHECK(h, ensure(h->in_off, m + 1, &dof));
+    if (nb) API_CHECK(h, cudaMemcpyAsync(db, strings, nb, cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                 h->stream));
+    return append_impl(h, db, dof, m);
+}
+
+setbwte_status setbwte_clear(setbwte_t h) {
+    API_ENTER(h);
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    h->n = 0;
+    h->m = 0;
+    h->cur = 0;
+    API_CHECK(h, cudaMemset(h->d_C.p, 0, 8 * sizeof(uint64_t)));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_size(setbwte_t h, uint64_t* n, uint64_t* m) {
+    if (!h) return SETBWTE_E_INVALID_ARG;
+    if (h->failed) return SETBWTE_E_STATE;
+    if (n) *n = h->n;
+    if (m) *m = h->m;
+    return SETBWTE_OK;
+}
+
+static setbwte_status bwt_impl(setbwte_t h, uint8_t* out, uint64_t cap, uint64_t* n, bool dev) {
+    API_ENTER(h);
+    if (!n) return SETBWTE_E_INVALID_ARG;
+    *n = h->n;
+    if (!out) return SETBWTE_OK;
+    if (cap < h->n) return SETBWTE_E_INVALID_ARG;
+    if (h->n == 0) return SETBWTE_OK;
+    uint8_t* target = out;
+    if (!dev) API_CHECK(h, ensure(h->outbuf, h->n, &target));
+    API_CHECK(h, launch_decode(h->prof, h->stream, cur_blk(h), h->n, (const uint8_t*)h->d_sym.p,
+                               target));
+    if (!dev)
+        API_CHECK(h, cudaMemcpyAsync(out, target, h->n, cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_bwt(setbwte_t h, uint8_t* out, uint64_t cap, uint64_t* n) {
+    return bwt_impl(h, out, cap, n, false);
+}
+
+setbwte_status setbwte_bwt_device(setbwte_t h, uint8_t* d_out, uint64_t cap, uint64_t* n) {
+    return bwt_impl(h, d_out, cap, n, true);
+}
+
+setbwte_status setbwte_rank(setbwte_t h, uint8_t c, uint64_t k, uint64_t* out) {
+    API_ENTER(h);
+    if (!out) return SETBWTE_E_INVALID_ARG;
+    if (c != '$' && h->code_of[c] == 0xFF) return SETBWTE_E_INVALID_ARG;
+    if (k > h->n) return SETBWTE_E_OUT_OF_RANGE;
+    if (h->n == 0) {
+        *out = 0;
+        return SETBWTE_OK;
+    }
+    uint64_t* d;
+    API_CHECK(h, ensure(h->small, 8, &d));
+    uint8_t* dc = reinterpret_cast<uint8_t*>(d + 2);
+    API_CHECK(h, cudaMemcpyAsync(d, &k, 8, cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, cudaMemcpyAsync(dc, &c, 1, cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_blk(h), cur_sb(h), h->n,
+                                   (const uint8_t*)h->d_code_of.p, dc, d, 1, d + 1));
+    uint64_t r = 0;
+    API_CHECK(h, cudaMemcpyAsync(&r, d + 1, 8, cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    *out = r;
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_rank_batch(setbwte_t h, const uint8_t* c_dev, const uint64_t* k_dev,
+                                  uint64_t q, uint64_t* out_dev) {
+    API_ENTER(h);
+    if (q == 0) return SETBWTE_OK;
+    if (!c_dev || !k_dev || !out_dev) return SETBWTE_E_INVALID_ARG;
+    if (h->n == 0) {
+        // only k = 0 is in range: rank 0; others are out of range
+        API_CHECK(h, cudaMemsetAsync(out_dev, 0xFF, q * sizeof(uint64_t), h->stream));
+        // a zero-sized index has no dictionary; answer k=0 queries on the host path
+        std::vector<uint64_t> k(q);
+        API_CHECK(h, cudaMemcpyAsync(k.data(), k_dev, q * 8, cudaMemcpyDeviceToHost, h->stream));
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+        std::vector<uint8_t> c(q);
+        API_CHECK(h, cudaMemcpy(c.data(), c_dev, q, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> r(q);
+        for (uint64_t i = 0; i < q; ++i)
+            r[i] = (k[i] == 0 && (c[i] == '$' || h->code_of[c[i]] != 0xFF)) ? 0 : ~0ull;
+        API_CHECK(h, cudaMemcpy(out_dev, r.data(), q * 8, cudaMemcpyHostToDevice));
+        return SETBWTE_OK;
+    }
+    API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_blk(h), cur_sb(h), h->n,
+                                   (const uint8_t*)h->d_code_of.p, c_dev, k_dev, q, out_dev));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                                    uint64_t m, uint32_t* sa_out, uint8_t* bint_out) {
+    API_ENTER(h);
+    if (m == 0) return SETBWTE_OK;
+    if (!offsets || (offsets[m] > 0 && !strings)) return SETBWTE_E_INVALID_ARG;
+    const uint64_t nb = offsets[m];
+    const uint64_t n_suf = nb + m;
+    if (n_suf >= (1ull << 31)) return SETBWTE_E_UNSUPPORTED;
+    uint8_t* db;
+    uint64_t* dof;
+    API_CHECK(h, ensure(h->in_bytes, nb + 16, &db));
+    API_CHECK(h, ensure(h->in_off, m + 1, &dof));
+    if (nb) API_CHECK(h, cudaMemcpyAsync(db, strings, nb, cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    PackOut po;
+    setbwte_status st = pack_input(h, db, dof, m, &po);
+    if (st != SETBWTE_OK) return st;
+    uint32_t* saf;
+    uint64_t* pos;
+    uint8_t *bint, *asc;
+    API_CHECK(h, ensure(h->saf, n_suf, &saf));
+    API_CHECK(h, ensure(h->pos, n_suf, &pos));
+    API_CHECK(h, ensure(h->bint, n_suf, &bint));
+    API_CHECK(h, ensure(h->outbuf, n_suf, &asc));
+    API_CHECK(h, sort_block(h->prof, h->stream, h->sort, po.pk.text, po.pk.term, 0,
+                            (uint32_t)n_suf, saf, nullptr));
+    API_CHECK(h, launch_gather(h->prof, h->stream, po.pk.text, po.pk.term, 0, saf, nullptr,
+                               (uint32_t)n_suf, pos, bint));
+    API_CHECK(h, launch_bint_ascii(h->prof, h->stream, bint, (uint32_t)n_suf,
+                                   (const uint8_t*)h->d_sym.p, asc));
+    if (sa_out)
+        API_CHECK(h, cudaMemcpyAsync(sa_out, saf, n_suf * 4, cudaMemcpyDeviceToHost, h->stream));
+    if (bint_out)
+        API_CHECK(h, cudaMemcpyAsync(bint_out, asc, n_suf, cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                                     uint64_t m, uint64_t* g_out) {
+    API_ENTER(h);
+    if (m == 0) return SETBWTE_OK;
+    if (!offsets || !g_out || (offsets[m] > 0 && !strings)) return SETBWTE_E_INVALID_ARG;
+    const uint64_t nb = offsets[m];
+    const uint64_t n_suf = nb + m;
+    uint8_t* db;
+    uint64_t* dof;
+    API_CHECK(h, ensure(h->in_bytes, nb + 16, &db));
+    API_CHECK(h, ensure(h->in_off, m + 1, &dof));
+    if (nb) API_CHECK(h, cudaMemcpyAsync(db, strings, nb, cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    PackOut po;
+    setbwte_status st = pack_input(h, db, dof, m, &po);
+    if (st != SETBWTE_OK) return st;
+    uint64_t* g;
+    API_CHECK(h, ensure(h->g, n_suf, &g));
+    st = compute_ranks_for(h, po.pk, 0, m, 0, n_suf, g);
+    if (st != SETBWTE_OK) return st;
+    API_CHECK(h, cudaMemcpyAsync(g_out, g, n_suf * 8, cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) {
+    if (!h || !key) return SETBWTE_E_INVALID_ARG;
+    if (h->failed) return SETBWTE_E_STATE;
+    if (!strcmp(key, "block_suffixes")) {
+        if (value < 1 || value > (1ull << 30)) return SETBWTE_E_INVALID_ARG;
+        h->M = value;
+    } else if (!strcmp(key, "profile")) {
+        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        h->prof.on = value == 1;
+    } else if (!strcmp(key, "rank_ilp")) {
+        if (value < 1 || value > 4) return SETBWTE_E_INVALID_ARG;
+        h->rank_ilp = (int)value;
+    } else {
+        return SETBWTE_E_INVALID_ARG;
+    }
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_set_stream(setbwte_t h, void* cuda_stream) {
+    API_ENTER(h);
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,
+                                     setbwte_allgather_fn allgather, void* ctx) {
+    if (!h) return SETBWTE_E_INVALID_ARG;
+    if (world < 1 || world > 1023 || rank < 0 || rank >= world) return SETBWTE_E_INVALID_ARG;
+    if (world > 1 && !allgather) return SETBWTE_E_INVALID_ARG;
+    h->rank = rank;
+    h->world = world;
+    h->allgather = allgather;
+    h->allgather_ctx = ctx;
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_stats(setbwte_t h, char* out, uint64_t cap, uint64_t* n) {
+    if (!h || !n) return SETBWTE_E_INVALID_ARG;
+    *n = h->stats_json.size() + 1;
+    if (!out) return SETBWTE_OK;
+    if (cap < *n) return SETBWTE_E_INVALID_ARG;
+    memcpy(out, h->stats_json.c_str(), *n);
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_last_error(setbwte_t h, uint64_t* pos, uint8_t* byte) {
+    if (!h) return SETBWTE_E_INVALID_ARG;
+    if (pos) *pos = h->err_pos;
+    if (byte) *byte = h->err_byte;
+    return SETBWTE_OK;
+}
+
+}  // extern "C"

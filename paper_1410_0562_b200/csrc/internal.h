@@ -1,0 +1,148 @@
+// internal.h -- host-side runtime pieces shared by the .cu files of
+// libsetbwte.so (not part of the C-ABI; see include/setbwte.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace setbwte {
+
+// Growth-only device buffer (contents are NOT preserved on growth).
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+cudaError_t ensure_bytes(DevBuf& b, size_t bytes);
+
+template <class T>
+inline cudaError_t ensure(DevBuf& b, size_t count, T** out) {
+    cudaError_t e = ensure_bytes(b, count * sizeof(T) + 64);
+    *out = static_cast<T*>(b.p);
+    return e;
+}
+
+// Per-kernel accounting: launch counts always; CUDA-event time when profiling.
+struct KStat {
+    uint64_t launches = 0;
+    double ms = 0.0;
+    double bytes = 0.0;   // algorithmic bytes
+    uint64_t units = 0;   // the unit the bytes are counted per (suffixes, LF steps, ...)
+};
+
+struct Profiler {
+    bool on = false;
+    struct Rec {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, KStat> k;
+    uint64_t total_launches = 0;
+
+    cudaEvent_t get_event();
+    void begin(const char* name, cudaStream_t s, double bytes, uint64_t units, cudaEvent_t* ev);
+    void end(const char* name, cudaStream_t s, cudaEvent_t a);
+    cudaError_t resolve();  // after a stream sync: accumulate event times
+    void add_bytes(const char* name, double bytes, uint64_t units) {
+        KStat& ks = k[name];
+        ks.bytes += bytes;
+        ks.units += units;
+    }
+    void reset();
+    ~Profiler();
+};
+
+// Launch helper: counts the launch and brackets it with events when profiling.
+#define SB_LAUNCH(prof, stream, name, bytes, units, ...)                    \
+    do {                                                                    \
+        cudaEvent_t _ev = nullptr;                                          \
+        (prof).begin(name, stream, (double)(bytes), (uint64_t)(units), &_ev); \
+        __VA_ARGS__;                                                        \
+        (prof).end(name, stream, _ev);                                      \
+    } while (0)
+
+#define SB_CHECK(expr)                             \
+    do {                                           \
+        cudaError_t _e = (expr);                   \
+        if (_e != cudaSuccess) return _e;          \
+    } while (0)
+
+inline unsigned grid_for(uint64_t n, unsigned threads, unsigned cap = 148u * 32u) {
+    uint64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// ---------------------------------------------------------------------------
+// Stage launchers (each file documents its kernels).
+// ---------------------------------------------------------------------------
+
+// pack.cu -- A0: validate + pack an append (Alg.1; layout in common.cuh).
+struct Packed {
+    uint32_t* text;       // 2-bit slot text
+    uint32_t* term;       // terminator bitmap
+    uint64_t* slot_off;   // m+1 slot offsets (slot_off[j] = offsets[j] + j)
+    uint64_t n_slots;
+};
+cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
+                        const uint64_t* d_off, uint64_t m, uint64_t n_bytes,
+                        const uint8_t* d_code_of, Packed pk, unsigned long long* d_err_pos,
+                        int* d_bad_offsets);
+// Greedy block partition (reading R8): blocks end at the first
+// string boundary where the block holds >= M suffixes.  Writes K+1 pairs
+// (string index, slot offset) into d_bounds and K into *d_k.
+cudaError_t launch_partition(Profiler& prof, cudaStream_t s, const uint64_t* d_slot_off,
+                             uint64_t m, uint64_t M, uint64_t* d_bounds, uint64_t* d_k);
+
+// Split strings [j0, j1) into `parts` contiguous slices balanced by suffix
+// count: out[r] = first string of slice r, out[parts] = j1.
+cudaError_t launch_slices(Profiler& prof, cudaStream_t s, const uint64_t* d_slot_off,
+                          uint64_t j0, uint64_t j1, int parts, uint64_t* d_out);
+
+// sort.cu -- A1 ConstructSA (Sec.3).
+struct SortScratch {
+    DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr;
+};
+struct SortStats {
+    uint64_t digit_passes = 0;
+    uint64_t rounds = 0;
+    std::vector<uint64_t> active_per_pass;  // elements entering each digit pass
+};
+cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
+                       const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
+                       uint32_t* d_sa_final, SortStats* st);
+
+// ranks.cu -- A3 ComputeRanks (Lemma 1, Alg.2) and the
+// fused A2/A4 extraction + gather (Alg.1).
+cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
+                                 const uint64_t* slot_off, uint64_t j0, uint64_t j1,
+                                 uint64_t slot_base, const Blk* blk, const uint64_t* sb,
+                                 const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps,
+                                 uint64_t* g, int ilp);
+cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
+                          const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
+                          const uint64_t* g, uint32_t n_suf, uint64_t* pos, uint8_t* bint);
+
+// insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
+cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+                          const uint64_t* pos, const uint8_t* bint, uint64_t n_ins,
+                          Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot, uint64_t m_new,
+                          uint64_t* d_C);
+cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+                              uint64_t n, const uint8_t* code_of, const uint8_t* c,
+                              const uint64_t* k, uint64_t q, uint64_t* out);
+cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Blk* blk, uint64_t n,
+                          const uint8_t* sym_ascii, uint8_t* out);
+// Debug/export: SA + B_int ASCII of a sorted block.
+cudaError_t launch_bint_ascii(Profiler& prof, cudaStream_t s, const uint8_t* bint,
+                              uint32_t n_suf, const uint8_t* sym_ascii, uint8_t* out);
+
+}  // namespace setbwte

@@ -1,0 +1,91 @@
+// ranks.cu -- A3 ComputeRanks and the fused A2 + A4 step.
+//
+// ComputeRanks (Lemma 1, Algorithm 2): for every string
+// P_j of the block, independently,
+//     i := m_ext                      (reading R1; the paper prints n_ext)
+//     g[offs[j] + |P_j|] := i
+//     for k = |P_j|-1 .. 0:  c := P_j[k];  i := C[c] + rank(c, i, B_ext);
+//                            g[offs[j] + k] := i
+// One thread walks one string backwards; each LF step is one 32-byte Blk
+// sector plus one superblock counter (common.cuh dict_rank).
+//
+// Gather (Alg.1), fused: for each SA position i,
+//     s = SA_int[i];  B_int[i] = P[k-1] or '$';  pos[i] = g[s] + i
+// where pos[i] = g_sa[i] + i is the final position of B_int[i] in the new
+// B_ext (reading R4).
+#include "internal.h"
+
+namespace setbwte {
+
+__global__ void __launch_bounds__(256) compute_ranks_kernel(
+    const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
+    uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+    const uint64_t* __restrict__ Cd, uint64_t m_ext, uint64_t* __restrict__ g) {
+    const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
+    for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s0 = slot_off[j];
+        const uint64_t e = slot_off[j + 1] - 1;  // terminator slot
+        uint64_t i = m_ext;
+        g[e - slot_base] = i;
+        uint64_t p = e;
+        uint64_t wi = ~0ull;
+        uint32_t word = 0;
+        while (p > s0) {
+            --p;
+            if ((p >> 4) != wi) {
+                wi = p >> 4;
+                word = __ldg(text + wi);
+            }
+            const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
+            const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
+            i = Cc + dict_rank(blk, sb, c, i);
+            g[p - slot_base] = i;
+        }
+    }
+}
+
+cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
+                                 const uint64_t* slot_off, uint64_t j0, uint64_t j1,
+                                 uint64_t slot_base, const Blk* blk, const uint64_t* sb,
+                                 const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps,
+                                 uint64_t* g, int ilp) {
+    (void)ilp;
+    if (j1 <= j0) return cudaSuccess;
+    // algorithmic bytes per LF step (= base): one 32 B Blk sector + 8 B g write
+    // + 0.25 B packed symbol; per string: 16 B slot offsets + 8 B terminator g
+    // (DESIGN.md "Rooflines").  Units = LF steps.
+    const uint64_t nstr = j1 - j0;
+    SB_LAUNCH(prof, s, "compute_ranks", 40.25 * (double)n_steps + 24.0 * (double)nstr, n_steps,
+              compute_ranks_kernel<<<grid_for(nstr, 256, 1u << 20), 256, 0, s>>>(
+                  text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, g));
+    return cudaGetLastError();
+}
+
+__global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
+                              uint64_t slot_base, const uint32_t* __restrict__ sa,
+                              const uint64_t* __restrict__ g, uint32_t n_suf,
+                              uint64_t* __restrict__ pos, uint8_t* __restrict__ bint) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_suf;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t sl = sa[i];
+        const uint64_t p = slot_base + sl;
+        pos[i] = (g ? g[sl] : 0ull) + i;
+        uint8_t b;
+        if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
+        else b = (uint8_t)text_sym(text, p - 1);
+        bint[i] = b;
+    }
+}
+
+cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
+                          const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
+                          const uint64_t* g, uint32_t n_suf, uint64_t* pos, uint8_t* bint) {
+    // bytes per suffix: 4 (SA) + 8 (g) + 8 (pos) + 1 (B_int) + 0.375 (symbol + term bit)
+    SB_LAUNCH(prof, s, "gather", 21.375 * n_suf, n_suf,
+              gather_kernel<<<grid_for(n_suf, 256, 148u * 64u), 256, 0, s>>>(
+                  text, term, slot_base, sa, g, n_suf, pos, bint));
+    return cudaGetLastError();
+}
+
+}  // namespace setbwte

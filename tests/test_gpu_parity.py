@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+element by element, on seeded synthetic inputs.  Integer work => bit-exact."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import brute
+
+pytestmark = pytest.mark.gpu
+
+A = "ACGT"
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SPEC = json.load(open(os.path.join(GOLD, "spec_worked_examples.json")))
+TWO = json.load(open(os.path.join(GOLD, "two_block_example.json")))
+
+
+@pytest.fixture(scope="module")
+def SetBWTE():
+    from paper_1410_0562_b200 import SetBWTE
+    return SetBWTE
+
+
+def build(SetBWTE, data, offsets, M=None, splits=None, alphabet=A):
+    idx = SetBWTE(alphabet, block_suffixes=M)
+    m = len(offsets) - 1
+    cuts = [0] + list(splits or []) + [m]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        o = np.asarray(offsets[a:b + 1], dtype=np.uint64)
+        d = data[int(o[0]):int(o[-1])]
+        idx.append(d, o - o[0])
+    return idx
+
+
+# --- worked examples ----------------------------------------------------------
+
+def test_golden_bwt(SetBWTE):
+    for case in SPEC["bwt"]:
+        idx = SetBWTE(A)
+        for blk in case.get("blocks", [case["strings"]]):
+            idx.append_strings(blk)
+        assert idx.bwt().decode() == case["bwt"], case["cite"]
+
+
+def test_golden_two_block(SetBWTE):
+    idx = SetBWTE(A)
+    for blk in TWO["blocks"]:
+        d, o = synth.from_strings(blk["strings"])
+        sa, bint = idx.construct_sa(d, o)
+        assert list(sa) == blk["sa_slots"]
+        assert bint.decode() == blk["bint"]
+        assert list(idx.compute_ranks(d, o)) == blk["g"]
+        idx.append(d, o)
+        assert idx.bwt().decode() == blk["b_ext_after"]
+    B = idx.bwt()
+    assert B.decode() == TWO["one_shot_bwt"]
+
+
+def test_golden_stage_examples(SetBWTE):
+    idx = SetBWTE(A)
+    for case in SPEC["block_sa"]:
+        d, o = synth.from_strings(case["strings"])
+        sa, _ = idx.construct_sa(d, o)
+        slot = {p: s for s, p in enumerate(brute.slot_jk(case["strings"]))}
+        assert list(sa) == [slot[tuple(p)] for p in case["sa_jk"]], case["cite"]
+    for case in SPEC["compute_ranks"]:
+        idx2 = SetBWTE(A)
+        if case["ext"]:
+            idx2.append_strings(case["ext"])
+        d, o = synth.from_strings(case["block"])
+        assert list(idx2.compute_ranks(d, o)) == case["g"], case["cite"]
+    for case in SPEC["rank"]:
+        idx3 = SetBWTE(A)
+        # B of the worked example is the BWT of a set; rebuild it from its strings
+        strings = {"C$A": ["AC"], "CG$A$": ["AC", "G"]}[case["B"]]
+        idx3.append_strings(strings)
+        assert idx3.bwt().decode() == case["B"]
+        assert idx3.rank(case["c"], case["k"]) == case["rank"], case["cite"]
+
+
+# --- random small sets: every block size, every append split ------------------
+
+@pytest.mark.parametrize("seed", range(120))
+def test_random_sets_vs_oracle(SetBWTE, seed):
+    alpha = ["ACGT", "AC", "A", "ACG", "GT"][seed % 5]
+    d, o = synth.random_set(seed, max_m=64, max_len=50, alphabet=alpha)
+    want = oracle.bwt(A, d, o)
+    n = len(want)
+    m = len(o) - 1
+    for M in (1, 40, 400, n + 1):
+        assert build(SetBWTE, d, o, M=M).bwt() == want, ("M", M)
+    rng = np.random.default_rng(seed)
+    splits = sorted(set(rng.integers(0, m + 1, size=3).tolist()))
+    assert build(SetBWTE, d, o, M=int(rng.integers(1, 200)), splits=splits).bwt() == want
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_block_sa_and_ranks(SetBWTE, seed):
+    d, o = synth.random_set(100 + seed, max_m=64, max_len=50,
+                            alphabet=["ACGT", "AC"][seed % 2])
+    strings = synth.to_strings(d, o)
+    idx = SetBWTE(A)
+    sa, bint = idx.construct_sa(d, o)
+    want_sa = oracle.block_sa(A, d, o)
+    assert np.array_equal(sa.astype(np.uint64), want_sa)
+    assert bint == oracle.block_bint(A, d, o, want_sa)
+    cut = len(strings) // 2
+    ed, eo = synth.from_strings(strings[:cut])
+    bd, bo = synth.from_strings(strings[cut:])
+    idx.append(ed, eo)
+    g = idx.compute_ranks(bd, bo)
+    assert np.array_equal(g, oracle.compute_ranks(A, d, o, m_ext=cut))
+
+
+# --- c1 (BASELINE configs[0]): 1000 x 100 bp, K = 4, and sweeps ----------------
+
+@pytest.fixture(scope="module")
+def c1():
+    d, o = synth.uniform(1000, 100, seed=1)
+    return d, o, oracle.bwt(A, d, o, threads=None)
+
+
+@pytest.mark.parametrize("M", [25250, 101000, 50500, 101])
+def test_c1_block_sizes(SetBWTE, c1, M):
+    d, o, want = c1
+    idx = build(SetBWTE, d, o, M=M)
+    assert idx.bwt() == want
+    assert idx.stats()["blocks"] == -(-101000 // M)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_c1_random_append_splits(SetBWTE, c1, seed):
+    d, o, want = c1
+    rng = np.random.default_rng(seed)
+    splits = sorted(set(rng.integers(1, 1000, size=5).tolist()))
+    assert build(SetBWTE, d, o, M=int(rng.integers(2000, 40000)), splits=splits).bwt() == want
+
+
+def test_c1_rank_every_symbol(SetBWTE, c1):
+    d, o, want = c1
+    idx = build(SetBWTE, d, o, M=25250)
+    n = len(want)
+    arr = np.frombuffer(want, dtype=np.uint8)
+    ks = [0, 1, 63, 64, 65, 4095, 65535, 65536, 65537, n - 1, n] + \
+        list(np.random.default_rng(3).integers(0, n + 1, size=40))
+    for c in "$ACGT":
+        cum = np.concatenate([[0], np.cumsum(arr == ord(c))])
+        for k in ks:
+            assert idx.rank(c, int(k)) == int(cum[k]), (c, k)
+    # batched on the device
+    import torch
+    cq = torch.tensor([ord(c) for c in "$ACGT" for _ in ks], dtype=torch.uint8, device="cuda")
+    kq = torch.tensor([int(k) for _ in "$ACGT" for k in ks], dtype=torch.int64, device="cuda")
+    out = torch.empty_like(kq)
+    idx.rank_batch(cq, kq, out)
+    ref = [oracle.rank(want, c, int(k)) for c in "$ACGT" for k in ks]
+    assert out.cpu().tolist() == ref
+
+
+# --- sorts that exercise the digit passes and deep LCPs ------------------------
+
+@pytest.mark.parametrize("kind", ["uniform", "genome", "all_A", "AC_repeat", "staircase",
+                                  "many_empty", "long"])
+def test_block_sa_structured(SetBWTE, kind):
+    if kind == "uniform":
+        d, o = synth.uniform(3000, 100, seed=5)
+    elif kind == "genome":
+        d, o = synth.genome_sampled(4000, 100, 20000, seed=5)   # ~20x coverage: deep LCPs
+    elif kind == "long":
+        d, o = synth.uniform_var(30, 1000, 10000, seed=5)
+    else:
+        d, o = synth.adversarial(kind, m=150, L=100)
+    idx = SetBWTE(A)
+    sa, bint = idx.construct_sa(d, o)
+    want = oracle.block_sa(A, d, o, threads=None)
+    assert np.array_equal(sa.astype(np.uint64), want)
+    assert bint == oracle.block_bint(A, d, o, want)
+
+
+@pytest.mark.parametrize("kind", ["genome", "all_A", "long", "mixed_empty"])
+def test_build_structured(SetBWTE, kind):
+    if kind == "genome":
+        d, o = synth.genome_sampled(5000, 100, 30000, seed=9)
+        M = 100000
+    elif kind == "all_A":
+        d, o = synth.adversarial("all_A", m=400, L=100)
+        M = 10000
+    elif kind == "long":
+        d, o = synth.uniform_var(60, 1000, 10000, seed=9)
+        M = 50000
+    else:
+        d, o = synth.adversarial("many_empty", m=3000)
+        M = 777
+    want = oracle.bwt(A, d, o, threads=None)
+    assert build(SetBWTE, d, o, M=M).bwt() == want
+
+
+# --- edge cases ----------------------------------------------------------------
+
+def test_edge_cases(SetBWTE):
+    from paper_1410_0562_b200 import SetBWTEError
+    idx = SetBWTE(A)
+    assert idx.size() == (0, 0) and idx.bwt() == b""
+    assert idx.rank("A", 0) == 0
+    with pytest.raises(SetBWTEError) as e:
+        idx.rank("A", 1)
+    assert e.value.name == "E_OUT_OF_RANGE"
+    idx.append_strings([""])
+    assert idx.bwt() == b"$"
+    idx.append_strings([])                      # no-op
+    assert idx.size() == (1, 1)
+    # invalid character: error with position, index unchanged
+    with pytest.raises(SetBWTEError) as e:
+        idx.append_strings(["ACGT", "ACXGT"])
+    assert e.value.name == "E_INVALID_CHAR"
+    assert idx.last_error() == (6, ord("X"))
+    assert idx.bwt() == b"$"
+    # lowercase accepted (reading R10)
+    idx.append_strings(["acgt"])
+    assert idx.bwt() == oracle.bwt(A, *synth.from_strings(["", "ACGT"]))
+    with pytest.raises(SetBWTEError):
+        idx.rank("N", 1)
+    # bad offsets
+    with pytest.raises(SetBWTEError) as e:
+        idx.append(np.frombuffer(b"ACGT", np.uint8), np.array([0, 3, 2, 4], np.uint64))
+    assert e.value.name == "E_INVALID_ARG"
+    # clear
+    idx.clear()
+    assert idx.size() == (0, 0)
+    idx.append_strings(["AC", "G"])
+    assert idx.bwt() == b"CG$A$"
+
+
+def test_small_alphabets(SetBWTE):
+    for alpha in ["AC", "A", "GT", "ACG"]:
+        d, o = synth.random_set(77, max_m=40, max_len=40, alphabet=alpha)
+        idx = SetBWTE(alpha, block_suffixes=200)
+        idx.append(d, o)
+        # oracle in the same alphabet
+        assert idx.bwt() == oracle.bwt(alpha, d, o)
+
+
+def test_append_device_matches_host(SetBWTE):
+    import torch
+    d, o = synth.uniform(5000, 100, seed=11)
+    a = SetBWTE(A, block_suffixes=1 << 17)
+    a.append(d, o)
+    b = SetBWTE(A, block_suffixes=1 << 17)
+    b.append_device(torch.from_numpy(d).cuda(), torch.from_numpy(o.astype(np.int64)).cuda())
+    assert a.bwt() == b.bwt()
+    out = torch.empty(a.size()[0], dtype=torch.uint8, device="cuda")
+    a.bwt_device(out)
+    assert bytes(out.cpu().numpy()) == a.bwt()
+
+
+# --- scale: c2-shaped sets (many tiles, ragged tails) ---------------------------
+
+def test_scaled_c2_vs_oracle(SetBWTE):
+    d, o = synth.uniform(100_000, 100, seed=1)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = build(SetBWTE, d, o, M=1 << 20)
+    assert idx.bwt() == want
+
+
+def test_long_reads_vs_oracle(SetBWTE):
+    d, o = synth.uniform_var(2000, 1000, 10000, seed=4)     # c4-shaped lengths
+    want = oracle.bwt(A, d, o, threads=None)
+    assert build(SetBWTE, d, o, M=1 << 21).bwt() == want
+
+
+@pytest.mark.slow
+def test_c2_full_vs_oracle(SetBWTE):
+    """BASELINE configs[1] at full size, in the configuration bench.py times."""
+    d, o = synth.uniform(1_000_000, 100, seed=1)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = build(SetBWTE, d, o, M=1 << 24)
+    assert idx.stats()["blocks"] == 7
+    assert idx.bwt() == want
