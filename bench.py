@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py -- set-bwte BWT build throughput on B200 (BASELINE.json metric).
+
+One STEP = one whole pass of the hot path over one batch: clear the index and
+append the workload's reads (Algorithm 1 over all its blocks: pack, ConstructSA,
+B_int, ComputeRanks, g->g_sa gather, Insert + dictionary rebuild), inputs
+already resident in HBM.  Default workload = BASELINE configs[1] ("c2"):
+1M uniform reads x 100 bp, blocks of M = 2^24 suffixes (K = 7).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU, NCCL): every rank builds the same index;
+ComputeRanks is split by string across ranks and g is all-gathered
+ -> strong scaling of one build.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BWT build Mbases/s at 1/2/4/8 B200; ComputeRanks queries/s; % HBM roofline"
+UNIT = "Mbases/s"
+
+WORKLOADS = {
+    # name: (description, generator kwargs, block_suffixes)
+    "c1": ("c1: 1,000 uniform reads x 100 bp, K=4 blocks", dict(m=1000, L=100), 25250),
+    "c2": ("c2: 1M uniform reads x 100 bp (100 Mbp), M=2^24-suffix blocks",
+           dict(m=1_000_000, L=100), 1 << 24),
+    "c3": ("c3: 20M uniform reads x 100 bp (2 Gbp), M=2^27-suffix blocks",
+           dict(m=20_000_000, L=100), 1 << 27),
+    "c4": ("c4: 1M uniform reads of length U[1000,10000] (~5.5 Gbp), M=2^30-suffix blocks",
+           dict(m=1_000_000, lo=1000, hi=10000), 1 << 30),
+}
+
+# which library kernels make up which stage of Table 2's taxonomy
+STAGE_OF = {
+    "pack": "pack", "slot_offsets": "pack", "partition": "pack",
+    "sort_init": "sort", "sort_tiny": "sort", "sort_small": "sort", "sort_medium": "sort",
+    "sort_warp": "sort", "sort_ctl": "sort",
+    "sort_chunkify": "sort", "digit_hist": "sort", "digit_scan": "sort", "digit_scatter": "sort",
+    "compute_ranks": "rank", "slices": "rank", "gather": "gather", "insert": "insert",
+    "sb_scan": "insert",
+}
+
+
+def gen(workload: str, seed: int = 1):
+    import synth
+    _, kw, _ = WORKLOADS[workload]
+    if "L" in kw:
+        return synth.uniform(kw["m"], kw["L"], seed=seed)
+    return synth.uniform_var(kw["m"], kw["lo"], kw["hi"], seed=seed)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle (the slow CPU program) on the box's host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    import oracle
+    wl = args.workload
+    data, offsets = gen(wl)
+    m_sample = min(args.ref_sample_reads, len(offsets) - 1)
+    o = offsets[: m_sample + 1]
+    d = data[: int(o[-1])]
+    bases = float(o[-1])
+    cores = cpu_count()
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.bwt("ACGT", d, o, threads=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    value = bases * len(times) / t / 1e6
+    sample = "first %d reads (%d bases) of %s per step" % (m_sample, int(bases), wl)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * t / len(times), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[wl][0], "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores,
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1410_0562_b200 import SetBWTE
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = args.workload
+    desc, _, M = WORKLOADS[wl]
+    if args.block_suffixes:
+        M = args.block_suffixes
+    data, offsets = gen(wl)
+    m = len(offsets) - 1
+    bases = int(offsets[-1])
+    d_data = torch.from_numpy(data).to(dev)
+    d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    idx = SetBWTE("ACGT", block_suffixes=M, profile=True)
+    idx.set_stream(stream)
+    if world > 1:
+        from paper_1410_0562_b200.dist import make_allgather
+        idx.set_partition(rank, world, make_allgather())
+
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        idx.clear()
+        idx.append_device(d_data, d_off, m)
+
+    for _ in range(args.warmup):
+        l2_flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+
+    kern = {}
+    launches = 0
+    blocks = None
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    times = []
+    for _ in range(args.steps):
+        l2_flush.zero_()                     # flush L2 between timed iterations (untimed)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        st = idx.stats()
+        launches += st["launches"]
+        blocks = st["blocks"]
+        for k, v in st["kernels"].items():
+            a = kern.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0, "units": 0})
+            for f in a:
+                a[f] += v[f]
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    t_local = sum(times) / 1000.0
+    if world > 1:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    else:
+        t = t_local
+    value = bases * args.steps / t / 1e6
+
+    # ---- end to end through the public API: pinned host in, BWT back out ----
+    pin_data = torch.from_numpy(data).pin_memory()
+    pin_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
+    n_total = bases + m
+    pin_out = torch.empty(n_total, dtype=torch.uint8).pin_memory()
+    np_data = pin_data.numpy()
+    np_off = pin_off.numpy().view(np.uint64)
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        l2_flush.zero_()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        idx.clear()
+        idx.append(np_data, np_off)          # H2D of the step's inputs inside
+        idx.bwt(pin_out)                      # D2H of the step's result
+        e1.record(stream)
+        e1.synchronize()
+        if i >= args.warmup:
+            e2e_times.append(e0.elapsed_time(e1))
+    te = sum(e2e_times) / 1000.0
+    if world > 1:
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    e2e_value = bases * len(e2e_times) / te / 1e6
+    h2d = data.nbytes + offsets.nbytes
+    d2h = n_total
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = load_peaks()
+    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    dname, dk = dom
+    per_launch_bytes = dk["bytes"] / max(dk["launches"], 1)
+    avg_ms = dk["ms"] / max(dk["launches"], 1)
+    achieved = per_launch_bytes / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get(dname)
+    roof = {"kernel": dname, "bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
+            "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+            "bytes_per_launch": per_launch_bytes, "avg_launch_ms": round(avg_ms, 5),
+            "share_of_step": round(dk["ms"] / (t_local * 1000.0), 4), "peak_source": peak_src}
+    stages = {}
+    for k, v in kern.items():
+        sname = STAGE_OF.get(k, "other")
+        stages[sname] = stages.get(sname, 0.0) + v["ms"] / args.steps
+    cr = kern.get("compute_ranks")
+    qps = (cr["units"] / (cr["ms"] / 1000.0)) if cr and cr["ms"] > 0 else None
+
+    # ---- oracle beside it (rank 0, N = 1 only), + parity of this run ----
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        cores = cpu_count()
+        m_s = min(args.cpu_sample_reads, m)
+        o_s = offsets[: m_s + 1]
+        d_s = data[: int(o_s[-1])]
+        t0 = time.perf_counter()
+        want = oracle.bwt("ACGT", d_s, o_s, threads=cores)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(float(o_s[-1]) / dt / 1e6, 3), "unit": UNIT, "cores": cores,
+               "kind": "oracle",
+               "sample": "first %d reads (%d bases) of %s, one build" % (m_s, int(o_s[-1]), wl)}
+        if m_s == m:
+            parity = "bit-exact" if bytes(pin_out.numpy()[:n_total]) == want else "MISMATCH"
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000.0 * t / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": desc, "reads": m, "bases": bases, "block_suffixes": M,
+                       "blocks": blocks, "parallelism": "dp%d (ComputeRanks split by string)" % world,
+                       "l2": "flushed between timed steps (256 MiB write, untimed)"},
+            "compute_ranks_queries_per_s": qps, "stage_ms_per_step": stages,
+            "kernel_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in
+                                   sorted(kern.items(), key=lambda kv: -kv[1]["ms"])},
+            "roofline": roof, "cpu_baseline": cpu, "parity_vs_oracle": parity,
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    idx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--block-suffixes", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-reads", type=int, default=1_000_000)
+    ap.add_argument("--ref-sample-reads", type=int, default=100_000)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

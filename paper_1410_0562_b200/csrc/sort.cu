@@ -4,41 +4,51 @@
 // Suffixes are "long integer keys made of multiple 32-bit words": key
 // word d of the suffix at slot p is suffix_key(p, d) (common.cuh, reading R6).
 // The sort refines SEGMENTS -- ranges of the final suffix array whose members
-// agree on every key bit examined so far and are stored in slot order:
+// agree on every key bit examined so far and are stored in slot order -- by
+// size class:
 //
-// * a LARGE segment (> kCapB members) takes one stable 8-bit digit pass
-//   (histogram -> per-segment scan -> stable scatter) and splits into
-//   children;
-// * a SMALL segment (<= kCapB) is finished by one CTA in shared memory: a
-//   bitonic sort of (run, key word, index) composites, repeated on the
-//   still-tied runs with the next key word until none is left;
-// * a bucket is SIEVED -- written to its final place and dropped from the
-//   working set -- when it has one member, or when its members end inside the
-//   key window with equal keys (identical suffixes, already in slot order =
-//   string-index order).  This is the "sieves unique keys at each
-//   iteration" of P:89 (reading R7).
+//   LARGE  (> 4096)   one stable 8-bit MSD digit pass over all large segments:
+//                     per-chunk histogram -> per-segment scan -> stable
+//                     scatter staged through shared memory (coalesced runs);
+//   SMALL  (33..512)  one warp per segment: stable LSD radix sort of the
+//                     still-unknown key bits held in registers, exchanged
+//                     through a per-warp shared-memory buffer (no CTA barriers);
+//   MEDIUM (513..4096) one CTA per segment: the same LSD radix sort with the
+//                     tile in shared memory;
+//   TINY   (2..32)    one warp per segment: register bitonic sort across lanes.
 //
-// Ties are only ever broken by slot order, which the stable passes and the
-// index field of the composites preserve, so the result is the unique SA of
-// the block (reading R15).
+// After a word is sorted, ties (equal key words whose 14 symbols are all real)
+// move to the next word: runs of <= 32 are finished by one warp in registers,
+// longer runs become new segments of the next round.  A bucket is SIEVED --
+// written to its final place and dropped from the working set -- when it has
+// one member, or when its members end inside the key window with equal keys
+// (identical suffixes, already in slot order = string-index order).
+// This is the "sieves unique keys at each iteration" of P:89 (reading R7).
+//
+// Ties are only ever broken by slot order, which every pass preserves
+// (stable), so the result is the unique SA of the block (reading R15).
 #include <algorithm>
 
 #include "internal.h"
 
 namespace setbwte {
+namespace sortk {
 
-namespace {
-
-constexpr uint32_t kCapA = 256;    // small class A: <= 256 members, 128 threads
-constexpr uint32_t kNtA = 128;
-constexpr uint32_t kCapB = 4096;   // small class B: <= 4096 members, 512 threads
-constexpr uint32_t kNtB = 512;
+constexpr uint32_t kTiny = 32;
+constexpr uint32_t kCapS = 512;    // SMALL: one warp per segment, 16 items per lane
+constexpr int kIpl = kCapS / 32;
+constexpr int kWarpCta = 8;
+constexpr uint32_t kCapM = 4096;   // MEDIUM: 512 threads, 8 items each
+constexpr uint32_t kNtM = 512;
 constexpr uint32_t kChunk = 16384; // target chunk of a digit pass
 constexpr uint32_t kMaxChunks = 1024;
-constexpr int kDigNt = 256;        // digit-pass CTA
+constexpr int kDigNt = 512;        // digit-pass CTA
 constexpr int kDigIpt = 8;
 constexpr int kDigTile = kDigNt * kDigIpt;
-constexpr int kDigWarps = kDigNt / 32;
+
+enum { TINY = 0, SMALL = 1, MEDIUM = 2, LARGE = 3, NCLASS = 4 };
+// misc counters
+enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_N };
 
 struct Seg {
     uint32_t start, len, word, meta;  // meta: shift | buf << 8 | keys_valid << 9
@@ -49,8 +59,18 @@ struct SegX {
 struct Chunk {
     uint32_t seg, begin, end, pad;
 };
-// device counters
-enum { C_LARGE_IN = 0, C_LARGE_OUT, C_SMALL_A, C_SMALL_B, C_CHUNKS, C_ACTIVE, C_N };
+struct Lists {
+    Seg* seg[NCLASS];
+    uint32_t* cnt;  // NCLASS counters
+};
+struct Bufs {
+    uint32_t* sa[2];
+    uint32_t* key[2];
+    uint32_t* saf;
+    const uint32_t* text;
+    const uint32_t* term;
+    uint64_t base;
+};
 
 __device__ __forceinline__ uint32_t meta_shift(uint32_t m) { return m & 0xFF; }
 __device__ __forceinline__ uint32_t meta_buf(uint32_t m) { return (m >> 8) & 1; }
@@ -58,51 +78,169 @@ __device__ __forceinline__ uint32_t meta_kv(uint32_t m) { return (m >> 9) & 1; }
 __device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint32_t kv) {
     return shift | (buf << 8) | (kv << 9);
 }
+__device__ __forceinline__ int class_of(uint32_t len) {
+    return len <= kTiny ? TINY : len <= kCapS ? SMALL : len <= kCapM ? MEDIUM : LARGE;
+}
+__device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
+    const int k = class_of(c.len);
+    out.seg[k][atomicAdd(out.cnt + k, 1u)] = c;
+}
 
-__device__ __forceinline__ void emit_child(const Seg& c, Seg* large_out, Seg* small_a,
-                                           Seg* small_b, uint32_t* ctr) {
-    if (c.len <= kCapA) {
-        small_a[atomicAdd(ctr + C_SMALL_A, 1u)] = c;
-    } else if (c.len <= kCapB) {
-        small_b[atomicAdd(ctr + C_SMALL_B, 1u)] = c;
-    } else {
-        large_out[atomicAdd(ctr + C_LARGE_OUT, 1u)] = c;
+// ---------------------------------------------------------------------------
+// Warp-level finish of a run of L <= 32 suffixes (lanes 0..L-1 hold the slots
+// in slot order).  Sorts by key word `word`, then word+1, ... until no ties
+// remain, entirely in registers.  Returns the lane's slot in final order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint32_t word,
+                                                uint32_t key0, bool have_key, const Bufs& B) {
+    const uint32_t lane = threadIdx.x & 31;
+    const bool valid = lane < L;
+    bool active = valid;
+    uint32_t group = 0;
+    for (;;) {
+        uint32_t key = 0;
+        if (active) key = have_key ? key0 : suffix_key(B.text, B.term, B.base + slot, word);
+        have_key = false;
+        unsigned long long comp;
+        if (!valid) comp = ~0ull;
+        else if (active) comp = ((unsigned long long)group << 37) | ((unsigned long long)key << 5) | lane;
+        else comp = ((unsigned long long)lane << 37) | lane;
+#pragma unroll
+        for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, comp, j);
+                const bool up = (lane & k) == 0;
+                const bool lower = (lane & j) == 0;
+                const unsigned long long mn = comp < other ? comp : other;
+                const unsigned long long mx = comp < other ? other : comp;
+                comp = (lower == up) ? mn : mx;
+            }
+        }
+        slot = __shfl_sync(0xFFFFFFFFu, slot, (uint32_t)(comp & 31));
+        const unsigned long long hi = comp >> 5;
+        const unsigned long long prv = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
+        const unsigned long long nxt = __shfl_down_sync(0xFFFFFFFFu, hi, 1);
+        const bool eqp = valid && lane > 0 && prv == hi;
+        const bool eqn = valid && lane + 1 < L && nxt == hi;
+        const uint32_t k32 = (uint32_t)(hi & 0xFFFFFFFFull);
+        active = (eqp || eqn) && ((k32 & 15u) == (uint32_t)kKeySyms);
+        const uint32_t starts = __ballot_sync(0xFFFFFFFFu, valid && !eqp);
+        group = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
+        if (!__any_sync(0xFFFFFFFFu, active)) break;
+        ++word;
+    }
+    return slot;
+}
+
+// ---------------------------------------------------------------------------
+// Block-level stable ranking of up to NT*IPT items by an 8-bit digit.
+// Item `it` of a thread is tile element warp*32*IPT + it*32 + lane; invalid
+// items carry digit 0x100.  On return dest[it] is the item's position in the
+// tile stably sorted by digit, dstart[d] the first position of digit d
+// (dstart[256] = number of valid items).  wcnt: NW*256 u32 of shared memory.
+// ---------------------------------------------------------------------------
+template <int NT, int IPT>
+__device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t (&dest)[IPT],
+                                           uint32_t* wcnt, uint32_t* dstart, uint32_t* tmp) {
+    constexpr int NW = NT / 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t i = tid; i < NW * 256; i += NT) wcnt[i] = 0;
+    __syncthreads();
+    uint32_t* mine = wcnt + warp * 256;
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+        const uint32_t d = dig[it];
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t leader = __ffs(peers) - 1;
+        uint32_t b = 0;
+        if (lane == leader && d < 256) {
+            b = mine[d];
+            mine[d] = b + __popc(peers);
+        }
+        b = __shfl_sync(0xFFFFFFFFu, b, leader);
+        dest[it] = b + __popc(peers & ((1u << lane) - 1u));
+        __syncwarp();
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    if (tid < 256) {
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t t = wcnt[w * 256 + tid];
+            wcnt[w * 256 + tid] = tot;
+            tot += t;
+        }
+        // exclusive scan of tot over the 256 digits (8 warps)
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        if (lane == 31) tmp[warp] = incl;
+        dstart[tid] = incl - tot;  // partial; warp prefix added below
+    }
+    __syncthreads();
+    if (tid < 256) {
+        uint32_t pre = 0;
+        for (uint32_t w = 0; w < warp; ++w) pre += tmp[w];
+        dstart[tid] += pre;
+        if (tid == 255) dstart[256] = dstart[255] + tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+        const uint32_t d = dig[it];
+        if (d < 256) dest[it] += dstart[d] + mine[d];
     }
 }
 
-__global__ void sort_init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ saf,
-                                 uint32_t n, Seg* large_in, Seg* small_a, Seg* small_b,
-                                 uint32_t* ctr) {
+// ---------------------------------------------------------------------------
+// init / control
+// ---------------------------------------------------------------------------
+__global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ saf, uint32_t n,
+                            Lists in, Lists out, uint32_t* misc) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         sa0[i] = (uint32_t)i;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        for (int c = 0; c < C_N; ++c) ctr[c] = 0;
-        if (n == 1) {
-            saf[0] = 0;
-        } else if (n > 1) {
-            Seg s{0u, n, 0u, make_meta(24, 0, 0)};
-            if (n <= kCapA) small_a[ctr[C_SMALL_A]++] = s;
-            else if (n <= kCapB) small_b[ctr[C_SMALL_B]++] = s;
-            else large_in[ctr[C_LARGE_IN]++] = s;
+        for (int c = 0; c < NCLASS; ++c) {
+            in.cnt[c] = 0;
+            out.cnt[c] = 0;
         }
+        for (int c = 0; c < M_N; ++c) misc[c] = 0;
+        if (n == 1) saf[0] = 0;
+        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 0)});
     }
 }
 
-// Split each large segment into <= kMaxChunks chunks of ~kChunk members.
-__global__ void chunkify_kernel(const Seg* __restrict__ segs, SegX* __restrict__ segx,
-                                Chunk* __restrict__ chunks, uint32_t* ctr) {
-    const uint32_t n = ctr[C_LARGE_IN];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const Seg s = segs[i];
+__global__ void reset_counts_kernel(uint32_t* cnt, uint32_t* misc) {
+    if (threadIdx.x < NCLASS) cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) misc[M_CHUNKS] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// LARGE: one stable 8-bit MSD digit pass
+// ---------------------------------------------------------------------------
+__global__ void chunkify_kernel(Lists in, SegX* __restrict__ segx, Chunk* __restrict__ chunks,
+                                uint32_t* misc) {
+    const uint32_t n = in.cnt[LARGE];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const Seg s = in.seg[LARGE][i];
         uint32_t nch = (s.len + kChunk - 1) / kChunk;
         nch = nch > kMaxChunks ? kMaxChunks : nch;
         const uint32_t clen = (s.len + nch - 1) / nch;
         nch = (s.len + clen - 1) / clen;
-        const uint32_t base = atomicAdd(ctr + C_CHUNKS, nch);
-        atomicAdd(ctr + C_ACTIVE, s.len);
-        segx[i] = SegX{base, nch, clen, 0u};
-        for (uint32_t c = 0; c < nch; ++c) {
+        uint32_t base = 0;
+        if (lane == 0) {
+            base = atomicAdd(misc + M_CHUNKS, nch);
+            atomicAdd(misc + M_ACTIVE, s.len);
+            segx[i] = SegX{base, nch, clen, 0u};
+        }
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        for (uint32_t c = lane; c < nch; c += 32) {
             const uint32_t b = s.start + c * clen;
             const uint32_t e = min(b + clen, s.start + s.len);
             chunks[base + c] = Chunk{i, b, e, 0u};
@@ -110,28 +248,25 @@ __global__ void chunkify_kernel(const Seg* __restrict__ segs, SegX* __restrict__
     }
 }
 
-// Pass 1 of a digit pass: per-chunk histogram of the current 8-bit digit.
-// Computes (and caches) the key word when the segment's keys are stale.
-__global__ void __launch_bounds__(kDigNt) digit_hist_kernel(
-    const Seg* __restrict__ segs, const Chunk* __restrict__ chunks, const uint32_t* ctr,
-    uint32_t* __restrict__ sa0, uint32_t* __restrict__ sa1, uint32_t* __restrict__ k0,
-    uint32_t* __restrict__ k1, const uint32_t* __restrict__ text,
-    const uint32_t* __restrict__ term, uint64_t base, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[256];
-    const uint32_t nch = ctr[C_CHUNKS];
-    const uint32_t lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chunk* __restrict__ chunks,
+                                                            const uint32_t* misc, Bufs B,
+                                                            uint32_t* __restrict__ hist) {
+    constexpr int NW = kDigNt / 32;
+    __shared__ uint32_t h[NW][256];
+    const uint32_t nch = misc[M_CHUNKS];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-        h[threadIdx.x] = 0;
+        for (uint32_t i = tid; i < NW * 256; i += kDigNt) (&h[0][0])[i] = 0;
         __syncthreads();
         const Chunk ch = chunks[c];
-        const Seg s = segs[ch.seg];
+        const Seg s = in.seg[LARGE][ch.seg];
         const uint32_t shift = meta_shift(s.meta);
         const uint32_t buf = meta_buf(s.meta);
         const bool kv = meta_kv(s.meta);
-        const uint32_t* S = buf ? sa1 : sa0;
-        uint32_t* K = buf ? k1 : k0;
+        const uint32_t* S = B.sa[buf];
+        uint32_t* K = B.key[buf];
         for (uint32_t p0 = ch.begin; p0 < ch.end; p0 += kDigNt) {
-            const uint32_t p = p0 + threadIdx.x;
+            const uint32_t p = p0 + tid;
             const bool valid = p < ch.end;
             uint32_t d = 0x100;
             if (valid) {
@@ -139,41 +274,54 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(
                 if (kv) {
                     key = K[p];
                 } else {
-                    key = suffix_key(text, term, base + S[p], s.word);
+                    key = suffix_key(B.text, B.term, B.base + S[p], s.word);
                     K[p] = key;
                 }
                 d = (key >> shift) & 0xFF;
             }
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-            if (valid && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], (uint32_t)__popc(peers));
+            const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+            if (__all_sync(0xFFFFFFFFu, d == d0)) {
+                if (lane == 0 && d0 < 256) atomicAdd(&h[warp][d0], 32u);
+            } else if (valid) {
+                atomicAdd(&h[warp][d], 1u);
+            }
         }
         __syncthreads();
-        hist[(size_t)c * 256 + threadIdx.x] = h[threadIdx.x];
+        if (tid < 256) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t += h[w][tid];
+            hist[(size_t)c * 256 + tid] = t;
+        }
         __syncthreads();
     }
 }
 
-// Pass 2: per segment, exclusive scan of the chunk histograms, digit bases,
-// sieve decisions and child segments.
-__global__ void __launch_bounds__(256) digit_scan_kernel(
-    const Seg* __restrict__ segs, SegX* __restrict__ segx, uint32_t* __restrict__ hist,
-    uint32_t* __restrict__ dbase, Seg* large_out, Seg* small_a, Seg* small_b, uint32_t* ctr) {
+__global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
+                                                         SegX* __restrict__ segx,
+                                                         uint32_t* __restrict__ hist,
+                                                         uint32_t* __restrict__ dbase) {
     __shared__ uint32_t wsum[8];
     __shared__ int all_one;
-    const uint32_t n = ctr[C_LARGE_IN];
+    const uint32_t n = in.cnt[LARGE];
     const uint32_t d = threadIdx.x, lane = d & 31, warp = d >> 5;
     for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
-        const Seg s = segs[si];
+        const Seg s = in.seg[LARGE][si];
         const SegX x = segx[si];
         uint32_t run = 0;
-        for (uint32_t c = x.chunk_base; c < x.chunk_base + x.nchunks; ++c) {
-            const size_t idx = (size_t)c * 256 + d;
-            const uint32_t v = hist[idx];
-            hist[idx] = run;
-            run += v;
+        constexpr int kB = 16;
+        for (uint32_t c0 = x.chunk_base; c0 < x.chunk_base + x.nchunks; c0 += kB) {
+            uint32_t v[kB];
+            const uint32_t cn = min((uint32_t)kB, x.chunk_base + x.nchunks - c0);
+#pragma unroll
+            for (int b = 0; b < kB; ++b) v[b] = (uint32_t)b < cn ? hist[(size_t)(c0 + b) * 256 + d] : 0u;
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                if ((uint32_t)b < cn) hist[(size_t)(c0 + b) * 256 + d] = run;
+                run += v[b];
+            }
         }
         if (d == 0) all_one = 0;
-        // exclusive scan of run over the 256 digits
         uint32_t incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -195,10 +343,10 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(
             if (resolved) {
                 flag = 0x80000000u;
             } else {
+                const uint32_t cbuf = all_one ? buf : 1u - buf;
                 Seg c;
                 c.start = s.start + excl;
                 c.len = run;
-                const uint32_t cbuf = all_one ? buf : 1u - buf;
                 if (shift == 0) {
                     c.word = s.word + 1;
                     c.meta = make_meta(24, cbuf, 0);
@@ -206,7 +354,7 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(
                     c.word = s.word;
                     c.meta = make_meta(shift - 8, cbuf, 1);
                 }
-                emit_child(c, large_out, small_a, small_b, ctr);
+                emit(out, c);
                 if (all_one) segx[si].skip = 1;
             }
         }
@@ -215,311 +363,492 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(
     }
 }
 
-// Pass 3: stable scatter of each chunk by digit.  Sieved buckets go straight
-// to the final SA, the others to the segment's other buffer.
 __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
-    const Seg* __restrict__ segs, const SegX* __restrict__ segx, const Chunk* __restrict__ chunks,
-    const uint32_t* ctr, const uint32_t* __restrict__ hist, const uint32_t* __restrict__ dbase,
-    uint32_t* __restrict__ sa0, uint32_t* __restrict__ sa1, uint32_t* __restrict__ k0,
-    uint32_t* __restrict__ k1, uint32_t* __restrict__ saf) {
-    __shared__ uint32_t run_base[256];
-    __shared__ uint32_t tile_cnt[256];
-    __shared__ uint8_t fin[256];
-    __shared__ uint32_t wcnt[kDigWarps][256];
-    const uint32_t nch = ctr[C_CHUNKS];
+    Lists in, const SegX* __restrict__ segx, const Chunk* __restrict__ chunks, const uint32_t* misc,
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ dbase, Bufs B) {
+    constexpr int NW = kDigNt / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);  // NW*256
+    uint32_t* s_key = wcnt + NW * 256;                        // kDigTile
+    uint32_t* s_slot = s_key + kDigTile;                      // kDigTile
+    uint32_t* dstart = s_slot + kDigTile;                     // 257
+    uint32_t* run_base = dstart + 260;                        // 256
+    uint32_t* tmp = run_base + 256;                           // 32
+    uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);      // 256
+    const uint32_t nch = misc[M_CHUNKS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
         const Chunk ch = chunks[c];
         if (segx[ch.seg].skip) continue;  // uniform across the CTA
-        const Seg s = segs[ch.seg];
+        const Seg s = in.seg[LARGE][ch.seg];
         const uint32_t shift = meta_shift(s.meta);
         const uint32_t buf = meta_buf(s.meta);
-        const uint32_t* S = buf ? sa1 : sa0;
-        const uint32_t* K = buf ? k1 : k0;
-        uint32_t* S2 = buf ? sa0 : sa1;
-        uint32_t* K2 = buf ? k0 : k1;
-        const uint32_t db = dbase[(size_t)ch.seg * 256 + tid];
-        run_base[tid] = (db & 0x7FFFFFFFu) + hist[(size_t)c * 256 + tid];
-        fin[tid] = (uint8_t)(db >> 31);
-        for (int w = 0; w < kDigWarps; ++w) wcnt[w][tid] = 0;
-        __syncthreads();
+        const uint32_t* S = B.sa[buf];
+        const uint32_t* K = B.key[buf];
+        uint32_t* S2 = B.sa[1 - buf];
+        uint32_t* K2 = B.key[1 - buf];
+        if (tid < 256) {
+            const uint32_t db = dbase[(size_t)ch.seg * 256 + tid];
+            run_base[tid] = (db & 0x7FFFFFFFu) + hist[(size_t)c * 256 + tid];
+            fin[tid] = (uint8_t)(db >> 31);
+        }
         for (uint32_t t0 = ch.begin; t0 < ch.end; t0 += kDigTile) {
-            uint32_t key[kDigIpt], slot[kDigIpt], dig[kDigIpt], lrank[kDigIpt];
+            const uint32_t tn = min((uint32_t)kDigTile, ch.end - t0);
+            uint32_t key[kDigIpt], slot[kDigIpt], dig[kDigIpt], dest[kDigIpt];
 #pragma unroll
             for (int it = 0; it < kDigIpt; ++it) {
-                const uint32_t p = t0 + warp * (32 * kDigIpt) + it * 32 + lane;
-                const bool valid = p < ch.end;
-                key[it] = valid ? K[p] : 0u;
-                slot[it] = valid ? S[p] : 0u;
+                const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
+                const bool valid = e < tn;
+                key[it] = valid ? K[t0 + e] : 0u;
+                slot[it] = valid ? S[t0 + e] : 0u;
                 dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
-                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dig[it]);
-                const uint32_t leader = __ffs(peers) - 1;
-                const uint32_t prior = __popc(peers & ((1u << lane) - 1u));
-                uint32_t b = 0;
-                if (valid && lane == leader) {
-                    b = wcnt[warp][dig[it]];
-                    wcnt[warp][dig[it]] = b + __popc(peers);
-                }
-                b = __shfl_sync(0xFFFFFFFFu, b, leader);
-                lrank[it] = b + prior;
-                __syncwarp();  // order the leader's wcnt update before the next item's read
             }
-            __syncthreads();
-            {
-                uint32_t acc = 0;
-                for (int w = 0; w < kDigWarps; ++w) {
-                    const uint32_t t = wcnt[w][tid];
-                    wcnt[w][tid] = acc;
-                    acc += t;
-                }
-                tile_cnt[tid] = acc;
-            }
-            __syncthreads();
+            block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
 #pragma unroll
             for (int it = 0; it < kDigIpt; ++it) {
-                if (dig[it] > 0xFFu) continue;
-                const uint32_t dp = run_base[dig[it]] + wcnt[warp][dig[it]] + lrank[it];
-                if (fin[dig[it]]) {
-                    saf[dp] = slot[it];
-                } else {
-                    S2[dp] = slot[it];
-                    K2[dp] = key[it];
+                if (dig[it] < 256) {
+                    s_key[dest[it]] = key[it];
+                    s_slot[dest[it]] = slot[it];
                 }
             }
             __syncthreads();
-            run_base[tid] += tile_cnt[tid];
-            for (int w = 0; w < kDigWarps; ++w) wcnt[w][tid] = 0;
+            // coalesced write-out: consecutive tile positions of one digit go to
+            // consecutive global positions
+            for (uint32_t i = tid; i < tn; i += kDigNt) {
+                const uint32_t k = s_key[i];
+                const uint32_t d = (k >> shift) & 0xFFu;
+                const uint32_t gp = run_base[d] + (i - dstart[d]);
+                if (fin[d]) {
+                    B.saf[gp] = s_slot[i];
+                } else {
+                    S2[gp] = s_slot[i];
+                    K2[gp] = k;
+                }
+            }
+            __syncthreads();
+            if (tid < 256) run_base[tid] += dstart[tid + 1] - dstart[tid];
             __syncthreads();
         }
     }
 }
 
-// Block-wide inclusive max-scan of a[0..P) (P elements, NT threads).
-template <int NT>
-__device__ void block_max_scan(uint16_t* a, uint32_t P, uint32_t* aux) {
-    const uint32_t per = (P + NT - 1) / NT;
-    const uint32_t b = threadIdx.x * per;
-    const uint32_t e = min(b + per, P);
-    uint32_t m = 0;
-    for (uint32_t i = b; i < e; ++i) {
-        m = max(m, (uint32_t)a[i]);
-        a[i] = (uint16_t)m;
+constexpr size_t scatter_smem() {
+    return (size_t)(kDigNt / 32) * 256 * 4 + 2 * (size_t)kDigTile * 4 + 260 * 4 + 256 * 4 +
+           32 * 4 + 256 + 16;
+}
+
+// ---------------------------------------------------------------------------
+// TINY: one warp per segment
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* misc) {
+    const uint32_t n = in.cnt[TINY];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const Seg s = in.seg[TINY][i];
+        const uint32_t buf = meta_buf(s.meta);
+        const bool kv = meta_kv(s.meta);
+        uint32_t slot = 0, key = 0;
+        if (lane < s.len) {
+            slot = B.sa[buf][s.start + lane];
+            if (kv) key = B.key[buf][s.start + lane];
+        }
+        if (lane == 0) atomicAdd(misc + M_ELEMS_T, s.len);
+        slot = warp_finish(slot, s.len, s.word, key, kv, B);
+        if (lane < s.len) B.saf[s.start + lane] = slot;
     }
-    aux[threadIdx.x] = m;
-    __syncthreads();
-    for (uint32_t o = 1; o < NT; o <<= 1) {
-        const uint32_t v = threadIdx.x >= o ? aux[threadIdx.x - o] : 0u;
-        __syncthreads();
-        aux[threadIdx.x] = max(aux[threadIdx.x], v);
-        __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// SMALL: one warp per segment, LSD radix sort in registers
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, Lists out, Bufs B,
+                                                                 uint32_t* misc) {
+    __shared__ uint32_t s_cnt[kWarpCta][256];
+    __shared__ uint2 s_buf[kWarpCta][kCapS];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t* cnt = s_cnt[wib];
+    uint2* buf = s_buf[wib];
+    const uint32_t n = in.cnt[SMALL];
+    const uint32_t nw = gridDim.x * kWarpCta;
+    for (uint32_t si = blockIdx.x * kWarpCta + wib; si < n; si += nw) {
+        const Seg s = in.seg[SMALL][si];
+        const uint32_t L = s.len;
+        const uint32_t nit = (L + 31) >> 5;
+        const uint32_t bid = meta_buf(s.meta);
+        const bool kv = meta_kv(s.meta);
+        const uint32_t* S = B.sa[bid];
+        if (lane == 0) atomicAdd(misc + M_ELEMS_S, L);
+        uint32_t key[kIpl], slot[kIpl], rank[kIpl];
+#pragma unroll
+        for (int it = 0; it < kIpl; ++it) {
+            key[it] = 0xFFFFFFFFu;  // padding sorts last (stably after every real key)
+            slot[it] = 0;
+            const uint32_t e = it * 32 + lane;
+            if ((uint32_t)it < nit && e < L) {
+                slot[it] = S[s.start + e];
+                key[it] = kv ? B.key[bid][s.start + e]
+                             : suffix_key(B.text, B.term, B.base + slot[it], s.word);
+            }
+        }
+        const uint32_t top = kv ? meta_shift(s.meta) : 24u;
+        for (uint32_t sh = 0; sh <= top; sh += 8) {
+            const uint32_t d0 = (__shfl_sync(0xFFFFFFFFu, key[0], 0) >> sh) & 0xFFu;
+            bool same = true;
+#pragma unroll
+            for (int it = 0; it < kIpl; ++it)
+                if ((uint32_t)it < nit && it * 32 + lane < L) same &= ((key[it] >> sh) & 0xFFu) == d0;
+            if (__all_sync(0xFFFFFFFFu, same)) continue;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cnt[lane * 8 + j] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < kIpl; ++it) {
+                if ((uint32_t)it < nit) {
+                    const uint32_t d = (key[it] >> sh) & 0xFFu;
+                    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+                    const uint32_t leader = __ffs(peers) - 1;
+                    uint32_t b = 0;
+                    if (lane == leader) {
+                        b = cnt[d];
+                        cnt[d] = b + __popc(peers);
+                    }
+                    b = __shfl_sync(0xFFFFFFFFu, b, leader);
+                    rank[it] = b + __popc(peers & ((1u << lane) - 1u));
+                    __syncwarp();
+                }
+            }
+            {
+                uint32_t v[8], sum = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    v[j] = cnt[lane * 8 + j];
+                    sum += v[j];
+                }
+                uint32_t incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                uint32_t run = incl - sum;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    cnt[lane * 8 + j] = run;
+                    run += v[j];
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < kIpl; ++it) {
+                if ((uint32_t)it < nit) {
+                    const uint32_t d = (key[it] >> sh) & 0xFFu;
+                    buf[cnt[d] + rank[it]] = make_uint2(key[it], slot[it]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < kIpl; ++it) {
+                if ((uint32_t)it < nit) {
+                    const uint2 v = buf[it * 32 + lane];
+                    key[it] = v.x;
+                    slot[it] = v.y;
+                }
+            }
+            __syncwarp();
+        }
+        // final order out; stash (key, slot) for the tie scan
+#pragma unroll
+        for (int it = 0; it < kIpl; ++it) {
+            const uint32_t e = it * 32 + lane;
+            if ((uint32_t)it < nit) {
+                buf[e] = make_uint2(key[it], slot[it]);
+                if (e < L) B.saf[s.start + e] = slot[it];
+            }
+        }
+        __syncwarp();
+        // ties on this word with 14 real symbols: finish runs <= 32 here, emit
+        // longer runs as segments of the next word
+        for (uint32_t it = 0; it < nit; ++it) {
+            const uint32_t e = it * 32 + lane;
+            const uint32_t k = buf[e].x;
+            const bool st = e < L && (e == 0 || buf[e - 1].x != k) && e + 1 < L &&
+                            buf[e + 1].x == k && (k & 15u) == (uint32_t)kKeySyms;
+            uint32_t m = __ballot_sync(0xFFFFFFFFu, st);
+            while (m) {
+                const uint32_t l = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t rs = it * 32 + l;
+                const uint32_t rk = buf[rs].x;
+                uint32_t Lr = 0;
+                for (uint32_t c = rs + 1;; c += 32) {
+                    const uint32_t q = c + lane;
+                    const bool eq = q < L && buf[q].x == rk;
+                    const uint32_t ne = __ballot_sync(0xFFFFFFFFu, !eq);
+                    if (ne) {
+                        Lr = c + (__ffs(ne) - 1) - rs;
+                        break;
+                    }
+                }
+                if (Lr <= kTiny) {
+                    uint32_t sl = lane < Lr ? buf[rs + lane].y : 0u;
+                    sl = warp_finish(sl, Lr, s.word + 1, 0u, false, B);
+                    if (lane < Lr) B.saf[s.start + rs + lane] = sl;
+                } else {
+                    for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = buf[rs + q].y;
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
+                }
+            }
+        }
+        __syncwarp();
     }
-    const uint32_t pre = threadIdx.x > 0 ? aux[threadIdx.x - 1] : 0u;
-    for (uint32_t i = b; i < e; ++i) a[i] = (uint16_t)max((uint32_t)a[i], pre);
-    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// MEDIUM: one CTA per segment, LSD radix in shared memory
+// ---------------------------------------------------------------------------
+template <int CAP, int NT>
+constexpr size_t local_smem() {
+    return (size_t)CAP * 16 + (size_t)(NT / 32) * 256 * 4 + 260 * 4 + 32 * 4 + (CAP / 2) * 8 + 64;
 }
 
 template <int CAP, int NT>
-constexpr size_t local_sort_smem() {
-    return (size_t)CAP * (8 + 4 + 2 + 1) + (size_t)NT * 4 + 16;
-}
-
-// Finish a small segment in shared memory (all remaining key words).
-template <int CAP, int NT>
-__global__ void __launch_bounds__(NT) local_sort_kernel(
-    const Seg* __restrict__ list, const uint32_t* ctr, int which, const uint32_t* __restrict__ sa0,
-    const uint32_t* __restrict__ sa1, uint32_t* __restrict__ saf,
-    const uint32_t* __restrict__ text, const uint32_t* __restrict__ term, uint64_t base) {
+__global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls, Bufs B,
+                                                    uint32_t* misc) {
+    constexpr int IPT = CAP / NT;
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned long long* comp = reinterpret_cast<unsigned long long*>(smem_raw);
-    uint32_t* slot = reinterpret_cast<uint32_t*>(comp + CAP);
-    uint32_t* aux = slot + CAP;
-    uint16_t* run = reinterpret_cast<uint16_t*>(aux + NT);
-    uint8_t* act = reinterpret_cast<uint8_t*>(run + CAP);
-    constexpr int IDXB = 12;  // index / run-start field width (CAP <= 4096)
-    static_assert(CAP <= (1 << IDXB), "CAP too large for the composite");
-    const uint32_t n = ctr[which];
+    uint32_t* const keyA0 = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* const slotA0 = keyA0 + CAP;
+    uint32_t* const keyB0 = slotA0 + CAP;
+    uint32_t* const slotB0 = keyB0 + CAP;
+    uint32_t* wcnt = slotB0 + CAP;          // NW*256
+    uint32_t* dstart = wcnt + NW * 256;     // 257
+    uint32_t* tmp = dstart + 260;           // 32
+    uint2* runs = reinterpret_cast<uint2*>(tmp + 32);  // CAP/2
+    __shared__ uint32_t n_runs;
+    __shared__ int same_digit;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = in.cnt[cls];
     for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
-        const Seg s = list[si];
+        uint32_t *keyA = keyA0, *slotA = slotA0, *keyB = keyB0, *slotB = slotB0;
+        const Seg s = in.seg[cls][si];
         const uint32_t len = s.len;
-        uint32_t P = 2;
-        while (P < len) P <<= 1;
-        const uint32_t* S = meta_buf(s.meta) ? sa1 : sa0;
-        for (uint32_t i = threadIdx.x; i < len; i += NT) {
-            slot[i] = S[s.start + i];
-            run[i] = 0;
-            act[i] = 1;
+        const uint32_t buf = meta_buf(s.meta);
+        const bool kv = meta_kv(s.meta);
+        uint32_t* S = B.sa[buf];
+        if (tid == 0) {
+            atomicAdd(misc + M_ELEMS_M, len);
+            n_runs = 0;
+        }
+        for (uint32_t i = tid; i < len; i += NT) {
+            const uint32_t sl = S[s.start + i];
+            slotA[i] = sl;
+            keyA[i] = kv ? B.key[buf][s.start + i] : suffix_key(B.text, B.term, B.base + sl, s.word);
         }
         __syncthreads();
-        uint32_t word = s.word;
-        for (;;) {
-            for (uint32_t i = threadIdx.x; i < P; i += NT) {
-                unsigned long long cmp;
-                if (i < len) {
-                    if (act[i]) {
-                        const uint32_t key = suffix_key(text, term, base + slot[i], word);
-                        cmp = ((unsigned long long)run[i] << (32 + IDXB)) |
-                              ((unsigned long long)key << IDXB) | i;
-                    } else {
-                        cmp = ((unsigned long long)i << (32 + IDXB)) | i;
-                    }
-                } else {
-                    cmp = ~0ull;
-                }
-                comp[i] = cmp;
-            }
+        // LSD passes over the digits not yet known to be equal
+        const uint32_t top = kv ? meta_shift(s.meta) : 24u;
+        for (uint32_t sh = 0; sh <= top; sh += 8) {
+            if (tid == 0) same_digit = 1;
             __syncthreads();
-            // bitonic sort of comp[0..P)
-            for (uint32_t k = 2; k <= P; k <<= 1) {
-                for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-                    for (uint32_t t = threadIdx.x; t < (P >> 1); t += NT) {
-                        const uint32_t i = 2 * t - (t & (j - 1));
-                        const uint32_t q = i + j;
-                        const unsigned long long a = comp[i], b = comp[q];
-                        const bool up = (i & k) == 0;
-                        if ((a > b) == up) {
-                            comp[i] = b;
-                            comp[q] = a;
-                        }
-                    }
-                    __syncthreads();
+            const uint32_t d0 = (keyA[0] >> sh) & 0xFFu;
+            bool same = true;
+            for (uint32_t i = tid; i < len; i += NT) same &= ((keyA[i] >> sh) & 0xFFu) == d0;
+            if (!same) same_digit = 0;
+            __syncthreads();
+            if (same_digit) continue;
+            uint32_t dig[IPT], dest[IPT];
+#pragma unroll
+            for (int it = 0; it < IPT; ++it) {
+                const uint32_t e = warp * (32 * IPT) + it * 32 + lane;
+                dig[it] = e < len ? ((keyA[e] >> sh) & 0xFFu) : 0x100u;
+            }
+            block_rank<NT, IPT>(dig, dest, wcnt, dstart, tmp);
+#pragma unroll
+            for (int it = 0; it < IPT; ++it) {
+                if (dig[it] < 256) {
+                    const uint32_t e = warp * (32 * IPT) + it * 32 + lane;
+                    keyB[dest[it]] = keyA[e];
+                    slotB[dest[it]] = slotA[e];
                 }
             }
-            // permute slots; derive new tied runs
-            uint32_t newslot[(CAP + NT - 1) / NT];
-            int r = 0;
-            for (uint32_t i = threadIdx.x; i < len; i += NT, ++r)
-                newslot[r] = slot[comp[i] & ((1u << IDXB) - 1)];
             __syncthreads();
-            r = 0;
-            bool any = false;
-            for (uint32_t i = threadIdx.x; i < len; i += NT, ++r) {
-                slot[i] = newslot[r];
-                const unsigned long long hi = comp[i] >> IDXB;
-                const bool eqp = i > 0 && (comp[i - 1] >> IDXB) == hi;
-                const bool eqn = i + 1 < len && (comp[i + 1] >> IDXB) == hi;
-                const uint32_t key = (uint32_t)(hi & 0xFFFFFFFFull);
-                const bool a = (eqp || eqn) && ((key & 15u) == (uint32_t)kKeySyms);
-                act[i] = a;
-                any |= a;
-                run[i] = eqp ? 0 : (uint16_t)i;
-            }
-            __syncthreads();
-            if (!__syncthreads_or(any)) break;
-            block_max_scan<NT>(run, len, aux);
-            ++word;
+            uint32_t* t;
+            t = keyA; keyA = keyB; keyB = t;
+            t = slotA; slotA = slotB; slotB = t;
         }
-        for (uint32_t i = threadIdx.x; i < len; i += NT) saf[s.start + i] = slot[i];
+        // write the order; collect tied runs (equal word, 14 real symbols)
+        for (uint32_t i = tid; i < len; i += NT) {
+            B.saf[s.start + i] = slotA[i];
+            const uint32_t k = keyA[i];
+            const bool starts = (i == 0 || keyA[i - 1] != k) && i + 1 < len && keyA[i + 1] == k &&
+                                (k & 15u) == (uint32_t)kKeySyms;
+            if (starts) {
+                uint32_t L = 2;
+                while (i + L < len && keyA[i + L] == k) ++L;
+                runs[atomicAdd(&n_runs, 1u)] = make_uint2(i, L);
+            }
+        }
+        __syncthreads();
+        const uint32_t nr = n_runs;
+        for (uint32_t r = warp; r < nr; r += NW) {
+            const uint2 rr = runs[r];
+            if (rr.y <= kTiny) {
+                uint32_t sl = lane < rr.y ? slotA[rr.x + lane] : 0u;
+                sl = warp_finish(sl, rr.y, s.word + 1, 0u, false, B);
+                if (lane < rr.y) B.saf[s.start + rr.x + lane] = sl;
+            } else {
+                for (uint32_t q = lane; q < rr.y; q += 32) S[s.start + rr.x + q] = slotA[rr.x + q];
+                if (lane == 0) emit(out, Seg{s.start + rr.x, rr.y, s.word + 1, make_meta(24, buf, 0)});
+            }
+        }
         __syncthreads();
     }
 }
 
-__global__ void sort_advance_kernel(uint32_t* ctr) {
-    ctr[C_LARGE_IN] = ctr[C_LARGE_OUT];
-    ctr[C_LARGE_OUT] = 0;
-    ctr[C_CHUNKS] = 0;
-}
+}  // namespace sortk
 
-__global__ void sort_zero_small_kernel(uint32_t* ctr) {
-    ctr[C_SMALL_A] = 0;
-    ctr[C_SMALL_B] = 0;
-}
-
-}  // namespace
+using namespace sortk;
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
                        uint32_t* d_sa_final, SortStats* st) {
     if (n_suf == 0) return cudaSuccess;
-    uint32_t *sa0, *sa1, *k0, *k1, *hist, *ctr, *dbase;
-    Seg *la, *lb, *sma, *smb;
-    Chunk* chunks;
     const size_t n = n_suf;
-    const size_t max_large = n / (kCapB + 1) + 1;
+    const size_t cap[NCLASS] = {n / 2 + 1, n / (kTiny + 1) + 1, n / (kCapS + 1) + 1,
+                                n / (kCapM + 1) + 1};
+    const size_t max_large = cap[LARGE];
     const size_t max_chunks = n / kChunk + max_large + 1;
+    uint32_t *sa0, *sa1, *k0, *k1, *hist, *ctr;
     SB_CHECK(ensure(ws.sa0, n, &sa0));
     SB_CHECK(ensure(ws.sa1, n, &sa1));
     SB_CHECK(ensure(ws.k0, n, &k0));
     SB_CHECK(ensure(ws.k1, n, &k1));
-    // segs_a / segs_b each hold: Seg[max_large] + SegX[max_large] + dbase[max_large*256]
-    const size_t seg_bytes = max_large * (sizeof(Seg) + sizeof(SegX) + 256 * sizeof(uint32_t));
-    uint8_t *ra, *rb;
-    SB_CHECK(ensure(ws.segs_a, seg_bytes, &ra));
-    SB_CHECK(ensure(ws.segs_b, seg_bytes, &rb));
-    SB_CHECK(ensure(ws.small_a, n / 2 + 1, &sma));
-    SB_CHECK(ensure(ws.small_b, n / (kCapA + 1) + 1, &smb));
+    size_t list_elems = 0;
+    for (int c = 0; c < NCLASS; ++c) list_elems += cap[c];
+    Seg *la, *lb;
+    SB_CHECK(ensure(ws.segs_a, list_elems, &la));
+    SB_CHECK(ensure(ws.segs_b, list_elems, &lb));
+    SegX* segx;
+    uint32_t* dbase;
+    Chunk* chunks;
+    SB_CHECK(ensure(ws.small_a, max_large, &segx));
+    SB_CHECK(ensure(ws.small_b, max_large * 256, &dbase));
     SB_CHECK(ensure(ws.chunks, max_chunks, &chunks));
     SB_CHECK(ensure(ws.hist, max_chunks * 256, &hist));
-    SB_CHECK(ensure(ws.ctr, 16, &ctr));
-    la = reinterpret_cast<Seg*>(ra);
-    lb = reinterpret_cast<Seg*>(rb);
-    SegX* segx = reinterpret_cast<SegX*>(ra + max_large * sizeof(Seg));
-    dbase = reinterpret_cast<uint32_t*>(ra + max_large * (sizeof(Seg) + sizeof(SegX)));
+    SB_CHECK(ensure(ws.ctr, 2 * NCLASS + M_N + 8, &ctr));
+    uint32_t* misc = ctr + 2 * NCLASS;
+    Lists A, Bl;
+    {
+        size_t off = 0;
+        for (int c = 0; c < NCLASS; ++c) {
+            A.seg[c] = la + off;
+            Bl.seg[c] = lb + off;
+            off += cap[c];
+        }
+        A.cnt = ctr;
+        Bl.cnt = ctr + NCLASS;
+    }
+    Bufs B;
+    B.sa[0] = sa0;
+    B.sa[1] = sa1;
+    B.key[0] = k0;
+    B.key[1] = k1;
+    B.saf = d_sa_final;
+    B.text = text;
+    B.term = term;
+    B.base = slot_base;
+
+    static int attr_dev = -1;
+    int dev = 0;
+    SB_CHECK(cudaGetDevice(&dev));
+    constexpr size_t sm_m = local_smem<kCapM, kNtM>();
+    constexpr size_t sm_d = scatter_smem();
+    if (attr_dev != dev) {
+        SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
+        SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
+        attr_dev = dev;
+    }
 
     SB_LAUNCH(prof, s, "sort_init", 4.0 * n, n,
-              sort_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa0, d_sa_final, n_suf, la, sma,
-                                                                 smb, ctr));
+              init_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc));
     SB_CHECK(cudaGetLastError());
-    const unsigned g_small = 148u * 16u;
-    constexpr size_t smem_a = local_sort_smem<kCapA, kNtA>();
-    constexpr size_t smem_b = local_sort_smem<kCapB, kNtB>();
-    static bool attr_done = false;
-    if (!attr_done) {
-        SB_CHECK(cudaFuncSetAttribute(local_sort_kernel<kCapA, kNtA>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
-        SB_CHECK(cudaFuncSetAttribute(local_sort_kernel<kCapB, kNtB>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-        attr_done = true;
+    uint32_t h_cnt[NCLASS] = {0, 0, 0, 0};
+    if (n > 1) {
+        const uint32_t c = n <= kTiny ? TINY : n <= kCapS ? SMALL : n <= kCapM ? MEDIUM : LARGE;
+        h_cnt[c] = 1;
     }
+    Lists in = A, out = Bl;
     uint32_t prev_active = 0;
-    const unsigned g_dig = 148u * 8u;
-    uint32_t h_ctr[C_N];
+    uint64_t act_local = 0;
+    uint32_t h_misc[M_N] = {0, 0, 0, 0, 0};
     for (;;) {
-        // finish every small segment produced so far
-        SB_LAUNCH(prof, s, "local_sort_a", 0, 0,
-                  (local_sort_kernel<kCapA, kNtA><<<g_small, kNtA, smem_a, s>>>(
-                      sma, ctr, C_SMALL_A, sa0, sa1, d_sa_final, text, term, slot_base)));
+        if (!(h_cnt[0] | h_cnt[1] | h_cnt[2] | h_cnt[3])) break;
+        if (h_cnt[TINY]) {
+            SB_LAUNCH(prof, s, "sort_tiny", 0, 0,
+                      tiny_kernel<<<grid_for((uint64_t)h_cnt[TINY] * 32, 256, 148u * 16u), 256, 0,
+                                    s>>>(in, B, misc));
+            SB_CHECK(cudaGetLastError());
+        }
+        if (h_cnt[SMALL]) {
+            SB_LAUNCH(prof, s, "sort_small", 0, 0,
+                      warp_sort_kernel<<<grid_for((uint64_t)h_cnt[SMALL] * 32, kWarpCta * 32,
+                                                  148u * 8u),
+                                         kWarpCta * 32, 0, s>>>(in, out, B, misc));
+            SB_CHECK(cudaGetLastError());
+        }
+        if (h_cnt[MEDIUM]) {
+            SB_LAUNCH(prof, s, "sort_medium", 0, 0,
+                      (local_kernel<kCapM, kNtM><<<std::min<uint32_t>(h_cnt[MEDIUM], 148u * 3u),
+                                                   kNtM, sm_m, s>>>(in, out, MEDIUM, B, misc)));
+            SB_CHECK(cudaGetLastError());
+        }
+        if (h_cnt[LARGE]) {
+            SB_LAUNCH(prof, s, "sort_chunkify", 0, 0,
+                      chunkify_kernel<<<grid_for((uint64_t)h_cnt[LARGE] * 32, 128), 128, 0, s>>>(
+                          in, segx, chunks, misc));
+            SB_CHECK(cudaGetLastError());
+            const unsigned g_dig = 148u * 4u;
+            SB_LAUNCH(prof, s, "digit_hist", 0, 0,
+                      digit_hist_kernel<<<g_dig, kDigNt, 0, s>>>(in, chunks, misc, B, hist));
+            SB_CHECK(cudaGetLastError());
+            SB_LAUNCH(prof, s, "digit_scan", 0, 0,
+                      digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 8u), 256, 0, s>>>(
+                          in, out, segx, hist, dbase));
+            SB_CHECK(cudaGetLastError());
+            SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
+                      digit_scatter_kernel<<<g_dig, kDigNt, sm_d, s>>>(in, segx, chunks, misc, hist,
+                                                                      dbase, B));
+            SB_CHECK(cudaGetLastError());
+        }
+        SB_LAUNCH(prof, s, "sort_ctl", 0, 0, reset_counts_kernel<<<1, 32, 0, s>>>(in.cnt, misc));
         SB_CHECK(cudaGetLastError());
-        SB_LAUNCH(prof, s, "local_sort_b", 0, 0,
-                  (local_sort_kernel<kCapB, kNtB><<<148u * 3u, kNtB, smem_b, s>>>(
-                      smb, ctr, C_SMALL_B, sa0, sa1, d_sa_final, text, term, slot_base)));
-        SB_CHECK(cudaGetLastError());
-        SB_LAUNCH(prof, s, "sort_ctl", 0, 0, sort_zero_small_kernel<<<1, 1, 0, s>>>(ctr));
-        SB_CHECK(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+        std::swap(in, out);
+        SB_CHECK(cudaMemcpyAsync(h_cnt, in.cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+        SB_CHECK(cudaMemcpyAsync(h_misc, misc, sizeof(h_misc), cudaMemcpyDeviceToHost, s));
         SB_CHECK(cudaStreamSynchronize(s));
-        if (st && st->digit_passes > 0) {
-            st->active_per_pass.push_back((uint32_t)(h_ctr[C_ACTIVE] - prev_active));
-            prev_active = h_ctr[C_ACTIVE];
+        if (h_misc[M_ACTIVE] != prev_active) {
+            const uint32_t delta = h_misc[M_ACTIVE] - prev_active;
+            act_local += delta;
+            if (st) {
+                st->active_per_pass.push_back(delta);
+                st->digit_passes++;
+            }
+            prev_active = h_misc[M_ACTIVE];
         }
-        if (h_ctr[C_LARGE_IN] == 0) break;
-        // one stable 8-bit digit pass over every large segment
-        SB_LAUNCH(prof, s, "sort_chunkify", 0, 0,
-                  chunkify_kernel<<<grid_for(h_ctr[C_LARGE_IN], 128), 128, 0, s>>>(la, segx, chunks,
-                                                                                  ctr));
-        SB_CHECK(cudaGetLastError());
-        SB_LAUNCH(prof, s, "digit_hist", 0, 0,
-                  digit_hist_kernel<<<g_dig, kDigNt, 0, s>>>(la, chunks, ctr, sa0, sa1, k0, k1,
-                                                             text, term, slot_base, hist));
-        SB_CHECK(cudaGetLastError());
-        SB_LAUNCH(prof, s, "digit_scan", 0, 0,
-                  digit_scan_kernel<<<grid_for(h_ctr[C_LARGE_IN], 1, 148u * 8u), 256, 0, s>>>(
-                      la, segx, hist, dbase, lb, sma, smb, ctr));
-        SB_CHECK(cudaGetLastError());
-        SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
-                  digit_scatter_kernel<<<g_dig, kDigNt, 0, s>>>(la, segx, chunks, ctr, hist,
-                                                                dbase, sa0, sa1, k0, k1,
-                                                                d_sa_final));
-        SB_CHECK(cudaGetLastError());
-        SB_LAUNCH(prof, s, "sort_ctl", 0, 0, sort_advance_kernel<<<1, 1, 0, s>>>(ctr));
-        SB_CHECK(cudaGetLastError());
-        if (st) {
-            st->digit_passes++;
-        }
-        std::swap(la, lb);
-        std::swap(ra, rb);
-        segx = reinterpret_cast<SegX*>(ra + max_large * sizeof(Seg));
-        dbase = reinterpret_cast<uint32_t*>(ra + max_large * (sizeof(Seg) + sizeof(SegX)));
     }
     if (st) st->rounds++;
+    // algorithmic bytes: a digit pass reads/writes the
+    // (slot, key) pair -- histogram 8 B, scatter 16 B per active element; the
+    // local sorts read (slot, key) and write the final SA entry (12 B/element).
+    prof.add_bytes("digit_hist", 8.0 * act_local, act_local);
+    prof.add_bytes("digit_scatter", 16.0 * act_local, act_local);
+    prof.add_bytes("sort_tiny", 12.0 * h_misc[M_ELEMS_T], h_misc[M_ELEMS_T]);
+    prof.add_bytes("sort_small", 12.0 * h_misc[M_ELEMS_S], h_misc[M_ELEMS_S]);
+    prof.add_bytes("sort_medium", 12.0 * h_misc[M_ELEMS_M], h_misc[M_ELEMS_M]);
     return cudaSuccess;
 }
 
