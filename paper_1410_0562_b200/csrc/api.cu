@@ -232,24 +232,24 @@ inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cu
 // slots starting at slot_base).  With world > 1, only this rank's slice is
 // computed and the slices are exchanged by the allgather callback.
 setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1,
-                                 uint64_t slot_base, uint64_t n_suf, uint64_t* g) {
+                                 uint64_t slot_base, uint64_t n_suf, void* g, int gw) {
     if (h->n == 0) {
         // empty B_ext: every suffix has rank 0
-        API_CHECK(h, cudaMemsetAsync(g, 0, n_suf * sizeof(uint64_t), h->stream));
+        API_CHECK(h, cudaMemsetAsync(g, 0, n_suf * gw, h->stream));
         return SETBWTE_OK;
     }
     if (h->world <= 1) {
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_blk(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->m, n_suf - (j1 - j0), g,
-                                          h->rank_ilp));
+                                          gw, h->rank_ilp));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
     uint64_t* d_sl;
     API_CHECK(h, ensure(h->small, 2 * (size_t)h->world + 8, &d_sl));
     API_CHECK(h, launch_slices(h->prof, h->stream, pk.slot_off, j0, j1, h->world, d_sl));
-    std::vector<uint64_t> sl(h->world + 1), so(h->world + 1);
+    std::vector<uint64_t> sl(h->world + 1);
     API_CHECK(h, cudaMemcpyAsync(sl.data(), d_sl, sizeof(uint64_t) * (h->world + 1),
                                  cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
@@ -263,9 +263,9 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     const uint64_t steps = (slot_of[h->rank + 1] - slot_of[h->rank]) - (b - a);
     API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
                                       cur_blk(h), cur_sb(h), (const uint64_t*)h->d_C.p, h->m,
-                                      steps, g, h->rank_ilp));
+                                      steps, g, gw, h->rank_ilp));
     std::vector<uint64_t> bytes(h->world);
-    for (int r = 0; r < h->world; ++r) bytes[r] = 8 * (slot_of[r + 1] - slot_of[r]);
+    for (int r = 0; r < h->world; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
     if (!h->allgather) return SETBWTE_E_STATE;
     int rc = h->allgather(g, bytes.data(), h->world, (void*)h->stream, h->allgather_ctx);
     if (rc != 0) return SETBWTE_E_STATE;
@@ -277,6 +277,8 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
 setbwte_status process_block(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1, uint64_t S0,
                              uint64_t S1) {
     const uint64_t n_suf = S1 - S0;
+    // g / pos width: u32 while every position of the new B_ext fits
+    const int gw = (h->n + n_suf) < (1ull << 32) ? 4 : 8;
     uint32_t* saf;
     uint64_t *g, *pos;
     uint8_t* bint;
@@ -288,11 +290,11 @@ setbwte_status process_block(setbwte_t h, const Packed& pk, uint64_t j0, uint64_
     API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, S0, (uint32_t)n_suf,
                             saf, &h->sstats));
     // g := ComputeRanks(S_jk, B_ext)
-    setbwte_status st = compute_ranks_for(h, pk, j0, j1, S0, n_suf, g);
+    setbwte_status st = compute_ranks_for(h, pk, j0, j1, S0, n_suf, g, gw);
     if (st != SETBWTE_OK) return st;
     // B_int := B(S_jk, SA_int) and g_sa / pos, fused
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, S0, saf, g, (uint32_t)n_suf,
-                               pos, bint));
+                               pos, gw, bint));
     // B_ext := Insert(B_int, g_sa, B_ext)
     const uint64_t n_out = h->n + n_suf;
     const uint64_t nblk = (n_out >> 6) + 1;
@@ -304,7 +306,7 @@ setbwte_status process_block(setbwte_t h, const Packed& pk, uint64_t j0, uint64_
     API_CHECK(h, ensure(h->sb[nxt], nsb * 4, &osb));
     API_CHECK(h, ensure(h->sb_tot, nsb * 4, &tot));
     const uint64_t m_new = h->m + (j1 - j0);
-    API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, bint, n_suf, ob, osb,
+    API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_suf, ob, osb,
                                tot, m_new, (uint64_t*)h->d_C.p));
     h->cur = nxt;
     h->n = n_out;
@@ -613,7 +615,7 @@ setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const u
     API_CHECK(h, sort_block(h->prof, h->stream, h->sort, po.pk.text, po.pk.term, 0,
                             (uint32_t)n_suf, saf, nullptr));
     API_CHECK(h, launch_gather(h->prof, h->stream, po.pk.text, po.pk.term, 0, saf, nullptr,
-                               (uint32_t)n_suf, pos, bint));
+                               (uint32_t)n_suf, pos, 8, bint));
     API_CHECK(h, launch_bint_ascii(h->prof, h->stream, bint, (uint32_t)n_suf,
                                    (const uint8_t*)h->d_sym.p, asc));
     if (sa_out)
@@ -642,7 +644,7 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
     if (st != SETBWTE_OK) return st;
     uint64_t* g;
     API_CHECK(h, ensure(h->g, n_suf, &g));
-    st = compute_ranks_for(h, po.pk, 0, m, 0, n_suf, g);
+    st = compute_ranks_for(h, po.pk, 0, m, 0, n_suf, g, 8);
     if (st != SETBWTE_OK) return st;
     API_CHECK(h, cudaMemcpyAsync(g_out, g, n_suf * 8, cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));

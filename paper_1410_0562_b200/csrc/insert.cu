@@ -18,15 +18,16 @@
 namespace setbwte {
 
 namespace {
-constexpr int kInsNt = 512;
+constexpr int kInsNt = 1024;  // one thread per output word of a superblock
+static_assert(kInsNt == kBlkPerSb, "insert: one thread per Blk of the superblock");
 constexpr int kInsWarps = kInsNt / 32;
 
-__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* __restrict__ a, uint64_t n,
-                                                    uint64_t x) {
+template <class G>
+__device__ __forceinline__ uint64_t lower_bound_g(const G* __restrict__ a, uint64_t n, uint64_t x) {
     uint64_t lo = 0, hi = n;
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
+        if ((uint64_t)__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
@@ -36,165 +37,132 @@ __device__ __forceinline__ uint64_t funnel(uint64_t a, uint64_t b, uint32_t sh) 
 }
 }  // namespace
 
+template <class G>
 __global__ void __launch_bounds__(kInsNt) insert_kernel(
-    const Blk* __restrict__ in_blk, uint64_t n_in, const uint64_t* __restrict__ pos,
+    const Blk* __restrict__ in_blk, uint64_t n_in, const G* __restrict__ pos,
     const uint8_t* __restrict__ bint, uint64_t n_ins, Blk* __restrict__ out_blk, uint64_t n_out,
     uint64_t* __restrict__ sb_tot) {
-    __shared__ uint32_t wstart[kBlkPerSb + 1];
-    __shared__ uint64_t w_lo[kBlkPerSb], w_hi[kBlkPerSb], w_dol[kBlkPerSb];
-    __shared__ uint16_t w_cnt[4][kBlkPerSb];
-    __shared__ uint32_t scan_tmp[kInsWarps][4];
+    __shared__ uint32_t wcnt[kBlkPerSb];
+    __shared__ uint32_t wsum[kInsWarps][4];
     __shared__ uint64_t i_range[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
     for (uint64_t sbi = blockIdx.x; sbi < nsb; sbi += gridDim.x) {
         const uint64_t o0 = sbi << kSbShift;
-        if (tid == 0) i_range[0] = lower_bound_u64(pos, n_ins, o0);
-        if (tid == 32) i_range[1] = lower_bound_u64(pos, n_ins, o0 + (1ull << kSbShift));
-        for (uint32_t w = tid; w <= (uint32_t)kBlkPerSb; w += kInsNt) wstart[w] = 0;
+        if (tid == 0) i_range[0] = lower_bound_g(pos, n_ins, o0);
+        if (tid == 32) i_range[1] = lower_bound_g(pos, n_ins, o0 + (1ull << kSbShift));
+        wcnt[tid] = 0;
         __syncthreads();
         const uint64_t i_lo = i_range[0], i_hi = i_range[1];
         for (uint64_t i = i_lo + tid; i < i_hi; i += kInsNt)
-            atomicAdd(&wstart[(uint32_t)((__ldg(pos + i) - o0) >> 6)], 1u);
+            atomicAdd(&wcnt[(uint32_t)(((uint64_t)__ldg(pos + i) - o0) >> 6)], 1u);
         __syncthreads();
-        // exclusive scan of wstart[0..1024) -> wstart, wstart[1024] = total
-        {
-            const uint32_t a0 = wstart[2 * tid], a1 = wstart[2 * tid + 1];
-            uint32_t incl = a0 + a1;
+        // exclusive scan over the 1024 words: a = first inserted index of word tid
+        const uint32_t cnt = wcnt[tid];
+        uint32_t incl = cnt;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= (uint32_t)o) incl += y;
-            }
-            if (lane == 31) scan_tmp[warp][0] = incl;
-            __syncthreads();
-            uint32_t pre = 0;
-            for (uint32_t w = 0; w < warp; ++w) pre += scan_tmp[w][0];
-            const uint32_t ex = pre + incl - a0 - a1;
-            __syncthreads();
-            wstart[2 * tid] = ex;
-            wstart[2 * tid + 1] = ex + a0;
-            if (tid == kInsNt - 1) wstart[kBlkPerSb] = ex + a0 + a1;
-            __syncthreads();
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
         }
-        const uint64_t span = n_out - o0;  // >= 0 by the grid range
-        const uint32_t wmax = (uint32_t)min((uint64_t)kBlkPerSb, (span >> 6) + 1);
-        for (uint32_t w = warp; w < wmax; w += kInsWarps) {
-            const uint64_t ow0 = o0 + ((uint64_t)w << 6);
-            const uint64_t a = i_lo + wstart[w];
-            const uint32_t cnt = wstart[w + 1] - wstart[w];
-            uint64_t M = 0;
-            for (uint32_t q = lane; q < cnt; q += 32) M |= 1ull << (__ldg(pos + a + q) - ow0);
-            const uint32_t Mlo = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)M);
-            const uint32_t Mhi = __reduce_or_sync(0xFFFFFFFFu, (uint32_t)(M >> 32));
-            M = ((uint64_t)Mhi << 32) | Mlo;
-            // window of 64 external symbols starting at e_base = ow0 - a
-            const uint64_t e_base = ow0 - a;
+        if (lane == 31) wsum[warp][0] = incl;
+        __syncthreads();
+        uint32_t pre = 0;
+        for (uint32_t w = 0; w < warp; ++w) pre += wsum[w][0];
+        const uint64_t a = i_lo + pre + incl - cnt;
+        // one thread merges one 64-symbol output word
+        const uint64_t ow0 = o0 + ((uint64_t)tid << 6);
+        const bool wvalid = ow0 <= n_out;
+        uint64_t ol = 0, oh = 0, od = 0;
+        uint32_t c4[4] = {0, 0, 0, 0};
+        if (wvalid) {
+            const uint64_t e0 = ow0 - a;  // external symbols before this word
             uint64_t xl = 0, xh = 0, xd = 0;
-            if (e_base < n_in) {
-                const uint64_t eb = e_base >> 6;
-                const uint32_t sh = (uint32_t)(e_base & 63);
+            if (e0 < n_in) {
+                const uint64_t eb = e0 >> 6;
+                const uint32_t sh = (uint32_t)(e0 & 63);
                 const Blk* b0 = in_blk + eb;
-                const uint64_t l0 = __ldg(&b0->lo), h0 = __ldg(&b0->hi), d0 = __ldg(&b0->dol);
+                const ulonglong2 p0 = __ldg(reinterpret_cast<const ulonglong2*>(b0) + 1);
+                const uint64_t l0 = __ldg(&b0->lo);
                 uint64_t l1 = 0, h1 = 0, d1 = 0;
                 if (sh != 0 && ((eb + 1) << 6) < n_in) {
                     l1 = __ldg(&b0[1].lo);
-                    h1 = __ldg(&b0[1].hi);
-                    d1 = __ldg(&b0[1].dol);
+                    const ulonglong2 p1 = __ldg(reinterpret_cast<const ulonglong2*>(b0 + 1) + 1);
+                    h1 = p1.x;
+                    d1 = p1.y;
                 }
                 xl = funnel(l0, l1, sh);
-                xh = funnel(h0, h1, sh);
-                xd = funnel(d0, d1, sh);
+                xh = funnel(p0.x, h1, sh);
+                xd = funnel(p0.y, d1, sh);
             }
-            uint32_t code[2], dol[2];
+            uint32_t filled = 0, used = 0;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const uint32_t t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
+                const uint32_t run = t - filled;
+                if (run) {
+                    const uint64_t m = (1ull << run) - 1ull;
+                    ol |= ((xl >> used) & m) << filled;
+                    oh |= ((xh >> used) & m) << filled;
+                    od |= ((xd >> used) & m) << filled;
+                    used += run;
+                }
+                const uint64_t b = __ldg(bint + a + k);
+                ol |= (b & 1ull) << t;
+                oh |= ((b >> 1) & 1ull) << t;
+                od |= ((b >> 2) & 1ull) << t;
+                filled = t + 1;
+            }
+            const uint64_t span = n_out - ow0;
+            const uint32_t lim = span >= 64 ? 64u : (uint32_t)span;
+            if (lim > filled) {
+                const uint32_t run = lim - filled;
+                const uint64_t m = run == 64 ? ~0ull : (1ull << run) - 1ull;
+                ol |= ((xl >> used) & m) << filled;
+                oh |= ((xh >> used) & m) << filled;
+                od |= ((xd >> used) & m) << filled;
+            }
+            const uint64_t V = lim == 64 ? ~0ull : ((1ull << lim) - 1ull);  // real positions
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t t = lane + 32 * h;
-                const uint32_t r = __popcll(M & ((1ull << t) - 1ull));
-                if ((M >> t) & 1ull) {
-                    const uint8_t b = __ldg(bint + a + r);
-                    code[h] = b & 3u;
-                    dol[h] = b >> 2;
-                } else {
-                    const uint32_t x = t - r;
-                    code[h] = (uint32_t)(((xl >> x) & 1ull) | (((xh >> x) & 1ull) << 1));
-                    dol[h] = (uint32_t)((xd >> x) & 1ull);
-                }
-                if (ow0 + t >= n_out) {
-                    code[h] = 0;
-                    dol[h] = 0;
-                }
-            }
-            const uint64_t lo = (uint64_t)__ballot_sync(0xFFFFFFFFu, code[0] & 1u) |
-                                ((uint64_t)__ballot_sync(0xFFFFFFFFu, code[1] & 1u) << 32);
-            const uint64_t hi = (uint64_t)__ballot_sync(0xFFFFFFFFu, code[0] >> 1) |
-                                ((uint64_t)__ballot_sync(0xFFFFFFFFu, code[1] >> 1) << 32);
-            const uint64_t dl = (uint64_t)__ballot_sync(0xFFFFFFFFu, dol[0]) |
-                                ((uint64_t)__ballot_sync(0xFFFFFFFFu, dol[1]) << 32);
-            if (lane < 4) {
-                const uint64_t V = (n_out - ow0 >= 64) ? ~0ull : ((1ull << (n_out - ow0)) - 1ull);
-                w_cnt[lane][w] = (uint16_t)__popcll(match_plane(lane, lo, hi, dl) & V);
-            }
-            if (lane == 0) {
-                w_lo[w] = lo;
-                w_hi[w] = hi;
-                w_dol[w] = dl;
-            }
+            for (int c = 0; c < 4; ++c) c4[c] = __popcll(match_plane(c, ol, oh, od) & V);
         }
-        __syncthreads();
-        // exclusive scan of the per-word counts (4 codes) over the superblock
-        {
-            uint32_t v0[4], v1[4], incl[4];
-            const uint32_t wa = 2 * tid, wb = 2 * tid + 1;
+        // in-superblock exclusive prefix of the per-word counts (4 codes)
+        uint32_t inc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) inc[c] = c4[c];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                v0[c] = wa < wmax ? w_cnt[c][wa] : 0u;
-                v1[c] = wb < wmax ? w_cnt[c][wb] : 0u;
-                incl[c] = v0[c] + v1[c];
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc[c], o);
+                if (lane >= (uint32_t)o) inc[c] += y;
             }
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl[c], o);
-                    if (lane >= (uint32_t)o) incl[c] += y;
-                }
-            }
-            if (lane == 31) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) scan_tmp[warp][c] = incl[c];
-            }
-            __syncthreads();
-            uint32_t pre[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
-            for (uint32_t w = 0; w < (uint32_t)kInsWarps; ++w) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (w < warp) pre[c] += scan_tmp[w][c];
-                    tot[c] += scan_tmp[w][c];
-                }
-            }
-            Blk* ob = out_blk + (sbi << (kSbShift - 6));
-            if (wa < wmax) {
-                Blk b;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) b.cnt[c] = (uint16_t)(pre[c] + incl[c] - v0[c] - v1[c]);
-                b.lo = w_lo[wa];
-                b.hi = w_hi[wa];
-                b.dol = w_dol[wa];
-                ob[wa] = b;
-            }
-            if (wb < wmax) {
-                Blk b;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) b.cnt[c] = (uint16_t)(pre[c] + incl[c] - v1[c]);
-                b.lo = w_lo[wb];
-                b.hi = w_hi[wb];
-                b.dol = w_dol[wb];
-                ob[wb] = b;
-            }
-            if (tid < 4) sb_tot[sbi * 4 + tid] = tot[tid];
-            __syncthreads();
         }
+        __syncthreads();  // wsum reuse
+        if (lane == 31) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) wsum[warp][c] = inc[c];
+        }
+        __syncthreads();
+        uint32_t pw[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
+        for (uint32_t w = 0; w < (uint32_t)kInsWarps; ++w) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t v = wsum[w][c];
+                if (w < warp) pw[c] += v;
+                tot[c] += v;
+            }
+        }
+        if (wvalid) {
+            Blk b;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) b.cnt[c] = (uint16_t)(pw[c] + inc[c] - c4[c]);
+            b.lo = ol;
+            b.hi = oh;
+            b.dol = od;
+            out_blk[(sbi << (kSbShift - 6)) + tid] = b;
+        }
+        if (tid < 4) sb_tot[sbi * 4 + tid] = tot[tid];
+        __syncthreads();
     }
 }
 
@@ -238,16 +206,25 @@ __global__ void __launch_bounds__(1024) sb_scan_kernel(const uint64_t* __restric
 }
 
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
-                          const uint64_t* pos, const uint8_t* bint, uint64_t n_ins,
+                          const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot, uint64_t m_new,
                           uint64_t* d_C) {
     const uint64_t n_out = n_in + n_ins;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
-    // algorithmic bytes: read n_in/2 + write n_out/2 (4 bits/symbol) + 9 B per inserted
-    const double bytes = 0.5 * (double)n_in + 0.5 * (double)n_out + 9.0 * (double)n_ins;
-    SB_LAUNCH(prof, s, "insert", bytes, n_out,
-              insert_kernel<<<(unsigned)(nsb < 148u * 64u ? nsb : 148u * 64u), kInsNt, 0, s>>>(
-                  in_blk, n_in, pos, bint, n_ins, out_blk, n_out, sb_tot));
+    // algorithmic bytes: read n_in/2 + write n_out/2 (4 bits/symbol) + (gw + 1) B per inserted
+    const double bytes = 0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins;
+    const unsigned grid = (unsigned)(nsb < 148u * 64u ? nsb : 148u * 64u);
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "insert", bytes, n_out,
+                  insert_kernel<uint32_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint32_t*)pos,
+                                                                   bint, n_ins, out_blk, n_out,
+                                                                   sb_tot));
+    } else {
+        SB_LAUNCH(prof, s, "insert", bytes, n_out,
+                  insert_kernel<uint64_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint64_t*)pos,
+                                                                   bint, n_ins, out_blk, n_out,
+                                                                   sb_tot));
+    }
     SB_CHECK(cudaGetLastError());
     SB_LAUNCH(prof, s, "sb_scan", 64.0 * nsb, nsb,
               sb_scan_kernel<<<1, 1024, 0, s>>>(sb_tot, nsb, out_sb, m_new, d_C));

@@ -125,15 +125,16 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
 cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
-                                 const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps,
-                                 uint64_t* g, int ilp);
+                                 const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
+                                 int gw, int ilp);
+// g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64)
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
-                          const uint64_t* g, uint32_t n_suf, uint64_t* pos, uint8_t* bint);
+                          const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
-                          const uint64_t* pos, const uint8_t* bint, uint64_t n_ins,
+                          const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot, uint64_t m_new,
                           uint64_t* d_C);
 cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,

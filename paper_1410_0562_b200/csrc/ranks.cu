@@ -13,21 +13,26 @@
 //     s = SA_int[i];  B_int[i] = P[k-1] or '$';  pos[i] = g[s] + i
 // where pos[i] = g_sa[i] + i is the final position of B_int[i] in the new
 // B_ext (reading R4).
+//
+// g and pos are stored as u32 while the index stays below 2^32 symbols and as
+// u64 beyond (G = uint32_t / uint64_t): the narrower g of one block is small
+// enough to stay L2-resident between ComputeRanks and the gather.
 #include "internal.h"
 
 namespace setbwte {
 
+template <class G>
 __global__ void __launch_bounds__(256) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
     uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
-    const uint64_t* __restrict__ Cd, uint64_t m_ext, uint64_t* __restrict__ g) {
+    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
     for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
          j += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t s0 = slot_off[j];
         const uint64_t e = slot_off[j + 1] - 1;  // terminator slot
         uint64_t i = m_ext;
-        g[e - slot_base] = i;
+        g[e - slot_base] = (G)i;
         uint64_t p = e;
         uint64_t wi = ~0ull;
         uint32_t word = 0;
@@ -40,7 +45,7 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
             const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
             const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
             i = Cc + dict_rank(blk, sb, c, i);
-            g[p - slot_base] = i;
+            g[p - slot_base] = (G)i;
         }
     }
 }
@@ -48,29 +53,38 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
 cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
-                                 const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps,
-                                 uint64_t* g, int ilp) {
+                                 const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
+                                 int gw, int ilp) {
     (void)ilp;
     if (j1 <= j0) return cudaSuccess;
-    // algorithmic bytes per LF step (= base): one 32 B Blk sector + 8 B g write
-    // + 0.25 B packed symbol; per string: 16 B slot offsets + 8 B terminator g
+    // algorithmic bytes per LF step (= base): one 32 B Blk sector + g write
+    // + 0.25 B packed symbol; per string: 16 B slot offsets + the terminator g
     // (DESIGN.md "Rooflines").  Units = LF steps.
     const uint64_t nstr = j1 - j0;
-    SB_LAUNCH(prof, s, "compute_ranks", 40.25 * (double)n_steps + 24.0 * (double)nstr, n_steps,
-              compute_ranks_kernel<<<grid_for(nstr, 256, 1u << 20), 256, 0, s>>>(
-                  text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, g));
+    const double bytes = (32.25 + gw) * (double)n_steps + (16.0 + gw) * (double)nstr;
+    const unsigned grid = grid_for(nstr, 256, 1u << 20);
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                  compute_ranks_kernel<uint32_t><<<grid, 256, 0, s>>>(
+                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g));
+    } else {
+        SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                  compute_ranks_kernel<uint64_t><<<grid, 256, 0, s>>>(
+                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g));
+    }
     return cudaGetLastError();
 }
 
+template <class G>
 __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
                               uint64_t slot_base, const uint32_t* __restrict__ sa,
-                              const uint64_t* __restrict__ g, uint32_t n_suf,
-                              uint64_t* __restrict__ pos, uint8_t* __restrict__ bint) {
+                              const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
+                              uint8_t* __restrict__ bint) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_suf;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t sl = sa[i];
         const uint64_t p = slot_base + sl;
-        pos[i] = (g ? g[sl] : 0ull) + i;
+        pos[i] = (G)((g ? (uint64_t)__ldg(g + sl) : 0ull) + i);
         uint8_t b;
         if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
         else b = (uint8_t)text_sym(text, p - 1);
@@ -80,11 +94,21 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
 
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
-                          const uint64_t* g, uint32_t n_suf, uint64_t* pos, uint8_t* bint) {
-    // bytes per suffix: 4 (SA) + 8 (g) + 8 (pos) + 1 (B_int) + 0.375 (symbol + term bit)
-    SB_LAUNCH(prof, s, "gather", 21.375 * n_suf, n_suf,
-              gather_kernel<<<grid_for(n_suf, 256, 148u * 64u), 256, 0, s>>>(
-                  text, term, slot_base, sa, g, n_suf, pos, bint));
+                          const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint) {
+    // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol + term bit)
+    const double bytes = (5.375 + 2.0 * gw) * n_suf;
+    const unsigned grid = grid_for(n_suf, 256, 148u * 64u);
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "gather", bytes, n_suf,
+                  gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
+                                                               (const uint32_t*)g, n_suf,
+                                                               (uint32_t*)pos, bint));
+    } else {
+        SB_LAUNCH(prof, s, "gather", bytes, n_suf,
+                  gather_kernel<uint64_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
+                                                               (const uint64_t*)g, n_suf,
+                                                               (uint64_t*)pos, bint));
+    }
     return cudaGetLastError();
 }
 

@@ -51,7 +51,7 @@ enum { TINY = 0, SMALL = 1, MEDIUM = 2, LARGE = 3, NCLASS = 4 };
 enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_N };
 
 struct Seg {
-    uint32_t start, len, word, meta;  // meta: shift | buf << 8 | keys_valid << 9
+    uint32_t start, len, word, meta;  // meta: shift | buf<<8 | keys_valid<<9 | iota<<10
 };
 struct SegX {
     uint32_t chunk_base, nchunks, chunk_len, skip;
@@ -75,8 +75,10 @@ struct Bufs {
 __device__ __forceinline__ uint32_t meta_shift(uint32_t m) { return m & 0xFF; }
 __device__ __forceinline__ uint32_t meta_buf(uint32_t m) { return (m >> 8) & 1; }
 __device__ __forceinline__ uint32_t meta_kv(uint32_t m) { return (m >> 9) & 1; }
-__device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint32_t kv) {
-    return shift | (buf << 8) | (kv << 9);
+__device__ __forceinline__ uint32_t meta_iota(uint32_t m) { return (m >> 10) & 1; }
+__device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint32_t kv,
+                                              uint32_t iota = 0) {
+    return shift | (buf << 8) | (kv << 9) | (iota << 10);
 }
 __device__ __forceinline__ int class_of(uint32_t len) {
     return len <= kTiny ? TINY : len <= kCapS ? SMALL : len <= kCapM ? MEDIUM : LARGE;
@@ -92,11 +94,15 @@ __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
 // remain, entirely in registers.  Returns the lane's slot in final order.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint32_t word,
-                                                uint32_t key0, bool have_key, const Bufs& B) {
+                                                uint32_t key0, bool have_key, const Bufs& B,
+                                                uint32_t group0 = 0) {
+    // Several independent runs may be packed into one call: lanes [g, g+len)
+    // of each run carry group0 = g (its first lane); runs never mix because
+    // the composite sorts by group first.
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = lane < L;
     bool active = valid;
-    uint32_t group = 0;
+    uint32_t group = group0;
     for (;;) {
         uint32_t key = 0;
         if (active) key = have_key ? key0 : suffix_key(B.text, B.term, B.base + slot, word);
@@ -196,6 +202,50 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
 }
 
 // ---------------------------------------------------------------------------
+// Key word 0 of every slot of the block (the first MSD pass's keys): 16
+// consecutive slots per thread share 3 text words and 2 terminator words;
+// 64-byte vector stores.  Same encoding as suffix_key (common.cuh).
+// ---------------------------------------------------------------------------
+__global__ void keygen_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
+                              uint64_t base, uint32_t n, uint32_t* __restrict__ key) {
+    const uint32_t ng = (n + 15) >> 4;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+        const uint64_t p0 = base + 16ull * g;
+        const uint64_t w = p0 >> 4;
+        const uint32_t off = (uint32_t)(p0 & 15);
+        const uint32_t t0 = __ldg(text + w), t1 = __ldg(text + w + 1), t2 = __ldg(text + w + 2);
+        const uint64_t v01 = ((uint64_t)t0 << 32) | t1, v12 = ((uint64_t)t1 << 32) | t2;
+        const uint64_t tb = p0 >> 5;
+        const uint32_t toff = (uint32_t)(p0 & 31);
+        const uint64_t T = ((uint64_t)__ldg(term + tb) << 32) | __ldg(term + tb + 1);
+        uint32_t k[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t o = off + j;
+            const uint64_t v = o < 16 ? (v01 << (2 * o)) : (v12 << (2 * (o - 16)));
+            uint32_t syms = (uint32_t)(v >> 36);
+            uint32_t ended = (uint32_t)__clzll((long long)(T << (toff + j)));
+            ended = ended > (uint32_t)kKeySyms ? (uint32_t)kKeySyms : ended;
+            const uint32_t keep = 2 * ended;
+            const uint32_t mask = keep == 0 ? 0u : (0x0FFFFFFFu & ~((1u << (28 - keep)) - 1u));
+            k[j] = ((syms & mask) << 4) | ended;
+        }
+        const uint32_t i0 = 16 * g;
+        if (i0 + 16 <= n) {
+            uint4* dst = reinterpret_cast<uint4*>(key + i0);
+            dst[0] = make_uint4(k[0], k[1], k[2], k[3]);
+            dst[1] = make_uint4(k[4], k[5], k[6], k[7]);
+            dst[2] = make_uint4(k[8], k[9], k[10], k[11]);
+            dst[3] = make_uint4(k[12], k[13], k[14], k[15]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (i0 + j < n) key[i0 + j] = k[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // init / control
 // ---------------------------------------------------------------------------
 __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ saf, uint32_t n,
@@ -210,7 +260,7 @@ __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ s
         }
         for (int c = 0; c < M_N; ++c) misc[c] = 0;
         if (n == 1) saf[0] = 0;
-        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 0)});
+        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 1, 1)});
     }
 }
 
@@ -297,68 +347,98 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
     }
 }
 
-__global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
-                                                         SegX* __restrict__ segx,
-                                                         uint32_t* __restrict__ hist,
-                                                         uint32_t* __restrict__ dbase) {
+__global__ void __launch_bounds__(1024) digit_scan_kernel(Lists in, Lists out,
+                                                          SegX* __restrict__ segx,
+                                                          uint32_t* __restrict__ hist,
+                                                          uint32_t* __restrict__ dbase) {
+    constexpr int kParts = 4;
+    __shared__ uint32_t psum[kParts][256];
     __shared__ uint32_t wsum[8];
+    __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
     __shared__ int all_one;
     const uint32_t n = in.cnt[LARGE];
-    const uint32_t d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    const uint32_t t = threadIdx.x, d = t & 255, part = t >> 8, lane = t & 31, warp = t >> 5;
     for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
         const Seg s = in.seg[LARGE][si];
         const SegX x = segx[si];
-        uint32_t run = 0;
+        // chunk counts of digit d, split into kParts contiguous ranges
+        const uint32_t c_lo = x.chunk_base + (uint32_t)((uint64_t)x.nchunks * part / kParts);
+        const uint32_t c_hi = x.chunk_base + (uint32_t)((uint64_t)x.nchunks * (part + 1) / kParts);
         constexpr int kB = 16;
-        for (uint32_t c0 = x.chunk_base; c0 < x.chunk_base + x.nchunks; c0 += kB) {
+        uint32_t sum = 0;
+        for (uint32_t c0 = c_lo; c0 < c_hi; c0 += kB) {
             uint32_t v[kB];
-            const uint32_t cn = min((uint32_t)kB, x.chunk_base + x.nchunks - c0);
 #pragma unroll
-            for (int b = 0; b < kB; ++b) v[b] = (uint32_t)b < cn ? hist[(size_t)(c0 + b) * 256 + d] : 0u;
+            for (int b = 0; b < kB; ++b) v[b] = c0 + b < c_hi ? hist[(size_t)(c0 + b) * 256 + d] : 0u;
+#pragma unroll
+            for (int b = 0; b < kB; ++b) sum += v[b];
+        }
+        psum[part][d] = sum;
+        if (t < NCLASS) ccount[t] = 0;
+        if (t == 0) all_one = 0;
+        __syncthreads();
+        uint32_t run = 0;
+        for (uint32_t q = 0; q < part; ++q) run += psum[q][d];
+        uint32_t total = 0;
+        for (uint32_t q = 0; q < kParts; ++q) total += psum[q][d];
+        for (uint32_t c0 = c_lo; c0 < c_hi; c0 += kB) {
+            uint32_t v[kB];
+#pragma unroll
+            for (int b = 0; b < kB; ++b) v[b] = c0 + b < c_hi ? hist[(size_t)(c0 + b) * 256 + d] : 0u;
 #pragma unroll
             for (int b = 0; b < kB; ++b) {
-                if ((uint32_t)b < cn) hist[(size_t)(c0 + b) * 256 + d] = run;
+                if (c0 + b < c_hi) hist[(size_t)(c0 + b) * 256 + d] = run;
                 run += v[b];
             }
         }
-        if (d == 0) all_one = 0;
-        uint32_t incl = run;
+        // exclusive scan of the digit totals (threads of part 0)
+        uint32_t excl = 0;
+        if (part == 0) {
+            uint32_t incl = total;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
-        }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        uint32_t wpre = 0;
-        for (uint32_t w = 0; w < warp; ++w) wpre += wsum[w];
-        const uint32_t excl = wpre + incl - run;
-        if (run == s.len) all_one = 1;
-        __syncthreads();
-        const uint32_t shift = meta_shift(s.meta);
-        const uint32_t buf = meta_buf(s.meta);
-        const bool resolved = (run == 1) || (shift == 0 && (d & 15u) < (uint32_t)kKeySyms);
-        uint32_t flag = 0;
-        if (run > 0) {
-            if (resolved) {
-                flag = 0x80000000u;
-            } else {
-                const uint32_t cbuf = all_one ? buf : 1u - buf;
-                Seg c;
-                c.start = s.start + excl;
-                c.len = run;
-                if (shift == 0) {
-                    c.word = s.word + 1;
-                    c.meta = make_meta(24, cbuf, 0);
-                } else {
-                    c.word = s.word;
-                    c.meta = make_meta(shift - 8, cbuf, 1);
-                }
-                emit(out, c);
-                if (all_one) segx[si].skip = 1;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
             }
+            if (lane == 31) wsum[warp] = incl;
+            if (total == s.len) all_one = 1;
+            excl = incl - total;
         }
-        dbase[(size_t)si * 256 + d] = (s.start + excl) | flag;
+        __syncthreads();
+        int cls = -1;
+        Seg c;
+        uint32_t local = 0;
+        if (part == 0) {
+            for (uint32_t w = 0; w < warp; ++w) excl += wsum[w];
+            const uint32_t shift = meta_shift(s.meta);
+            const uint32_t buf = meta_buf(s.meta);
+            const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < (uint32_t)kKeySyms);
+            uint32_t flag = 0;
+            if (total > 0) {
+                if (resolved) {
+                    flag = 0x80000000u;
+                } else {
+                    const uint32_t cbuf = all_one ? buf : 1u - buf;
+                    c.start = s.start + excl;
+                    c.len = total;
+                    if (shift == 0) {
+                        c.word = s.word + 1;
+                        c.meta = make_meta(24, cbuf, 0);
+                    } else {
+                        c.word = s.word;
+                        c.meta = make_meta(shift - 8, cbuf, 1);
+                    }
+                    cls = class_of(total);
+                    local = atomicAdd(&ccount[cls], 1u);
+                    if (all_one) segx[si].skip = 1;
+                }
+            }
+            dbase[(size_t)si * 256 + d] = (s.start + excl) | flag;
+        }
+        __syncthreads();
+        if (t < NCLASS && ccount[t]) cbase[t] = atomicAdd(out.cnt + t, ccount[t]);
+        __syncthreads();
+        if (cls >= 0) out.seg[cls][cbase[cls] + local] = c;
         __syncthreads();
     }
 }
@@ -385,6 +465,7 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
         const uint32_t buf = meta_buf(s.meta);
         const uint32_t* S = B.sa[buf];
         const uint32_t* K = B.key[buf];
+        const bool iota = meta_iota(s.meta);
         uint32_t* S2 = B.sa[1 - buf];
         uint32_t* K2 = B.key[1 - buf];
         if (tid < 256) {
@@ -400,7 +481,7 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
                 const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
                 const bool valid = e < tn;
                 key[it] = valid ? K[t0 + e] : 0u;
-                slot[it] = valid ? S[t0 + e] : 0u;
+                slot[it] = valid ? (iota ? t0 + e : S[t0 + e]) : 0u;
                 dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
             }
             block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
@@ -567,8 +648,10 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
             }
         }
         __syncwarp();
-        // ties on this word with 14 real symbols: finish runs <= 32 here, emit
-        // longer runs as segments of the next word
+        // ties on this word with 14 real symbols: runs <= 32 are packed into
+        // shared warp_finish calls, longer runs become segments of the next word
+        uint32_t lb = 0, my_pos = 0, my_grp = 0;
+        bool mine = false;
         for (uint32_t it = 0; it < nit; ++it) {
             const uint32_t e = it * 32 + lane;
             const uint32_t k = buf[e].x;
@@ -591,14 +674,29 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
                     }
                 }
                 if (Lr <= kTiny) {
-                    uint32_t sl = lane < Lr ? buf[rs + lane].y : 0u;
-                    sl = warp_finish(sl, Lr, s.word + 1, 0u, false, B);
-                    if (lane < Lr) B.saf[s.start + rs + lane] = sl;
+                    if (lb + Lr > 32) {
+                        uint32_t sl = mine ? buf[my_pos].y : 0u;
+                        sl = warp_finish(sl, lb, s.word + 1, 0u, false, B, my_grp);
+                        if (mine) B.saf[s.start + my_pos] = sl;
+                        lb = 0;
+                        mine = false;
+                    }
+                    if (lane >= lb && lane < lb + Lr) {
+                        mine = true;
+                        my_pos = rs + lane - lb;
+                        my_grp = lb;
+                    }
+                    lb += Lr;
                 } else {
                     for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = buf[rs + q].y;
                     if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
                 }
             }
+        }
+        if (lb) {
+            uint32_t sl = mine ? buf[my_pos].y : 0u;
+            sl = warp_finish(sl, lb, s.word + 1, 0u, false, B, my_grp);
+            if (mine) B.saf[s.start + my_pos] = sl;
         }
         __syncwarp();
     }
@@ -773,6 +871,11 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         attr_dev = dev;
     }
 
+    SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
+              keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(text, term,
+                                                                                  slot_base, n_suf,
+                                                                                  k0));
+    SB_CHECK(cudaGetLastError());
     SB_LAUNCH(prof, s, "sort_init", 4.0 * n, n,
               init_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc));
     SB_CHECK(cudaGetLastError());
@@ -816,7 +919,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                       digit_hist_kernel<<<g_dig, kDigNt, 0, s>>>(in, chunks, misc, B, hist));
             SB_CHECK(cudaGetLastError());
             SB_LAUNCH(prof, s, "digit_scan", 0, 0,
-                      digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 8u), 256, 0, s>>>(
+                      digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 2u), 1024, 0, s>>>(
                           in, out, segx, hist, dbase));
             SB_CHECK(cudaGetLastError());
             SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
