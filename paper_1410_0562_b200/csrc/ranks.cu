@@ -82,13 +82,15 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
                               uint8_t* __restrict__ bint) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_suf;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t sl = sa[i];
+        // streaming (evict-first) accesses for SA / pos / B_int keep the
+        // just-written g resident in L2 for the random gather
+        const uint32_t sl = __ldcs(sa + i);
         const uint64_t p = slot_base + sl;
-        pos[i] = (G)((g ? (uint64_t)__ldg(g + sl) : 0ull) + i);
+        __stcs(pos + i, (G)((g ? (uint64_t)__ldg(g + sl) : 0ull) + i));
         uint8_t b;
         if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
         else b = (uint8_t)text_sym(text, p - 1);
-        bint[i] = b;
+        __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
     }
 }
 

@@ -46,9 +46,12 @@ constexpr int kDigNt = 512;        // digit-pass CTA
 constexpr int kDigIpt = 8;
 constexpr int kDigTile = kDigNt * kDigIpt;
 
-enum { TINY = 0, SMALL = 1, MEDIUM = 2, LARGE = 3, NCLASS = 4 };
+// BIT2..BIT16: 33..512 members whose unknown key bits fit in 16 (keys valid,
+// shift <= 8): one warp sorts 32*NIT packed (key bits, index) u32 values with a
+// register bitonic network.  SMALL: the other 33..512 segments (warp LSD radix).
+enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MEDIUM, LARGE, NCLASS };
 // misc counters
-enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_N };
+enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_N };
 
 struct Seg {
     uint32_t start, len, word, meta;  // meta: shift | buf<<8 | keys_valid<<9 | iota<<10
@@ -80,12 +83,39 @@ __device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint
                                               uint32_t iota = 0) {
     return shift | (buf << 8) | (kv << 9) | (iota << 10);
 }
-__device__ __forceinline__ int class_of(uint32_t len) {
-    return len <= kTiny ? TINY : len <= kCapS ? SMALL : len <= kCapM ? MEDIUM : LARGE;
+__host__ __device__ __forceinline__ int class_of(const Seg& c) {
+    if (c.len <= kTiny) return TINY;
+    if (c.len <= kCapS) {
+        if (((c.meta >> 9) & 1) && (c.meta & 0xFF) <= 8)
+            return c.len <= 64 ? BIT2 : c.len <= 128 ? BIT4 : c.len <= 256 ? BIT8 : BIT16;
+        return SMALL;
+    }
+    return c.len <= kCapM ? MEDIUM : LARGE;
 }
 __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
-    const int k = class_of(c.len);
+    const int k = class_of(c);
     out.seg[k][atomicAdd(out.cnt + k, 1u)] = c;
+}
+
+// Lanes of the warp holding the same NB-bit digit (a ballot per bit: short
+// fixed latency, unlike MATCH.ANY whose result latency serialised the ranking
+// loops -- ncu, profiles/).
+template <int NB>
+__device__ __forceinline__ uint32_t peers_of(uint32_t d) {
+    uint32_t peers = 0xFFFFFFFFu;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const uint32_t bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -157,7 +187,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
 #pragma unroll
     for (int it = 0; it < IPT; ++it) {
         const uint32_t d = dig[it];
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t peers = peers_of<9>(d);
         const uint32_t leader = __ffs(peers) - 1;
         uint32_t b = 0;
         if (lane == leader && d < 256) {
@@ -165,7 +195,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
             mine[d] = b + __popc(peers);
         }
         b = __shfl_sync(0xFFFFFFFFu, b, leader);
-        dest[it] = b + __popc(peers & ((1u << lane) - 1u));
+        dest[it] = b + __popc(peers & lanemask_lt());
         __syncwarp();
     }
     __syncthreads();
@@ -315,25 +345,33 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
         const bool kv = meta_kv(s.meta);
         const uint32_t* S = B.sa[buf];
         uint32_t* K = B.key[buf];
-        for (uint32_t p0 = ch.begin; p0 < ch.end; p0 += kDigNt) {
-            const uint32_t p = p0 + tid;
-            const bool valid = p < ch.end;
-            uint32_t d = 0x100;
-            if (valid) {
-                uint32_t key;
-                if (kv) {
-                    key = K[p];
-                } else {
-                    key = suffix_key(B.text, B.term, B.base + S[p], s.word);
-                    K[p] = key;
+        constexpr int U = 8;
+        for (uint32_t p0 = ch.begin; p0 < ch.end; p0 += kDigNt * U) {
+            uint32_t key[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t p = p0 + u * kDigNt + tid;
+                key[u] = 0xFFFFFFFFu;
+                if (p < ch.end) {
+                    if (kv) {
+                        key[u] = __ldg(K + p);
+                    } else {
+                        key[u] = suffix_key(B.text, B.term, B.base + __ldg(S + p), s.word);
+                        K[p] = key[u];
+                    }
                 }
-                d = (key >> shift) & 0xFF;
             }
-            const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
-            if (__all_sync(0xFFFFFFFFu, d == d0)) {
-                if (lane == 0 && d0 < 256) atomicAdd(&h[warp][d0], 32u);
-            } else if (valid) {
-                atomicAdd(&h[warp][d], 1u);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t p = p0 + u * kDigNt + tid;
+                const uint32_t d = (key[u] >> shift) & 0xFFu;
+                const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+                const bool v = p < ch.end;
+                if (__all_sync(0xFFFFFFFFu, v && d == d0)) {
+                    if (lane == 0) atomicAdd(&h[warp][d0], 32u);
+                } else if (v) {
+                    atomicAdd(&h[warp][d], 1u);
+                }
             }
         }
         __syncthreads();
@@ -428,7 +466,7 @@ __global__ void __launch_bounds__(1024) digit_scan_kernel(Lists in, Lists out,
                         c.word = s.word;
                         c.meta = make_meta(shift - 8, cbuf, 1);
                     }
-                    cls = class_of(total);
+                    cls = class_of(c);
                     local = atomicAdd(&ccount[cls], 1u);
                     if (all_one) segx[si].skip = 1;
                 }
@@ -541,6 +579,147 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
 }
 
 // ---------------------------------------------------------------------------
+// Common tail of the warp sorts: buf[0..L) holds the segment's (key word,
+// slot) pairs in sorted order.  Write the final SA entries, then finish ties
+// on this word with 14 real symbols: runs <= 32 are packed into shared
+// warp_finish calls, longer runs become segments of the next word.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void warp_tail(const uint2* buf, const Seg& s, const Lists& out,
+                                          const Bufs& B) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t L = s.len;
+    const uint32_t nit = (L + 31) >> 5;
+    const uint32_t bid = meta_buf(s.meta);
+    for (uint32_t e = lane; e < L; e += 32) B.saf[s.start + e] = buf[e].y;
+        uint32_t lb = 0, my_pos = 0, my_grp = 0;
+        bool mine = false;
+        for (uint32_t it = 0; it < nit; ++it) {
+            const uint32_t e = it * 32 + lane;
+            const uint32_t k = buf[e].x;
+            const bool st = e < L && (e == 0 || buf[e - 1].x != k) && e + 1 < L &&
+                            buf[e + 1].x == k && (k & 15u) == (uint32_t)kKeySyms;
+            uint32_t m = __ballot_sync(0xFFFFFFFFu, st);
+            while (m) {
+                const uint32_t l = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t rs = it * 32 + l;
+                const uint32_t rk = buf[rs].x;
+                uint32_t Lr = 0;
+                for (uint32_t c = rs + 1;; c += 32) {
+                    const uint32_t q = c + lane;
+                    const bool eq = q < L && buf[q].x == rk;
+                    const uint32_t ne = __ballot_sync(0xFFFFFFFFu, !eq);
+                    if (ne) {
+                        Lr = c + (__ffs(ne) - 1) - rs;
+                        break;
+                    }
+                }
+                if (Lr <= kTiny) {
+                    if (lb + Lr > 32) {
+                        uint32_t sl = mine ? buf[my_pos].y : 0u;
+                        sl = warp_finish(sl, lb, s.word + 1, 0u, false, B, my_grp);
+                        if (mine) B.saf[s.start + my_pos] = sl;
+                        lb = 0;
+                        mine = false;
+                    }
+                    if (lane >= lb && lane < lb + Lr) {
+                        mine = true;
+                        my_pos = rs + lane - lb;
+                        my_grp = lb;
+                    }
+                    lb += Lr;
+                } else {
+                    for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = buf[rs + q].y;
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
+                }
+            }
+        }
+        if (lb) {
+            uint32_t sl = mine ? buf[my_pos].y : 0u;
+            sl = warp_finish(sl, lb, s.word + 1, 0u, false, B, my_grp);
+            if (mine) B.saf[s.start + my_pos] = sl;
+        }
+}
+
+// ---------------------------------------------------------------------------
+// BIT2..BIT16: one warp per segment, register bitonic network
+// ---------------------------------------------------------------------------
+// Ascending bitonic sort of N = 32*NIT values, lane-major (element e = lane*NIT
+// + r lives in register v[r] of lane e/NIT): strides below NIT stay in
+// registers, larger ones are one shuffle per value.
+template <int NIT>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[NIT]) {
+    constexpr int N = 32 * NIT;
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < NIT) {
+#pragma unroll
+                for (int r = 0; r < NIT; ++r) {
+                    if ((r & j) == 0) {
+                        const bool up = (((lane * NIT + r) & k) == 0);
+                        const uint32_t a = v[r], b = v[r | j];
+                        const uint32_t mn = min(a, b), mx = max(a, b);
+                        v[r] = up ? mn : mx;
+                        v[r | j] = up ? mx : mn;
+                    }
+                }
+            } else {
+                const int lj = j / NIT;
+                const bool lower = (lane & lj) == 0;
+#pragma unroll
+                for (int r = 0; r < NIT; ++r) {
+                    const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v[r], lj);
+                    const bool up = (((lane * NIT + r) & k) == 0);
+                    v[r] = (lower == up) ? min(v[r], o) : max(v[r], o);
+                }
+            }
+        }
+    }
+}
+
+template <int NIT>
+__global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists out, int cls,
+                                                               Bufs B, uint32_t* misc) {
+    constexpr int N = 32 * NIT;
+    constexpr int IDXB = NIT == 2 ? 6 : NIT == 4 ? 7 : NIT == 8 ? 8 : 9;
+    static_assert((1 << IDXB) == N, "index field");
+    __shared__ uint2 s_buf[kWarpCta][N];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint2* buf = s_buf[wib];
+    const uint32_t n = in.cnt[cls];
+    const uint32_t nw = gridDim.x * kWarpCta;
+    for (uint32_t si = blockIdx.x * kWarpCta + wib; si < n; si += nw) {
+        const Seg s = in.seg[cls][si];
+        const uint32_t L = s.len;
+        const uint32_t bid = meta_buf(s.meta);
+        const uint32_t rb = meta_shift(s.meta) + 8;  // unknown low key bits (<= 16)
+        const uint32_t rmask = (1u << rb) - 1u;
+        const uint32_t* S = B.sa[bid];
+        const uint32_t* K = B.key[bid];
+        if (lane == 0) atomicAdd(misc + M_ELEMS_B, L);
+        const uint32_t top = __ldg(K + s.start) & ~rmask;
+        uint32_t v[NIT];
+#pragma unroll
+        for (int r = 0; r < NIT; ++r) {
+            const uint32_t e = lane * NIT + r;
+            v[r] = e < L ? (((__ldg(K + s.start + e) & rmask) << IDXB) | e) : 0xFFFFFFFFu;
+        }
+        warp_bitonic<NIT>(v);
+#pragma unroll
+        for (int r = 0; r < NIT; ++r) {
+            const uint32_t e = lane * NIT + r;
+            if (e < L) buf[e] = make_uint2(top | (v[r] >> IDXB), __ldg(S + s.start + (v[r] & (N - 1))));
+        }
+        __syncwarp();
+        warp_tail(buf, s, out, B);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // SMALL: one warp per segment, LSD radix sort in registers
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, Lists out, Bufs B,
@@ -595,7 +774,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
                         cnt[d] = b + __popc(peers);
                     }
                     b = __shfl_sync(0xFFFFFFFFu, b, leader);
-                    rank[it] = b + __popc(peers & ((1u << lane) - 1u));
+                    rank[it] = b + __popc(peers & lanemask_lt());
                     __syncwarp();
                 }
             }
@@ -642,62 +821,10 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
 #pragma unroll
         for (int it = 0; it < kIpl; ++it) {
             const uint32_t e = it * 32 + lane;
-            if ((uint32_t)it < nit) {
-                buf[e] = make_uint2(key[it], slot[it]);
-                if (e < L) B.saf[s.start + e] = slot[it];
-            }
+            if ((uint32_t)it < nit) buf[e] = make_uint2(key[it], slot[it]);
         }
         __syncwarp();
-        // ties on this word with 14 real symbols: runs <= 32 are packed into
-        // shared warp_finish calls, longer runs become segments of the next word
-        uint32_t lb = 0, my_pos = 0, my_grp = 0;
-        bool mine = false;
-        for (uint32_t it = 0; it < nit; ++it) {
-            const uint32_t e = it * 32 + lane;
-            const uint32_t k = buf[e].x;
-            const bool st = e < L && (e == 0 || buf[e - 1].x != k) && e + 1 < L &&
-                            buf[e + 1].x == k && (k & 15u) == (uint32_t)kKeySyms;
-            uint32_t m = __ballot_sync(0xFFFFFFFFu, st);
-            while (m) {
-                const uint32_t l = __ffs(m) - 1;
-                m &= m - 1;
-                const uint32_t rs = it * 32 + l;
-                const uint32_t rk = buf[rs].x;
-                uint32_t Lr = 0;
-                for (uint32_t c = rs + 1;; c += 32) {
-                    const uint32_t q = c + lane;
-                    const bool eq = q < L && buf[q].x == rk;
-                    const uint32_t ne = __ballot_sync(0xFFFFFFFFu, !eq);
-                    if (ne) {
-                        Lr = c + (__ffs(ne) - 1) - rs;
-                        break;
-                    }
-                }
-                if (Lr <= kTiny) {
-                    if (lb + Lr > 32) {
-                        uint32_t sl = mine ? buf[my_pos].y : 0u;
-                        sl = warp_finish(sl, lb, s.word + 1, 0u, false, B, my_grp);
-                        if (mine) B.saf[s.start + my_pos] = sl;
-                        lb = 0;
-                        mine = false;
-                    }
-                    if (lane >= lb && lane < lb + Lr) {
-                        mine = true;
-                        my_pos = rs + lane - lb;
-                        my_grp = lb;
-                    }
-                    lb += Lr;
-                } else {
-                    for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = buf[rs + q].y;
-                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
-                }
-            }
-        }
-        if (lb) {
-            uint32_t sl = mine ? buf[my_pos].y : 0u;
-            sl = warp_finish(sl, lb, s.word + 1, 0u, false, B, my_grp);
-            if (mine) B.saf[s.start + my_pos] = sl;
-        }
+        warp_tail(buf, s, out, B);
         __syncwarp();
     }
 }
@@ -814,7 +941,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                        uint32_t* d_sa_final, SortStats* st) {
     if (n_suf == 0) return cudaSuccess;
     const size_t n = n_suf;
-    const size_t cap[NCLASS] = {n / 2 + 1, n / (kTiny + 1) + 1, n / (kCapS + 1) + 1,
+    const size_t cap[NCLASS] = {n / 2 + 1,         n / 33 + 1, n / 65 + 1, n / 129 + 1,
+                                n / 257 + 1,       n / 33 + 1, n / (kCapS + 1) + 1,
                                 n / (kCapM + 1) + 1};
     const size_t max_large = cap[LARGE];
     const size_t max_chunks = n / kChunk + max_large + 1;
@@ -879,17 +1007,33 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_LAUNCH(prof, s, "sort_init", 4.0 * n, n,
               init_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc));
     SB_CHECK(cudaGetLastError());
-    uint32_t h_cnt[NCLASS] = {0, 0, 0, 0};
-    if (n > 1) {
-        const uint32_t c = n <= kTiny ? TINY : n <= kCapS ? SMALL : n <= kCapM ? MEDIUM : LARGE;
-        h_cnt[c] = 1;
-    }
+    uint32_t h_cnt[NCLASS] = {0};
+    if (n > 1) h_cnt[class_of(Seg{0u, (uint32_t)n, 0u, 24u | (1u << 9)})] = 1;
     Lists in = A, out = Bl;
     uint32_t prev_active = 0;
     uint64_t act_local = 0;
-    uint32_t h_misc[M_N] = {0, 0, 0, 0, 0};
+    uint32_t h_misc[M_N] = {0};
     for (;;) {
-        if (!(h_cnt[0] | h_cnt[1] | h_cnt[2] | h_cnt[3])) break;
+        uint32_t any = 0;
+        for (int c = 0; c < NCLASS; ++c) any |= h_cnt[c];
+        if (!any) break;
+        {
+            const int cls[4] = {BIT2, BIT4, BIT8, BIT16};
+            const char* nm[4] = {"sort_bitonic64", "sort_bitonic128", "sort_bitonic256",
+                                 "sort_bitonic512"};
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t cnt = h_cnt[cls[q]];
+                if (!cnt) continue;
+                const unsigned grid = grid_for((uint64_t)cnt * 32, kWarpCta * 32, 148u * 16u);
+                switch (q) {
+                    case 0: SB_LAUNCH(prof, s, nm[q], 0, 0, bitonic_kernel<2><<<grid, kWarpCta * 32, 0, s>>>(in, out, BIT2, B, misc)); break;
+                    case 1: SB_LAUNCH(prof, s, nm[q], 0, 0, bitonic_kernel<4><<<grid, kWarpCta * 32, 0, s>>>(in, out, BIT4, B, misc)); break;
+                    case 2: SB_LAUNCH(prof, s, nm[q], 0, 0, bitonic_kernel<8><<<grid, kWarpCta * 32, 0, s>>>(in, out, BIT8, B, misc)); break;
+                    default: SB_LAUNCH(prof, s, nm[q], 0, 0, bitonic_kernel<16><<<grid, kWarpCta * 32, 0, s>>>(in, out, BIT16, B, misc)); break;
+                }
+                SB_CHECK(cudaGetLastError());
+            }
+        }
         if (h_cnt[TINY]) {
             SB_LAUNCH(prof, s, "sort_tiny", 0, 0,
                       tiny_kernel<<<grid_for((uint64_t)h_cnt[TINY] * 32, 256, 148u * 16u), 256, 0,
@@ -952,6 +1096,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     prof.add_bytes("sort_tiny", 12.0 * h_misc[M_ELEMS_T], h_misc[M_ELEMS_T]);
     prof.add_bytes("sort_small", 12.0 * h_misc[M_ELEMS_S], h_misc[M_ELEMS_S]);
     prof.add_bytes("sort_medium", 12.0 * h_misc[M_ELEMS_M], h_misc[M_ELEMS_M]);
+    prof.add_bytes("sort_bitonic", 12.0 * h_misc[M_ELEMS_B], h_misc[M_ELEMS_B]);
     return cudaSuccess;
 }
 
