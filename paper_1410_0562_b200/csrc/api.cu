@@ -120,7 +120,9 @@ struct DevErr {
 struct setbwte_s {
     int device = 0;
     cudaStream_t own_stream = nullptr;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;       // main stream (user's, or own_stream)
+    cudaStream_t sort_stream = nullptr;  // ConstructSA of the next block
+    cudaEvent_t ev_start = nullptr, ev_sorted[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     Profiler prof;
     bool failed = false;
 
@@ -272,29 +274,37 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     return SETBWTE_OK;
 }
 
-// One iteration of Algorithm 1 for the block of strings [j0, j1)
-// occupying slots [S0, S1) of the packed append.
-setbwte_status process_block(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1, uint64_t S0,
-                             uint64_t S1) {
-    const uint64_t n_suf = S1 - S0;
+// Algorithm 1 for one block of strings [j0, j1) occupying slots
+// [S0, S1) of the packed append, split in two stages on two streams so that
+// ConstructSA of block k+1 (sort stream) overlaps ComputeRanks / gather /
+// Insert of block k (main stream): the sort has no B_ext dependency
+// (the paper's stage pipeline P:190-191).
+struct BlockDesc {
+    uint64_t j0, j1, S0, S1;
+};
+
+// SA_int := ConstructSA(S_jk), sieving fused; on the sort stream.
+setbwte_status sort_stage(setbwte_t h, const Packed& pk, const BlockDesc& b, uint32_t* saf) {
+    API_CHECK(h, sort_block(h->prof, h->sort_stream, h->sort, pk.text, pk.term, b.S0,
+                            (uint32_t)(b.S1 - b.S0), saf, &h->sstats));
+    return SETBWTE_OK;
+}
+
+// ComputeRanks, B_int + g_sa gather, Insert; on the main stream.
+setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc& b,
+                                 const uint32_t* saf) {
+    const uint64_t n_suf = b.S1 - b.S0;
     // g / pos width: u32 while every position of the new B_ext fits
     const int gw = (h->n + n_suf) < (1ull << 32) ? 4 : 8;
-    uint32_t* saf;
-    uint64_t *g, *pos;
-    uint8_t* bint;
-    API_CHECK(h, ensure(h->saf, n_suf, &saf));
-    API_CHECK(h, ensure(h->g, n_suf, &g));
-    API_CHECK(h, ensure(h->pos, n_suf, &pos));
-    API_CHECK(h, ensure(h->bint, n_suf, &bint));
-    // SA_int := ConstructSA(S_jk) -- fused sieving
-    API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, S0, (uint32_t)n_suf,
-                            saf, &h->sstats));
+    uint64_t* g = (uint64_t*)h->g.p;
+    uint64_t* pos = (uint64_t*)h->pos.p;
+    uint8_t* bint = (uint8_t*)h->bint.p;
     // g := ComputeRanks(S_jk, B_ext)
-    setbwte_status st = compute_ranks_for(h, pk, j0, j1, S0, n_suf, g, gw);
+    setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw);
     if (st != SETBWTE_OK) return st;
     // B_int := B(S_jk, SA_int) and g_sa / pos, fused
-    API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, S0, saf, g, (uint32_t)n_suf,
-                               pos, gw, bint));
+    API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
+                               (uint32_t)n_suf, pos, gw, bint));
     // B_ext := Insert(B_int, g_sa, B_ext)
     const uint64_t n_out = h->n + n_suf;
     const uint64_t nblk = (n_out >> 6) + 1;
@@ -304,14 +314,61 @@ setbwte_status process_block(setbwte_t h, const Packed& pk, uint64_t j0, uint64_
     uint64_t *osb, *tot;
     API_CHECK(h, ensure(h->blk[nxt], nblk, &ob));
     API_CHECK(h, ensure(h->sb[nxt], nsb * 4, &osb));
-    API_CHECK(h, ensure(h->sb_tot, nsb * 4, &tot));
-    const uint64_t m_new = h->m + (j1 - j0);
+    API_CHECK(h, ensure(h->sb_tot, nsb * 4 + 4 + nsb + 2, &tot));  // totals + sb_start
+    const uint64_t m_new = h->m + (b.j1 - b.j0);
     API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_suf, ob, osb,
                                tot, m_new, (uint64_t*)h->d_C.p));
     h->cur = nxt;
     h->n = n_out;
     h->m = m_new;
     return SETBWTE_OK;
+}
+
+// Run Algorithm 1 over all blocks with the two-stage pipeline.
+setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<BlockDesc>& blocks) {
+    const size_t K = blocks.size();
+    uint64_t max_suf = 0, total = 0;
+    for (const BlockDesc& b : blocks) {
+        max_suf = std::max(max_suf, b.S1 - b.S0);
+        total += b.S1 - b.S0;
+    }
+    // reserve everything up front: a cudaFree/cudaMalloc mid-loop would
+    // serialise the two streams
+    uint32_t* saf2;
+    uint64_t* tmp;
+    uint8_t* tb;
+    API_CHECK(h, ensure(h->saf, 2 * max_suf + 64, &saf2));
+    API_CHECK(h, ensure(h->g, max_suf, &tmp));
+    API_CHECK(h, ensure(h->pos, max_suf, &tmp));
+    API_CHECK(h, ensure(h->bint, max_suf, &tb));
+    API_CHECK(h, sort_reserve(h->sort, (uint32_t)max_suf));
+    const uint64_t n_final = h->n + total;
+    API_CHECK(h, ensure(h->sb_tot, ((n_final >> kSbShift) + 1) * 5 + 8, &tmp));
+    uint32_t* saf[2] = {saf2, saf2 + max_suf + 32};
+    // the sort stream starts after everything queued on the main stream so far
+    API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
+    API_CHECK(h, cudaStreamWaitEvent(h->sort_stream, h->ev_start, 0));
+    setbwte_status st = SETBWTE_OK;
+    if (K > 0) st = sort_stage(h, pk, blocks[0], saf[0]);
+    for (size_t k = 0; k < K && st == SETBWTE_OK; ++k) {
+        API_CHECK(h, cudaEventRecord(h->ev_sorted[k & 1], h->sort_stream));
+        API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_sorted[k & 1], 0));
+        st = rank_insert_stage(h, pk, blocks[k], saf[k & 1]);
+        if (st != SETBWTE_OK) {
+            if (k > 0) h->failed = true;  // a partially applied append cannot be rolled back
+            break;
+        }
+        // SA_int buffer k&1 is free again once this block's gather has run
+        API_CHECK(h, cudaEventRecord(h->ev_used[k & 1], h->stream));
+        if (k + 1 < K) {
+            if (k >= 1) API_CHECK(h, cudaStreamWaitEvent(h->sort_stream, h->ev_used[(k + 1) & 1], 0));
+            st = sort_stage(h, pk, blocks[k + 1], saf[(k + 1) & 1]);
+        }
+    }
+    // main stream joins the sort stream before the call returns
+    API_CHECK(h, cudaEventRecord(h->ev_start, h->sort_stream));
+    API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
+    return st;
 }
 
 void build_stats(setbwte_t h) {
@@ -378,14 +435,11 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* d_bytes, const uint64_t* 
         if (bounds[2 * b + 3] - bounds[2 * b + 1] >= (1ull << 31)) return SETBWTE_E_UNSUPPORTED;
     }
     h->last_blocks = K;
-    for (uint64_t b = 0; b < K; ++b) {
-        st = process_block(h, po.pk, bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1],
-                           bounds[2 * b + 3]);
-        if (st != SETBWTE_OK) {
-            if (b > 0) h->failed = true;  // a partially applied append cannot be rolled back
-            return st;
-        }
-    }
+    std::vector<BlockDesc> blocks(K);
+    for (uint64_t b = 0; b < K; ++b)
+        blocks[b] = BlockDesc{bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1], bounds[2 * b + 3]};
+    st = run_blocks(h, po.pk, blocks);
+    if (st != SETBWTE_OK) return st;
     API_CHECK(h, cudaStreamSynchronize(h->stream));
     API_CHECK(h, h->prof.resolve());
     build_stats(h);
@@ -435,6 +489,10 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     h->sigma = (int)sigma;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&h->ev_start, &h->ev_sorted[0], &h->ev_sorted[1], &h->ev_used[0],
+                            &h->ev_used[1]})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     h->stream = h->own_stream;
     uint8_t* dc = nullptr;
     uint8_t* ds = nullptr;
@@ -466,8 +524,14 @@ void setbwte_destroy(setbwte_t h) {
                       &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos,
                       &h->bint, &h->outbuf, &h->sort.sa0, &h->sort.sa1, &h->sort.k0,
                       &h->sort.k1, &h->sort.segs_a, &h->sort.segs_b, &h->sort.small_a,
-                      &h->sort.small_b, &h->sort.chunks, &h->sort.hist, &h->sort.ctr};
+                      &h->sort.small_b, &h->sort.chunks, &h->sort.hist, &h->sort.ctr,
+                      &h->sort.gtot, &h->sort.groups};
     for (DevBuf* b : bufs) free_buf(*b);
+    if (h->sort_stream) cudaStreamSynchronize(h->sort_stream);
+    for (cudaEvent_t ev : {h->ev_start, h->ev_sorted[0], h->ev_sorted[1], h->ev_used[0],
+                           h->ev_used[1]})
+        if (ev) cudaEventDestroy(ev);
+    if (h->sort_stream) cudaStreamDestroy(h->sort_stream);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }

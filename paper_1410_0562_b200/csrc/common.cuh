@@ -91,12 +91,14 @@ __device__ __forceinline__ uint64_t dict_rank(const Blk* __restrict__ blk,
                                               uint64_t i) {
     const Blk* b = blk + (i >> 6);
     const uint64_t base = __ldg(sb + ((i >> kSbShift) << 2) + c);
-    // one 32-byte sector: cnt (8 B) + lo | hi + dol
-    const ulonglong2 r0 = __ldg(reinterpret_cast<const ulonglong2*>(b));
-    const ulonglong2 r1 = __ldg(reinterpret_cast<const ulonglong2*>(b) + 1);
-    const uint32_t r = (uint32_t)((r0.x >> (16 * c)) & 0xFFFFu);
+    // the whole 32-byte Blk (one sector) in one 256-bit load
+    uint64_t w0, w1, w2, w3;
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+        : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
+        : "l"(b));
+    const uint32_t r = (uint32_t)((w0 >> (16 * c)) & 0xFFFFu);
     const uint64_t mask = (1ull << (i & 63)) - 1ull;
-    return base + r + (uint64_t)__popcll(match_plane(c, r0.y, r1.x, r1.y) & mask);
+    return base + r + (uint64_t)__popcll(match_plane(c, w1, w2, w3) & mask);
 }
 
 }  // namespace setbwte

@@ -37,39 +37,67 @@ __device__ __forceinline__ uint64_t funnel(uint64_t a, uint64_t b, uint32_t sh) 
 }
 }  // namespace
 
+// Inclusive warp scan.
+__device__ __forceinline__ uint32_t warp_incl(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= (uint32_t)o) v += y;
+    }
+    return v;
+}
+
+constexpr uint32_t kStage = 16384;  // inserted entries staged in shared memory per superblock
+
+// sb_start[s] = first inserted index with pos >= s * 2^16, s in [0, nsb]: the
+// "vectorised binary search" of P:158 done as one parallel pass over pos
+// (each superblock boundary has exactly one writer).
+template <class G>
+__global__ void sb_bounds_kernel(const G* __restrict__ pos, uint64_t n_ins, uint64_t nsb,
+                                 uint64_t* __restrict__ sb_start) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n_ins;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t cur = i < n_ins ? ((uint64_t)pos[i] >> kSbShift) : nsb;
+        const uint64_t first = i > 0 ? ((uint64_t)pos[i - 1] >> kSbShift) + 1 : 0;
+        for (uint64_t sbi = first; sbi <= cur && sbi <= nsb; ++sbi) sb_start[sbi] = i;
+    }
+}
+
 template <class G>
 __global__ void __launch_bounds__(kInsNt) insert_kernel(
     const Blk* __restrict__ in_blk, uint64_t n_in, const G* __restrict__ pos,
     const uint8_t* __restrict__ bint, uint64_t n_ins, Blk* __restrict__ out_blk, uint64_t n_out,
-    uint64_t* __restrict__ sb_tot) {
+    uint64_t* __restrict__ sb_tot, const uint64_t* __restrict__ sb_start) {
     __shared__ uint32_t wcnt[kBlkPerSb];
-    __shared__ uint32_t wsum[kInsWarps][4];
-    __shared__ uint64_t i_range[2];
+    __shared__ uint16_t ent[kStage];  // (offset in word) | (B_int code+$ << 6)
+    __shared__ uint32_t wsum[4][kInsWarps];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
     for (uint64_t sbi = blockIdx.x; sbi < nsb; sbi += gridDim.x) {
         const uint64_t o0 = sbi << kSbShift;
-        if (tid == 0) i_range[0] = lower_bound_g(pos, n_ins, o0);
-        if (tid == 32) i_range[1] = lower_bound_g(pos, n_ins, o0 + (1ull << kSbShift));
         wcnt[tid] = 0;
         __syncthreads();
-        const uint64_t i_lo = i_range[0], i_hi = i_range[1];
-        for (uint64_t i = i_lo + tid; i < i_hi; i += kInsNt)
-            atomicAdd(&wcnt[(uint32_t)(((uint64_t)__ldg(pos + i) - o0) >> 6)], 1u);
-        __syncthreads();
-        // exclusive scan over the 1024 words: a = first inserted index of word tid
-        const uint32_t cnt = wcnt[tid];
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
+        const uint64_t i_lo = sb_start[sbi], i_hi = sb_start[sbi + 1];
+        const bool staged = i_hi - i_lo <= kStage;
+        // pass 1 (coalesced): inserted symbols per output word, staged entries
+        for (uint64_t i = i_lo + tid; i < i_hi; i += kInsNt) {
+            const uint32_t rel = (uint32_t)((uint64_t)__ldg(pos + i) - o0);
+            atomicAdd(&wcnt[rel >> 6], 1u);
+            if (staged) ent[i - i_lo] = (uint16_t)((rel & 63u) | ((uint32_t)__ldg(bint + i) << 6));
         }
-        if (lane == 31) wsum[warp][0] = incl;
         __syncthreads();
-        uint32_t pre = 0;
-        for (uint32_t w = 0; w < warp; ++w) pre += wsum[w][0];
-        const uint64_t a = i_lo + pre + incl - cnt;
+        // exclusive scan over the 1024 words (two-level)
+        const uint32_t cnt = wcnt[tid];
+        const uint32_t incl = warp_incl(cnt, lane);
+        if (lane == 31) wsum[0][warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t x = wsum[0][lane];
+            wsum[0][lane] = warp_incl(x, lane) - x;
+        }
+        __syncthreads();
+        const uint32_t arel = wsum[0][warp] + incl - cnt;  // inserted before this word
+        const uint64_t a = i_lo + arel;
         // one thread merges one 64-symbol output word
         const uint64_t ow0 = o0 + ((uint64_t)tid << 6);
         const bool wvalid = ow0 <= n_out;
@@ -81,23 +109,28 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
             if (e0 < n_in) {
                 const uint64_t eb = e0 >> 6;
                 const uint32_t sh = (uint32_t)(e0 & 63);
-                const Blk* b0 = in_blk + eb;
-                const ulonglong2 p0 = __ldg(reinterpret_cast<const ulonglong2*>(b0) + 1);
-                const uint64_t l0 = __ldg(&b0->lo);
-                uint64_t l1 = 0, h1 = 0, d1 = 0;
-                if (sh != 0 && ((eb + 1) << 6) < n_in) {
-                    l1 = __ldg(&b0[1].lo);
-                    const ulonglong2 p1 = __ldg(reinterpret_cast<const ulonglong2*>(b0 + 1) + 1);
-                    h1 = p1.x;
-                    d1 = p1.y;
-                }
-                xl = funnel(l0, l1, sh);
-                xh = funnel(p0.x, h1, sh);
-                xd = funnel(p0.y, d1, sh);
+                uint64_t b0[4], b1[4] = {0, 0, 0, 0};
+                asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                    : "=l"(b0[0]), "=l"(b0[1]), "=l"(b0[2]), "=l"(b0[3]) : "l"(in_blk + eb));
+                if (sh != 0 && ((eb + 1) << 6) < n_in)
+                    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                        : "=l"(b1[0]), "=l"(b1[1]), "=l"(b1[2]), "=l"(b1[3])
+                        : "l"(in_blk + eb + 1));
+                xl = funnel(b0[1], b1[1], sh);
+                xh = funnel(b0[2], b1[2], sh);
+                xd = funnel(b0[3], b1[3], sh);
             }
             uint32_t filled = 0, used = 0;
             for (uint32_t k = 0; k < cnt; ++k) {
-                const uint32_t t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
+                uint32_t t, b;
+                if (staged) {
+                    const uint32_t e = ent[arel + k];
+                    t = e & 63u;
+                    b = e >> 6;
+                } else {
+                    t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
+                    b = __ldg(bint + a + k);
+                }
                 const uint32_t run = t - filled;
                 if (run) {
                     const uint64_t m = (1ull << run) - 1ull;
@@ -106,10 +139,9 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
                     od |= ((xd >> used) & m) << filled;
                     used += run;
                 }
-                const uint64_t b = __ldg(bint + a + k);
-                ol |= (b & 1ull) << t;
-                oh |= ((b >> 1) & 1ull) << t;
-                od |= ((b >> 2) & 1ull) << t;
+                ol |= (uint64_t)(b & 1u) << t;
+                oh |= (uint64_t)((b >> 1) & 1u) << t;
+                od |= (uint64_t)((b >> 2) & 1u) << t;
                 filled = t + 1;
             }
             const uint64_t span = n_out - ow0;
@@ -128,40 +160,27 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
         // in-superblock exclusive prefix of the per-word counts (4 codes)
         uint32_t inc[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) inc[c] = c4[c];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc[c], o);
-                if (lane >= (uint32_t)o) inc[c] += y;
-            }
-        }
-        __syncthreads();  // wsum reuse
+        for (int c = 0; c < 4; ++c) inc[c] = warp_incl(c4[c], lane);
         if (lane == 31) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) wsum[warp][c] = inc[c];
+            for (int c = 0; c < 4; ++c) wsum[c][warp] = inc[c];
         }
         __syncthreads();
-        uint32_t pw[4] = {0, 0, 0, 0}, tot[4] = {0, 0, 0, 0};
-        for (uint32_t w = 0; w < (uint32_t)kInsWarps; ++w) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint32_t v = wsum[w][c];
-                if (w < warp) pw[c] += v;
-                tot[c] += v;
-            }
+        if (warp < 4) {
+            const uint32_t x = wsum[warp][lane];
+            const uint32_t y = warp_incl(x, lane);
+            wsum[warp][lane] = y - x;
+            if (lane == 31 && tid < 4 * 32) sb_tot[sbi * 4 + warp] = y;
         }
+        __syncthreads();
         if (wvalid) {
-            Blk b;
+            uint64_t w0 = 0;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) b.cnt[c] = (uint16_t)(pw[c] + inc[c] - c4[c]);
-            b.lo = ol;
-            b.hi = oh;
-            b.dol = od;
-            out_blk[(sbi << (kSbShift - 6)) + tid] = b;
+            for (int c = 0; c < 4; ++c)
+                w0 |= (uint64_t)(uint16_t)(wsum[c][warp] + inc[c] - c4[c]) << (16 * c);
+            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(out_blk + (sbi << (kSbShift - 6)) + tid),
+                         "l"(w0), "l"(ol), "l"(oh), "l"(od));
         }
-        if (tid < 4) sb_tot[sbi * 4 + tid] = tot[tid];
         __syncthreads();
     }
 }
@@ -214,16 +233,26 @@ cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uin
     // algorithmic bytes: read n_in/2 + write n_out/2 (4 bits/symbol) + (gw + 1) B per inserted
     const double bytes = 0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins;
     const unsigned grid = (unsigned)(nsb < 148u * 64u ? nsb : 148u * 64u);
+    uint64_t* sb_start = sb_tot + 4 * (nsb + 1);  // caller sized sb_tot for both
+    const unsigned gb = grid_for(n_ins + 1, 256);
     if (gw == 4) {
+        SB_LAUNCH(prof, s, "insert_bounds", (double)gw * n_ins, n_ins,
+                  sb_bounds_kernel<uint32_t><<<gb, 256, 0, s>>>((const uint32_t*)pos, n_ins, nsb,
+                                                                 sb_start));
+        SB_CHECK(cudaGetLastError());
         SB_LAUNCH(prof, s, "insert", bytes, n_out,
                   insert_kernel<uint32_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint32_t*)pos,
                                                                    bint, n_ins, out_blk, n_out,
-                                                                   sb_tot));
+                                                                   sb_tot, sb_start));
     } else {
+        SB_LAUNCH(prof, s, "insert_bounds", (double)gw * n_ins, n_ins,
+                  sb_bounds_kernel<uint64_t><<<gb, 256, 0, s>>>((const uint64_t*)pos, n_ins, nsb,
+                                                                 sb_start));
+        SB_CHECK(cudaGetLastError());
         SB_LAUNCH(prof, s, "insert", bytes, n_out,
                   insert_kernel<uint64_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint64_t*)pos,
                                                                    bint, n_ins, out_blk, n_out,
-                                                                   sb_tot));
+                                                                   sb_tot, sb_start));
     }
     SB_CHECK(cudaGetLastError());
     SB_LAUNCH(prof, s, "sb_scan", 64.0 * nsb, nsb,

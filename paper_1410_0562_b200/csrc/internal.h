@@ -109,16 +109,17 @@ cudaError_t launch_slices(Profiler& prof, cudaStream_t s, const uint64_t* d_slot
 
 // sort.cu -- A1 ConstructSA (Sec.3).
 struct SortScratch {
-    DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr;
+    DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr, gtot, groups;
 };
 struct SortStats {
     uint64_t digit_passes = 0;
     uint64_t rounds = 0;
     std::vector<uint64_t> active_per_pass;  // elements entering each digit pass
 };
+cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf);
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
-                       uint32_t* d_sa_final, SortStats* st);
+                       uint32_t* d_sa_final, SortStats* st, bool reserve_only = false);
 
 // ranks.cu -- A3 ComputeRanks (Lemma 1, Alg.2) and the
 // fused A2/A4 extraction + gather (Alg.1).

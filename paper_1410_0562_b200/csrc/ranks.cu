@@ -22,6 +22,20 @@
 namespace setbwte {
 
 template <class G>
+__device__ __forceinline__ void store4(G* dst, G a, G b, G c, G d);
+template <>
+__device__ __forceinline__ void store4<uint32_t>(uint32_t* dst, uint32_t a, uint32_t b, uint32_t c,
+                                                 uint32_t d) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<uint64_t>(uint64_t* dst, uint64_t a, uint64_t b, uint64_t c,
+                                                 uint64_t d) {
+    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "l"(a), "l"(b), "l"(c),
+                 "l"(d));
+}
+
+template <class G>
 __global__ void __launch_bounds__(256) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
     uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
@@ -29,15 +43,16 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
     for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
          j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s0 = slot_off[j];
-        const uint64_t e = slot_off[j + 1] - 1;  // terminator slot
+        // local slot indices: [l0, le], le = terminator
+        const uint64_t l0 = slot_off[j] - slot_base;
+        const uint64_t le = slot_off[j + 1] - 1 - slot_base;
         uint64_t i = m_ext;
-        g[e - slot_base] = (G)i;
-        uint64_t p = e;
+        g[le] = (G)i;
+        uint64_t lp = le;  // next step computes slot lp-1
         uint64_t wi = ~0ull;
         uint32_t word = 0;
-        while (p > s0) {
-            --p;
+        auto step = [&](uint64_t q) -> uint64_t {  // LF step for local slot q
+            const uint64_t p = q + slot_base;
             if ((p >> 4) != wi) {
                 wi = p >> 4;
                 word = __ldg(text + wi);
@@ -45,7 +60,25 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
             const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
             const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
             i = Cc + dict_rank(blk, sb, c, i);
-            g[p - slot_base] = (G)i;
+            return i;
+        };
+        // single steps down to a 4-aligned local slot, then 4 steps per
+        // vector store (one store instruction instead of four)
+        while (lp > l0 && (lp & 3) != 0) {
+            --lp;
+            g[lp] = (G)step(lp);
+        }
+        while (lp >= l0 + 4) {
+            const G a3 = (G)step(lp - 1);
+            const G a2 = (G)step(lp - 2);
+            const G a1 = (G)step(lp - 3);
+            const G a0 = (G)step(lp - 4);
+            lp -= 4;
+            store4<G>(g + lp, a0, a1, a2, a3);
+        }
+        while (lp > l0) {
+            --lp;
+            g[lp] = (G)step(lp);
         }
     }
 }

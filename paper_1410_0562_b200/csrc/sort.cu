@@ -40,8 +40,10 @@ constexpr int kIpl = kCapS / 32;
 constexpr int kWarpCta = 8;
 constexpr uint32_t kCapM = 4096;   // MEDIUM: 512 threads, 8 items each
 constexpr uint32_t kNtM = 512;
-constexpr uint32_t kChunk = 16384; // target chunk of a digit pass
+constexpr uint32_t kChunk = 16384; // largest chunk of a digit pass
+constexpr uint32_t kMinChunk = 2048;
 constexpr uint32_t kMaxChunks = 1024;
+constexpr uint32_t kGroup = 32;    // chunks per prefix group
 constexpr int kDigNt = 512;        // digit-pass CTA
 constexpr int kDigIpt = 8;
 constexpr int kDigTile = kDigNt * kDigIpt;
@@ -51,16 +53,19 @@ constexpr int kDigTile = kDigNt * kDigIpt;
 // register bitonic network.  SMALL: the other 33..512 segments (warp LSD radix).
 enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MEDIUM, LARGE, NCLASS };
 // misc counters
-enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_N };
+enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_N };
 
 struct Seg {
     uint32_t start, len, word, meta;  // meta: shift | buf<<8 | keys_valid<<9 | iota<<10
 };
 struct SegX {
-    uint32_t chunk_base, nchunks, chunk_len, skip;
+    uint32_t chunk_base, nchunks, group_base, skip;
 };
 struct Chunk {
-    uint32_t seg, begin, end, pad;
+    uint32_t seg, begin, end, group;
+};
+struct Group {
+    uint32_t first_chunk, nchunks;
 };
 struct Lists {
     Seg* seg[NCLASS];
@@ -107,7 +112,7 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d) {
     for (int b = 0; b < NB; ++b) {
         const uint32_t bit = (d >> b) & 1u;
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-        peers &= bit ? bal : ~bal;
+        peers &= bal ^ (bit - 1u);  // bit ? bal : ~bal, branch-free
     }
     return peers;
 }
@@ -184,18 +189,23 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
     for (uint32_t i = tid; i < NW * 256; i += NT) wcnt[i] = 0;
     __syncthreads();
     uint32_t* mine = wcnt + warp * 256;
+    // all MATCH.ANY first (independent, their latency overlaps), then the
+    // in-order per-warp counter updates: every lane reads its digit's counter
+    // (broadcast among peers), the lowest peer writes it back advanced.
+    // peers by ballots (MATCH.ANY measured slower here: MIO-pipe throughput);
+    // a full tile has no invalid items and needs only the 8 digit bits
+    uint32_t peers[IPT];
+    const bool full = __all_sync(0xFFFFFFFFu, dig[IPT - 1] < 256);
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) peers[it] = full ? peers_of<8>(dig[it]) : peers_of<9>(dig[it]);
+    const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int it = 0; it < IPT; ++it) {
         const uint32_t d = dig[it];
-        const uint32_t peers = peers_of<9>(d);
-        const uint32_t leader = __ffs(peers) - 1;
-        uint32_t b = 0;
-        if (lane == leader && d < 256) {
-            b = mine[d];
-            mine[d] = b + __popc(peers);
-        }
-        b = __shfl_sync(0xFFFFFFFFu, b, leader);
-        dest[it] = b + __popc(peers & lanemask_lt());
+        const bool ok = d < 256;
+        const uint32_t b = ok ? mine[d] : 0u;
+        dest[it] = b + __popc(peers[it] & lt);
+        if (ok && (peers[it] & lt) == 0) mine[d] = b + __popc(peers[it]);
         __syncwarp();
     }
     __syncthreads();
@@ -296,35 +306,49 @@ __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ s
 
 __global__ void reset_counts_kernel(uint32_t* cnt, uint32_t* misc) {
     if (threadIdx.x < NCLASS) cnt[threadIdx.x] = 0;
-    if (threadIdx.x == 0) misc[M_CHUNKS] = 0;
+    if (threadIdx.x == 0) {
+        misc[M_CHUNKS] = 0;
+        misc[M_GROUPS] = 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
 // LARGE: one stable 8-bit MSD digit pass
 // ---------------------------------------------------------------------------
+// Split each large segment into chunks (one CTA of the digit pass each) and
+// the chunks into prefix groups of kGroup.  Chunks are kMinChunk..kChunk long,
+// as many as keep every SM busy when few large segments are left.
 __global__ void chunkify_kernel(Lists in, SegX* __restrict__ segx, Chunk* __restrict__ chunks,
-                                uint32_t* misc) {
+                                Group* __restrict__ groups, uint32_t* misc) {
     const uint32_t n = in.cnt[LARGE];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    const uint32_t want = (148u * 8u + n - 1) / n;  // chunks per segment to fill the GPU
     for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
         const Seg s = in.seg[LARGE][i];
-        uint32_t nch = (s.len + kChunk - 1) / kChunk;
+        const uint32_t lo = (s.len + kChunk - 1) / kChunk;
+        const uint32_t hi = (s.len + kMinChunk - 1) / kMinChunk;
+        uint32_t nch = max(lo, min(hi, want));
         nch = nch > kMaxChunks ? kMaxChunks : nch;
         const uint32_t clen = (s.len + nch - 1) / nch;
         nch = (s.len + clen - 1) / clen;
-        uint32_t base = 0;
+        const uint32_t ngr = (nch + kGroup - 1) / kGroup;
+        uint32_t base = 0, gbase = 0;
         if (lane == 0) {
             base = atomicAdd(misc + M_CHUNKS, nch);
+            gbase = atomicAdd(misc + M_GROUPS, ngr);
             atomicAdd(misc + M_ACTIVE, s.len);
-            segx[i] = SegX{base, nch, clen, 0u};
+            segx[i] = SegX{base, nch, gbase, 0u};
         }
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        gbase = __shfl_sync(0xFFFFFFFFu, gbase, 0);
         for (uint32_t c = lane; c < nch; c += 32) {
             const uint32_t b = s.start + c * clen;
             const uint32_t e = min(b + clen, s.start + s.len);
-            chunks[base + c] = Chunk{i, b, e, 0u};
+            chunks[base + c] = Chunk{i, b, e, gbase + c / kGroup};
         }
+        for (uint32_t g = lane; g < ngr; g += 32)
+            groups[gbase + g] = Group{base + g * kGroup, min(kGroup, nch - g * kGroup)};
     }
 }
 
@@ -345,32 +369,51 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
         const bool kv = meta_kv(s.meta);
         const uint32_t* S = B.sa[buf];
         uint32_t* K = B.key[buf];
-        constexpr int U = 8;
-        for (uint32_t p0 = ch.begin; p0 < ch.end; p0 += kDigNt * U) {
-            uint32_t key[U];
+        if (kv) {
+            // keys valid: 4 consecutive keys per thread per 16-byte load
+            const uint32_t a0 = ch.begin & ~3u;
+            for (uint32_t p0 = a0; p0 < ch.end; p0 += kDigNt * 4 * 2) {
+                uint4 q[2];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t p = p0 + u * kDigNt + tid;
-                key[u] = 0xFFFFFFFFu;
-                if (p < ch.end) {
-                    if (kv) {
-                        key[u] = __ldg(K + p);
-                    } else {
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t p = p0 + (u * kDigNt + tid) * 4;
+                    q[u] = p < ch.end ? __ldg(reinterpret_cast<const uint4*>(K + p))
+                                      : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t p = p0 + (u * kDigNt + tid) * 4;
+                    const uint32_t kk[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const bool in = p + v >= ch.begin && p + v < ch.end;
+                        const uint32_t d = (kk[v] >> shift) & 0xFFu;
+                        const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+                        if (__all_sync(0xFFFFFFFFu, in && d == d0)) {
+                            if (lane == 0) atomicAdd(&h[warp][d0], 32u);
+                        } else if (in) {
+                            atomicAdd(&h[warp][d], 1u);
+                        }
+                    }
+                }
+            }
+        } else {
+            constexpr int U = 8;
+            for (uint32_t p0 = ch.begin; p0 < ch.end; p0 += kDigNt * U) {
+                uint32_t key[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t p = p0 + u * kDigNt + tid;
+                    key[u] = 0;
+                    if (p < ch.end) {
                         key[u] = suffix_key(B.text, B.term, B.base + __ldg(S + p), s.word);
                         K[p] = key[u];
                     }
                 }
-            }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t p = p0 + u * kDigNt + tid;
-                const uint32_t d = (key[u] >> shift) & 0xFFu;
-                const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
-                const bool v = p < ch.end;
-                if (__all_sync(0xFFFFFFFFu, v && d == d0)) {
-                    if (lane == 0) atomicAdd(&h[warp][d0], 32u);
-                } else if (v) {
-                    atomicAdd(&h[warp][d], 1u);
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t p = p0 + u * kDigNt + tid;
+                    if (p < ch.end) atomicAdd(&h[warp][(key[u] >> shift) & 0xFFu], 1u);
                 }
             }
         }
@@ -385,96 +428,100 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
     }
 }
 
-__global__ void __launch_bounds__(1024) digit_scan_kernel(Lists in, Lists out,
-                                                          SegX* __restrict__ segx,
-                                                          uint32_t* __restrict__ hist,
-                                                          uint32_t* __restrict__ dbase) {
-    constexpr int kParts = 4;
-    __shared__ uint32_t psum[kParts][256];
+// Exclusive prefix of the chunk histograms inside each group of <= kGroup
+// chunks (one CTA per group, one thread per digit); gtot = group totals.
+__global__ void __launch_bounds__(256) group_scan_kernel(const Group* __restrict__ groups,
+                                                         const uint32_t* misc,
+                                                         uint32_t* __restrict__ hist,
+                                                         uint32_t* __restrict__ gtot) {
+    const uint32_t ng = misc[M_GROUPS];
+    const uint32_t d = threadIdx.x;
+    for (uint32_t g = blockIdx.x; g < ng; g += gridDim.x) {
+        const Group gr = groups[g];
+        uint32_t v[kGroup];
+#pragma unroll
+        for (uint32_t b = 0; b < kGroup; ++b)
+            v[b] = b < gr.nchunks ? hist[(size_t)(gr.first_chunk + b) * 256 + d] : 0u;
+        uint32_t run = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < kGroup; ++b) {
+            if (b < gr.nchunks) hist[(size_t)(gr.first_chunk + b) * 256 + d] = run;
+            run += v[b];
+        }
+        gtot[(size_t)g * 256 + d] = run;
+    }
+}
+
+// Per segment: prefix over its groups (gtot -> exclusive group offsets),
+// digit bases, sieve decisions and child segments.
+__global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
+                                                         SegX* __restrict__ segx,
+                                                         uint32_t* __restrict__ gtot,
+                                                         uint32_t* __restrict__ dbase) {
     __shared__ uint32_t wsum[8];
     __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
     __shared__ int all_one;
     const uint32_t n = in.cnt[LARGE];
-    const uint32_t t = threadIdx.x, d = t & 255, part = t >> 8, lane = t & 31, warp = t >> 5;
+    const uint32_t d = threadIdx.x, lane = d & 31, warp = d >> 5;
     for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
         const Seg s = in.seg[LARGE][si];
         const SegX x = segx[si];
-        // chunk counts of digit d, split into kParts contiguous ranges
-        const uint32_t c_lo = x.chunk_base + (uint32_t)((uint64_t)x.nchunks * part / kParts);
-        const uint32_t c_hi = x.chunk_base + (uint32_t)((uint64_t)x.nchunks * (part + 1) / kParts);
-        constexpr int kB = 16;
-        uint32_t sum = 0;
-        for (uint32_t c0 = c_lo; c0 < c_hi; c0 += kB) {
-            uint32_t v[kB];
-#pragma unroll
-            for (int b = 0; b < kB; ++b) v[b] = c0 + b < c_hi ? hist[(size_t)(c0 + b) * 256 + d] : 0u;
-#pragma unroll
-            for (int b = 0; b < kB; ++b) sum += v[b];
-        }
-        psum[part][d] = sum;
-        if (t < NCLASS) ccount[t] = 0;
-        if (t == 0) all_one = 0;
-        __syncthreads();
-        uint32_t run = 0;
-        for (uint32_t q = 0; q < part; ++q) run += psum[q][d];
+        const uint32_t ngr = (x.nchunks + kGroup - 1) / kGroup;
         uint32_t total = 0;
-        for (uint32_t q = 0; q < kParts; ++q) total += psum[q][d];
-        for (uint32_t c0 = c_lo; c0 < c_hi; c0 += kB) {
-            uint32_t v[kB];
+        for (uint32_t g0 = 0; g0 < ngr; g0 += 8) {
+            uint32_t v[8];
 #pragma unroll
-            for (int b = 0; b < kB; ++b) v[b] = c0 + b < c_hi ? hist[(size_t)(c0 + b) * 256 + d] : 0u;
+            for (int b = 0; b < 8; ++b)
+                v[b] = g0 + b < ngr ? gtot[(size_t)(x.group_base + g0 + b) * 256 + d] : 0u;
 #pragma unroll
-            for (int b = 0; b < kB; ++b) {
-                if (c0 + b < c_hi) hist[(size_t)(c0 + b) * 256 + d] = run;
-                run += v[b];
+            for (int b = 0; b < 8; ++b) {
+                if (g0 + b < ngr) gtot[(size_t)(x.group_base + g0 + b) * 256 + d] = total;
+                total += v[b];
             }
         }
-        // exclusive scan of the digit totals (threads of part 0)
-        uint32_t excl = 0;
-        if (part == 0) {
-            uint32_t incl = total;
+        if (d < NCLASS) ccount[d] = 0;
+        if (d == 0) all_one = 0;
+        uint32_t incl = total;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= (uint32_t)o) incl += y;
-            }
-            if (lane == 31) wsum[warp] = incl;
-            if (total == s.len) all_one = 1;
-            excl = incl - total;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
         }
+        if (lane == 31) wsum[warp] = incl;
         __syncthreads();
+        if (total == s.len) all_one = 1;
+        uint32_t excl = incl - total;
+        for (uint32_t w = 0; w < warp; ++w) excl += wsum[w];
+        __syncthreads();
+        const uint32_t shift = meta_shift(s.meta);
+        const uint32_t buf = meta_buf(s.meta);
+        const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < (uint32_t)kKeySyms);
+        uint32_t flag = 0;
         int cls = -1;
         Seg c;
         uint32_t local = 0;
-        if (part == 0) {
-            for (uint32_t w = 0; w < warp; ++w) excl += wsum[w];
-            const uint32_t shift = meta_shift(s.meta);
-            const uint32_t buf = meta_buf(s.meta);
-            const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < (uint32_t)kKeySyms);
-            uint32_t flag = 0;
-            if (total > 0) {
-                if (resolved) {
-                    flag = 0x80000000u;
+        if (total > 0) {
+            if (resolved) {
+                flag = 0x80000000u;
+            } else {
+                const uint32_t cbuf = all_one ? buf : 1u - buf;
+                c.start = s.start + excl;
+                c.len = total;
+                if (shift == 0) {
+                    c.word = s.word + 1;
+                    c.meta = make_meta(24, cbuf, 0);
                 } else {
-                    const uint32_t cbuf = all_one ? buf : 1u - buf;
-                    c.start = s.start + excl;
-                    c.len = total;
-                    if (shift == 0) {
-                        c.word = s.word + 1;
-                        c.meta = make_meta(24, cbuf, 0);
-                    } else {
-                        c.word = s.word;
-                        c.meta = make_meta(shift - 8, cbuf, 1);
-                    }
-                    cls = class_of(c);
-                    local = atomicAdd(&ccount[cls], 1u);
-                    if (all_one) segx[si].skip = 1;
+                    c.word = s.word;
+                    c.meta = make_meta(shift - 8, cbuf, 1);
                 }
+                cls = class_of(c);
+                local = atomicAdd(&ccount[cls], 1u);
+                if (all_one) segx[si].skip = 1;
             }
-            dbase[(size_t)si * 256 + d] = (s.start + excl) | flag;
         }
+        dbase[(size_t)si * 256 + d] = (s.start + excl) | flag;
         __syncthreads();
-        if (t < NCLASS && ccount[t]) cbase[t] = atomicAdd(out.cnt + t, ccount[t]);
+        if (d < NCLASS && ccount[d]) cbase[d] = atomicAdd(out.cnt + d, ccount[d]);
         __syncthreads();
         if (cls >= 0) out.seg[cls][cbase[cls] + local] = c;
         __syncthreads();
@@ -483,7 +530,8 @@ __global__ void __launch_bounds__(1024) digit_scan_kernel(Lists in, Lists out,
 
 __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
     Lists in, const SegX* __restrict__ segx, const Chunk* __restrict__ chunks, const uint32_t* misc,
-    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ dbase, Bufs B) {
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gtot,
+    const uint32_t* __restrict__ dbase, Bufs B) {
     constexpr int NW = kDigNt / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);  // NW*256
@@ -508,7 +556,8 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
         uint32_t* K2 = B.key[1 - buf];
         if (tid < 256) {
             const uint32_t db = dbase[(size_t)ch.seg * 256 + tid];
-            run_base[tid] = (db & 0x7FFFFFFFu) + hist[(size_t)c * 256 + tid];
+            run_base[tid] = (db & 0x7FFFFFFFu) + gtot[(size_t)ch.group * 256 + tid] +
+                            hist[(size_t)c * 256 + tid];
             fin[tid] = (uint8_t)(db >> 31);
         }
         for (uint32_t t0 = ch.begin; t0 < ch.end; t0 += kDigTile) {
@@ -936,16 +985,22 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
 
 using namespace sortk;
 
+cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf) {
+    Profiler dummy;
+    (void)dummy;
+    return sort_block(dummy, nullptr, ws, nullptr, nullptr, 0, n_suf, nullptr, nullptr, true);
+}
+
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
-                       uint32_t* d_sa_final, SortStats* st) {
+                       uint32_t* d_sa_final, SortStats* st, bool reserve_only) {
     if (n_suf == 0) return cudaSuccess;
     const size_t n = n_suf;
     const size_t cap[NCLASS] = {n / 2 + 1,         n / 33 + 1, n / 65 + 1, n / 129 + 1,
                                 n / 257 + 1,       n / 33 + 1, n / (kCapS + 1) + 1,
                                 n / (kCapM + 1) + 1};
     const size_t max_large = cap[LARGE];
-    const size_t max_chunks = n / kChunk + max_large + 1;
+    const size_t max_chunks = n / kMinChunk + max_large + 1;
     uint32_t *sa0, *sa1, *k0, *k1, *hist, *ctr;
     SB_CHECK(ensure(ws.sa0, n, &sa0));
     SB_CHECK(ensure(ws.sa1, n, &sa1));
@@ -963,6 +1018,11 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_CHECK(ensure(ws.small_b, max_large * 256, &dbase));
     SB_CHECK(ensure(ws.chunks, max_chunks, &chunks));
     SB_CHECK(ensure(ws.hist, max_chunks * 256, &hist));
+    const size_t max_groups = max_chunks;  // <= one group per chunk
+    uint32_t* gtot;
+    Group* groups;
+    SB_CHECK(ensure(ws.gtot, max_groups * 256, &gtot));
+    SB_CHECK(ensure(ws.groups, max_groups, &groups));
     SB_CHECK(ensure(ws.ctr, 2 * NCLASS + M_N + 8, &ctr));
     uint32_t* misc = ctr + 2 * NCLASS;
     Lists A, Bl;
@@ -976,6 +1036,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         A.cnt = ctr;
         Bl.cnt = ctr + NCLASS;
     }
+    if (reserve_only) return cudaSuccess;
     Bufs B;
     B.sa[0] = sa0;
     B.sa[1] = sa1;
@@ -1056,19 +1117,22 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         if (h_cnt[LARGE]) {
             SB_LAUNCH(prof, s, "sort_chunkify", 0, 0,
                       chunkify_kernel<<<grid_for((uint64_t)h_cnt[LARGE] * 32, 128), 128, 0, s>>>(
-                          in, segx, chunks, misc));
+                          in, segx, chunks, groups, misc));
             SB_CHECK(cudaGetLastError());
-            const unsigned g_dig = 148u * 4u;
+            const unsigned g_dig = 148u * 8u;
             SB_LAUNCH(prof, s, "digit_hist", 0, 0,
                       digit_hist_kernel<<<g_dig, kDigNt, 0, s>>>(in, chunks, misc, B, hist));
             SB_CHECK(cudaGetLastError());
             SB_LAUNCH(prof, s, "digit_scan", 0, 0,
-                      digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 2u), 1024, 0, s>>>(
-                          in, out, segx, hist, dbase));
+                      group_scan_kernel<<<148u * 8u, 256, 0, s>>>(groups, misc, hist, gtot));
+            SB_CHECK(cudaGetLastError());
+            SB_LAUNCH(prof, s, "digit_scan", 0, 0,
+                      digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 8u), 256, 0, s>>>(
+                          in, out, segx, gtot, dbase));
             SB_CHECK(cudaGetLastError());
             SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
                       digit_scatter_kernel<<<g_dig, kDigNt, sm_d, s>>>(in, segx, chunks, misc, hist,
-                                                                      dbase, B));
+                                                                      gtot, dbase, B));
             SB_CHECK(cudaGetLastError());
         }
         SB_LAUNCH(prof, s, "sort_ctl", 0, 0, reset_counts_kernel<<<1, 32, 0, s>>>(in.cnt, misc));
