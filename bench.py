@@ -301,7 +301,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "share_of_step": round(dk["ms"] / (t_local * 1000.0), 4), "peak_source": peak_src}
     stages = {}
     for k, v in kern.items():
-        sname = STAGE_OF.get(k, "other")
+        sname = STAGE_OF.get(k) or ("sort" if k.startswith(("sort_", "digit_")) else
+                                    "insert" if k.startswith("insert") else "other")
         stages[sname] = stages.get(sname, 0.0) + v["ms"] / args.steps
     cr = kern.get("compute_ranks")
     qps = (cr["units"] / (cr["ms"] / 1000.0)) if cr and cr["ms"] > 0 else None

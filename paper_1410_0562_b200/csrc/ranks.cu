@@ -90,11 +90,11 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  int gw, int ilp) {
     (void)ilp;
     if (j1 <= j0) return cudaSuccess;
-    // algorithmic bytes per LF step (= base): one 32 B Blk sector + g write
-    // + 0.25 B packed symbol; per string: 16 B slot offsets + the terminator g
-    // (DESIGN.md "Rooflines").  Units = LF steps.
+    // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
+    // superblock counter + g write + 0.25 B packed symbol; per string: 16 B
+    // slot offsets + the terminator g.  Units = LF steps.
     const uint64_t nstr = j1 - j0;
-    const double bytes = (32.25 + gw) * (double)n_steps + (16.0 + gw) * (double)nstr;
+    const double bytes = (40.25 + gw) * (double)n_steps + (16.0 + gw) * (double)nstr;
     const unsigned grid = grid_for(nstr, 256, 1u << 20);
     if (gw == 4) {
         SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
