@@ -290,13 +290,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     per_launch_bytes = dk["bytes"] / max(dk["launches"], 1)
     avg_ms = dk["ms"] / max(dk["launches"], 1)
     achieved = per_launch_bytes / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else None
+    # DRAM traffic of one captured launch of this kernel (ncu --set full,
+    # profiles/traffic.json) next to that launch's algorithmic bytes
     traffic = None
+    traffic_note = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
-        traffic = json.load(open(tr_path)).get(dname)
+        ent = json.load(open(tr_path)).get(dname)
+        if ent:
+            traffic = ent.get("dram_bytes_per_launch")
+            traffic_note = {"algorithmic_bytes": ent.get("algorithmic_bytes_per_launch"),
+                            "launch": ent.get("launch")}
     roof = {"kernel": dname, "bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
             "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+            "traffic_launch": traffic_note,
             "bytes_per_launch": per_launch_bytes, "avg_launch_ms": round(avg_ms, 5),
             "share_of_step": round(dk["ms"] / (t_local * 1000.0), 4), "peak_source": peak_src}
     stages = {}
