@@ -6,7 +6,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -121,7 +124,8 @@ struct setbwte_s {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;       // main stream (user's, or own_stream)
-    cudaStream_t sort_stream = nullptr;  // ConstructSA of the next block
+    cudaStream_t sort_stream = nullptr;   // ConstructSA of upcoming blocks (lane 0)
+    cudaStream_t sort_stream2 = nullptr;  // lane 1
     cudaEvent_t ev_start = nullptr, ev_sorted[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     Profiler prof;
     bool failed = false;
@@ -141,7 +145,7 @@ struct setbwte_s {
     // append scratch
     DevBuf in_bytes, in_off, text, term, slot_off, bounds, err, small;
     DevBuf saf, g, pos, bint, outbuf;
-    SortScratch sort;
+    SortScratch sort, sort2;
 
     // options
     uint64_t M = 1ull << 24;
@@ -283,13 +287,6 @@ struct BlockDesc {
     uint64_t j0, j1, S0, S1;
 };
 
-// SA_int := ConstructSA(S_jk), sieving fused; on the sort stream.
-setbwte_status sort_stage(setbwte_t h, const Packed& pk, const BlockDesc& b, uint32_t* saf) {
-    API_CHECK(h, sort_block(h->prof, h->sort_stream, h->sort, pk.text, pk.term, b.S0,
-                            (uint32_t)(b.S1 - b.S0), saf, &h->sstats));
-    return SETBWTE_OK;
-}
-
 // ComputeRanks, B_int + g_sa gather, Insert; on the main stream.
 setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc& b,
                                  const uint32_t* saf) {
@@ -325,15 +322,31 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
 }
 
 // Run Algorithm 1 over all blocks with the two-stage pipeline.
+// Run Algorithm 1 over all blocks.  ConstructSA has no B_ext dependency, so
+// two host threads ("sort lanes", one CUDA stream each) sort blocks k+1 and
+// k+2 ahead while the calling thread runs ComputeRanks / gather / Insert of
+// block k on the main stream in block order.  The sort's round trips to the
+// host (segment counts) are then hidden behind the other lanes' kernels.
+struct SortLane {
+    cudaStream_t stream = nullptr;
+    SortScratch* ws = nullptr;
+    Profiler prof;
+    SortStats st;
+    uint32_t* saf = nullptr;
+    cudaEvent_t ev_sorted = nullptr;
+};
+
 setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<BlockDesc>& blocks) {
     const size_t K = blocks.size();
+    if (K == 0) return SETBWTE_OK;
     uint64_t max_suf = 0, total = 0;
     for (const BlockDesc& b : blocks) {
         max_suf = std::max(max_suf, b.S1 - b.S0);
         total += b.S1 - b.S0;
     }
+    const int NL = K >= 2 ? 2 : 1;  // sort lanes
     // reserve everything up front: a cudaFree/cudaMalloc mid-loop would
-    // serialise the two streams
+    // serialise the streams
     uint32_t* saf2;
     uint64_t* tmp;
     uint8_t* tb;
@@ -342,32 +355,108 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
     API_CHECK(h, ensure(h->pos, max_suf, &tmp));
     API_CHECK(h, ensure(h->bint, max_suf, &tb));
     API_CHECK(h, sort_reserve(h->sort, (uint32_t)max_suf));
+    if (NL > 1) API_CHECK(h, sort_reserve(h->sort2, (uint32_t)max_suf));
     const uint64_t n_final = h->n + total;
     API_CHECK(h, ensure(h->sb_tot, ((n_final >> kSbShift) + 1) * 5 + 8, &tmp));
-    uint32_t* saf[2] = {saf2, saf2 + max_suf + 32};
-    // the sort stream starts after everything queued on the main stream so far
+    SortLane lanes[2];
+    for (int l = 0; l < NL; ++l) {
+        lanes[l].stream = l == 0 ? h->sort_stream : h->sort_stream2;
+        lanes[l].ws = l == 0 ? &h->sort : &h->sort2;
+        lanes[l].saf = saf2 + l * (max_suf + 32);
+        lanes[l].ev_sorted = h->ev_sorted[l];
+        lanes[l].prof.on = h->prof.on;
+    }
+    // the sort lanes start after everything queued on the main stream so far
     API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
-    API_CHECK(h, cudaStreamWaitEvent(h->sort_stream, h->ev_start, 0));
+    for (int l = 0; l < NL; ++l) API_CHECK(h, cudaStreamWaitEvent(lanes[l].stream, h->ev_start, 0));
+
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<char> sorted(K, 0), used(K, 0);
+    cudaError_t lane_err = cudaSuccess;
+    bool abort = false;
+    auto lane_main = [&](int l) {
+        SortLane& L = lanes[l];
+        cudaError_t e = cudaSetDevice(h->device);
+        for (size_t k = l; k < K && e == cudaSuccess; k += NL) {
+            if (k >= (size_t)NL) {
+                // SA_int buffer of this lane is free once block k-NL's gather ran
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return used[k - NL] || abort; });
+                if (abort) break;
+                lk.unlock();
+                e = cudaStreamWaitEvent(L.stream, h->ev_used[l], 0);
+                if (e != cudaSuccess) break;
+            }
+            e = sort_block(L.prof, L.stream, *L.ws, pk.text, pk.term, blocks[k].S0,
+                           (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st);
+            if (e == cudaSuccess) e = cudaEventRecord(L.ev_sorted, L.stream);
+            std::lock_guard<std::mutex> lk(mu);
+            if (e != cudaSuccess) {
+                lane_err = e;
+                abort = true;
+            } else {
+                sorted[k] = 1;
+            }
+            cv.notify_all();
+        }
+    };
+    std::vector<std::thread> threads;
+    for (int l = 0; l < NL; ++l) threads.emplace_back(lane_main, l);
+
     setbwte_status st = SETBWTE_OK;
-    if (K > 0) st = sort_stage(h, pk, blocks[0], saf[0]);
-    for (size_t k = 0; k < K && st == SETBWTE_OK; ++k) {
-        API_CHECK(h, cudaEventRecord(h->ev_sorted[k & 1], h->sort_stream));
-        API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_sorted[k & 1], 0));
-        st = rank_insert_stage(h, pk, blocks[k], saf[k & 1]);
+    for (size_t k = 0; k < K; ++k) {
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return sorted[k] || abort; });
+            if (abort) break;
+        }
+        const int l = (int)(k % NL);
+        cudaError_t e = cudaStreamWaitEvent(h->stream, lanes[l].ev_sorted, 0);
+        if (e != cudaSuccess) {
+            st = from_cuda(h, e);
+        } else {
+            st = rank_insert_stage(h, pk, blocks[k], lanes[l].saf);
+            if (st == SETBWTE_OK) {
+                e = cudaEventRecord(h->ev_used[l], h->stream);
+                if (e != cudaSuccess) st = from_cuda(h, e);
+            }
+        }
+        std::lock_guard<std::mutex> lk(mu);
         if (st != SETBWTE_OK) {
             if (k > 0) h->failed = true;  // a partially applied append cannot be rolled back
+            abort = true;
+            cv.notify_all();
             break;
         }
-        // SA_int buffer k&1 is free again once this block's gather has run
-        API_CHECK(h, cudaEventRecord(h->ev_used[k & 1], h->stream));
-        if (k + 1 < K) {
-            if (k >= 1) API_CHECK(h, cudaStreamWaitEvent(h->sort_stream, h->ev_used[(k + 1) & 1], 0));
-            st = sort_stage(h, pk, blocks[k + 1], saf[(k + 1) & 1]);
-        }
+        used[k] = 1;
+        cv.notify_all();
     }
-    // main stream joins the sort stream before the call returns
-    API_CHECK(h, cudaEventRecord(h->ev_start, h->sort_stream));
-    API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
+    for (std::thread& t : threads) t.join();
+    if (st == SETBWTE_OK && lane_err != cudaSuccess) {
+        if (h->n != 0) h->failed = true;
+        st = from_cuda(h, lane_err);
+    }
+    // the main stream joins the sort lanes; their statistics merge into the handle's
+    for (int l = 0; l < NL; ++l) {
+        API_CHECK(h, cudaEventRecord(h->ev_start, lanes[l].stream));
+        API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
+        API_CHECK(h, cudaStreamSynchronize(lanes[l].stream));
+        API_CHECK(h, lanes[l].prof.resolve());
+        for (auto& kv : lanes[l].prof.k) {
+            KStat& d = h->prof.k[kv.first];
+            d.launches += kv.second.launches;
+            d.ms += kv.second.ms;
+            d.bytes += kv.second.bytes;
+            d.units += kv.second.units;
+        }
+        h->prof.total_launches += lanes[l].prof.total_launches;
+        h->sstats.digit_passes += lanes[l].st.digit_passes;
+        h->sstats.rounds += lanes[l].st.rounds;
+        h->sstats.active_per_pass.insert(h->sstats.active_per_pass.end(),
+                                         lanes[l].st.active_per_pass.begin(),
+                                         lanes[l].st.active_per_pass.end());
+    }
     return st;
 }
 
@@ -490,6 +579,7 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream2, cudaStreamNonBlocking);
     for (cudaEvent_t* ev : {&h->ev_start, &h->ev_sorted[0], &h->ev_sorted[1], &h->ev_used[0],
                             &h->ev_used[1]})
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
@@ -525,13 +615,18 @@ void setbwte_destroy(setbwte_t h) {
                       &h->bint, &h->outbuf, &h->sort.sa0, &h->sort.sa1, &h->sort.k0,
                       &h->sort.k1, &h->sort.segs_a, &h->sort.segs_b, &h->sort.small_a,
                       &h->sort.small_b, &h->sort.chunks, &h->sort.hist, &h->sort.ctr,
-                      &h->sort.gtot, &h->sort.groups};
+                      &h->sort.gtot, &h->sort.groups, &h->sort2.sa0, &h->sort2.sa1,
+                      &h->sort2.k0, &h->sort2.k1, &h->sort2.segs_a, &h->sort2.segs_b,
+                      &h->sort2.small_a, &h->sort2.small_b, &h->sort2.chunks, &h->sort2.hist,
+                      &h->sort2.ctr, &h->sort2.gtot, &h->sort2.groups};
     for (DevBuf* b : bufs) free_buf(*b);
     if (h->sort_stream) cudaStreamSynchronize(h->sort_stream);
+    if (h->sort_stream2) cudaStreamSynchronize(h->sort_stream2);
     for (cudaEvent_t ev : {h->ev_start, h->ev_sorted[0], h->ev_sorted[1], h->ev_used[0],
                            h->ev_used[1]})
         if (ev) cudaEventDestroy(ev);
     if (h->sort_stream) cudaStreamDestroy(h->sort_stream);
+    if (h->sort_stream2) cudaStreamDestroy(h->sort_stream2);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }

@@ -1047,18 +1047,13 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.term = term;
     B.base = slot_base;
 
-    static int attr_dev = -1;
-    int dev = 0;
-    SB_CHECK(cudaGetDevice(&dev));
+    // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
     constexpr size_t sm_d = scatter_smem();
-    if (attr_dev != dev) {
-        SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
-        SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
-        attr_dev = dev;
-    }
+    SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
+    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
 
     SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
               keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(text, term,
