@@ -143,7 +143,7 @@ struct setbwte_s {
     DevBuf d_C, sb_tot;
 
     // append scratch
-    DevBuf in_bytes, in_off, text, term, slot_off, bounds, err, small;
+    DevBuf in_bytes, in_off, text, term, slot_off, gfirst, bounds, err, small;
     DevBuf saf, g, pos, bint, outbuf;
     SortScratch sort, sort2;
 
@@ -207,6 +207,7 @@ setbwte_status pack_input(setbwte_t h, const uint8_t* d_bytes, const uint64_t* d
     API_CHECK(h, ensure(h->text, 2 * n_groups + 8, &pk.text));
     API_CHECK(h, ensure(h->term, n_groups + 8, &pk.term));
     API_CHECK(h, ensure(h->slot_off, m + 2, &pk.slot_off));
+    API_CHECK(h, ensure(h->gfirst, n_groups + 2, &pk.gfirst));
     DevErr* derr;
     API_CHECK(h, ensure(h->err, 1, &derr));
     DevErr init{~0ull, 0, 0};
@@ -299,10 +300,7 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // g := ComputeRanks(S_jk, B_ext)
     setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw);
     if (st != SETBWTE_OK) return st;
-    // B_int := B(S_jk, SA_int) and g_sa / pos, fused
-    API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
-                               (uint32_t)n_suf, pos, gw, bint));
-    // B_ext := Insert(B_int, g_sa, B_ext)
+    // B_ext := Insert(B_int, g_sa, B_ext) -- buffers first
     const uint64_t n_out = h->n + n_suf;
     const uint64_t nblk = (n_out >> 6) + 1;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
@@ -311,10 +309,15 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     uint64_t *osb, *tot;
     API_CHECK(h, ensure(h->blk[nxt], nblk, &ob));
     API_CHECK(h, ensure(h->sb[nxt], nsb * 4, &osb));
-    API_CHECK(h, ensure(h->sb_tot, nsb * 4 + 4 + nsb + 2, &tot));  // totals + sb_start
+    API_CHECK(h, ensure(h->sb_tot, nsb * 5 + 8, &tot));  // totals + sb_start
+    uint64_t* sb_start = tot + 4 * (nsb + 1);
+    // B_int := B(S_jk, SA_int), g_sa / pos and the superblock
+    // slices of pos, fused
+    API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
+                               (uint32_t)n_suf, pos, gw, bint, sb_start, nsb));
     const uint64_t m_new = h->m + (b.j1 - b.j0);
     API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_suf, ob, osb,
-                               tot, m_new, (uint64_t*)h->d_C.p));
+                               tot, sb_start, m_new, (uint64_t*)h->d_C.p));
     h->cur = nxt;
     h->n = n_out;
     h->m = m_new;
@@ -503,6 +506,7 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* d_bytes, const uint64_t* 
         build_stats(h);
         return SETBWTE_OK;
     }
+    if (m >= 0xFFFFFFFFull) return SETBWTE_E_UNSUPPORTED;  // u32 string ids in the packer
     PackOut po;
     setbwte_status st = pack_input(h, d_bytes, d_off, m, &po);
     if (st != SETBWTE_OK) return st;
@@ -610,7 +614,7 @@ void setbwte_destroy(setbwte_t h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     DevBuf* bufs[] = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0], &h->sb[1],
-                      &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term,
+                      &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term, &h->gfirst,
                       &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos,
                       &h->bint, &h->outbuf, &h->sort.sa0, &h->sort.sa1, &h->sort.k0,
                       &h->sort.k1, &h->sort.segs_a, &h->sort.segs_b, &h->sort.small_a,

@@ -49,20 +49,6 @@ __device__ __forceinline__ uint32_t warp_incl(uint32_t v, uint32_t lane) {
 
 constexpr uint32_t kStage = 16384;  // inserted entries staged in shared memory per superblock
 
-// sb_start[s] = first inserted index with pos >= s * 2^16, s in [0, nsb]: the
-// "vectorised binary search" of P:158 done as one parallel pass over pos
-// (each superblock boundary has exactly one writer).
-template <class G>
-__global__ void sb_bounds_kernel(const G* __restrict__ pos, uint64_t n_ins, uint64_t nsb,
-                                 uint64_t* __restrict__ sb_start) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n_ins;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t cur = i < n_ins ? ((uint64_t)pos[i] >> kSbShift) : nsb;
-        const uint64_t first = i > 0 ? ((uint64_t)pos[i - 1] >> kSbShift) + 1 : 0;
-        for (uint64_t sbi = first; sbi <= cur && sbi <= nsb; ++sbi) sb_start[sbi] = i;
-    }
-}
-
 template <class G>
 __global__ void __launch_bounds__(kInsNt) insert_kernel(
     const Blk* __restrict__ in_blk, uint64_t n_in, const G* __restrict__ pos,
@@ -120,39 +106,60 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
                 xh = funnel(b0[2], b1[2], sh);
                 xd = funnel(b0[3], b1[3], sh);
             }
-            uint32_t filled = 0, used = 0;
-            for (uint32_t k = 0; k < cnt; ++k) {
-                uint32_t t, b;
-                if (staged) {
-                    const uint32_t e = ent[arel + k];
-                    t = e & 63u;
-                    b = e >> 6;
-                } else {
-                    t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
-                    b = __ldg(bint + a + k);
-                }
-                const uint32_t run = t - filled;
-                if (run) {
-                    const uint64_t m = (1ull << run) - 1ull;
-                    ol |= ((xl >> used) & m) << filled;
-                    oh |= ((xh >> used) & m) << filled;
-                    od |= ((xd >> used) & m) << filled;
-                    used += run;
-                }
-                ol |= (uint64_t)(b & 1u) << t;
-                oh |= (uint64_t)((b >> 1) & 1u) << t;
-                od |= (uint64_t)((b >> 2) & 1u) << t;
-                filled = t + 1;
-            }
+            // merge one 32-symbol half at a time: all shifts stay 32-bit
             const uint64_t span = n_out - ow0;
             const uint32_t lim = span >= 64 ? 64u : (uint32_t)span;
-            if (lim > filled) {
-                const uint32_t run = lim - filled;
-                const uint64_t m = run == 64 ? ~0ull : (1ull << run) - 1ull;
-                ol |= ((xl >> used) & m) << filled;
-                oh |= ((xh >> used) & m) << filled;
-                od |= ((xd >> used) & m) << filled;
+            uint32_t oo[2][3];
+            uint32_t k = 0, used = 0;  // inserted consumed, external bits consumed
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const uint32_t base = 32u * hf;
+                const uint32_t wl = (uint32_t)(xl >> used), wh = (uint32_t)(xh >> used),
+                               wd = (uint32_t)(xd >> used);
+                uint32_t al = 0, ah = 0, ad = 0, filled = 0, u = 0;
+                const uint32_t hl = lim > base ? min(lim - base, 32u) : 0u;
+                while (k < cnt) {
+                    uint32_t t, b;
+                    if (staged) {
+                        const uint32_t e = ent[arel + k];
+                        t = e & 63u;
+                        b = e >> 6;
+                    } else {
+                        t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
+                        b = __ldg(bint + a + k);
+                    }
+                    if (t >= base + 32u) break;
+                    const uint32_t tt = t - base;
+                    const uint32_t run = tt - filled;
+                    if (run) {
+                        const uint32_t m = (1u << run) - 1u;
+                        al |= ((wl >> u) & m) << filled;
+                        ah |= ((wh >> u) & m) << filled;
+                        ad |= ((wd >> u) & m) << filled;
+                        u += run;
+                    }
+                    al |= (b & 1u) << tt;
+                    ah |= ((b >> 1) & 1u) << tt;
+                    ad |= ((b >> 2) & 1u) << tt;
+                    filled = tt + 1;
+                    ++k;
+                }
+                if (hl > filled) {
+                    const uint32_t run = hl - filled;
+                    const uint32_t m = run == 32 ? ~0u : (1u << run) - 1u;
+                    al |= ((wl >> u) & m) << filled;
+                    ah |= ((wh >> u) & m) << filled;
+                    ad |= ((wd >> u) & m) << filled;
+                    u += run;
+                }
+                used += u;
+                oo[hf][0] = al;
+                oo[hf][1] = ah;
+                oo[hf][2] = ad;
             }
+            ol = (uint64_t)oo[0][0] | ((uint64_t)oo[1][0] << 32);
+            oh = (uint64_t)oo[0][1] | ((uint64_t)oo[1][1] << 32);
+            od = (uint64_t)oo[0][2] | ((uint64_t)oo[1][2] << 32);
             const uint64_t V = lim == 64 ? ~0ull : ((1ull << lim) - 1ull);  // real positions
 #pragma unroll
             for (int c = 0; c < 4; ++c) c4[c] = __popcll(match_plane(c, ol, oh, od) & V);
@@ -226,29 +233,19 @@ __global__ void __launch_bounds__(1024) sb_scan_kernel(const uint64_t* __restric
 
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
-                          Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot, uint64_t m_new,
-                          uint64_t* d_C) {
+                          Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
+                          const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C) {
     const uint64_t n_out = n_in + n_ins;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
     // algorithmic bytes: read n_in/2 + write n_out/2 (4 bits/symbol) + (gw + 1) B per inserted
     const double bytes = 0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins;
     const unsigned grid = (unsigned)(nsb < 148u * 64u ? nsb : 148u * 64u);
-    uint64_t* sb_start = sb_tot + 4 * (nsb + 1);  // caller sized sb_tot for both
-    const unsigned gb = grid_for(n_ins + 1, 256);
     if (gw == 4) {
-        SB_LAUNCH(prof, s, "insert_bounds", (double)gw * n_ins, n_ins,
-                  sb_bounds_kernel<uint32_t><<<gb, 256, 0, s>>>((const uint32_t*)pos, n_ins, nsb,
-                                                                 sb_start));
-        SB_CHECK(cudaGetLastError());
         SB_LAUNCH(prof, s, "insert", bytes, n_out,
                   insert_kernel<uint32_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint32_t*)pos,
                                                                    bint, n_ins, out_blk, n_out,
                                                                    sb_tot, sb_start));
     } else {
-        SB_LAUNCH(prof, s, "insert_bounds", (double)gw * n_ins, n_ins,
-                  sb_bounds_kernel<uint64_t><<<gb, 256, 0, s>>>((const uint64_t*)pos, n_ins, nsb,
-                                                                 sb_start));
-        SB_CHECK(cudaGetLastError());
         SB_LAUNCH(prof, s, "insert", bytes, n_out,
                   insert_kernel<uint64_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint64_t*)pos,
                                                                    bint, n_ins, out_blk, n_out,

@@ -90,6 +90,7 @@ struct Packed {
     uint32_t* text;       // 2-bit slot text
     uint32_t* term;       // terminator bitmap
     uint64_t* slot_off;   // m+1 slot offsets (slot_off[j] = offsets[j] + j)
+    uint32_t* gfirst;     // string owning slot 32g, per 32-slot group
     uint64_t n_slots;
 };
 cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
@@ -129,15 +130,17 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
                                  int gw, int ilp);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64)
+// With sb_start != NULL also writes sb_start[0..nsb] (superblock slices of pos).
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
-                          const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint);
+                          const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
+                          uint64_t* sb_start = nullptr, uint64_t nsb = 0);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
-                          Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot, uint64_t m_new,
-                          uint64_t* d_C);
+                          Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
+                          const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C);
 cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
                               uint64_t n, const uint8_t* code_of, const uint8_t* c,
                               const uint64_t* k, uint64_t q, uint64_t* out);

@@ -8,56 +8,92 @@
 
 namespace setbwte {
 
-// slot_off[j] = offsets[j] + j; flags non-CSR offsets.
+// slot_off[j] = offsets[j] + j; flags non-CSR offsets; gfirst[g] = the string
+// owning slot 32g (each string writes the groups that start inside it).
 __global__ void slot_off_kernel(const uint64_t* __restrict__ off, uint64_t m, uint64_t n_bytes,
-                                uint64_t* __restrict__ slot_off, int* __restrict__ bad) {
+                                uint64_t* __restrict__ slot_off, uint32_t* __restrict__ gfirst,
+                                int* __restrict__ bad) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= m;
          j += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t o = off[j];
         slot_off[j] = o + j;
         if (j == 0 && o != 0) *bad = 1;
         if (j == m && o != n_bytes) *bad = 1;
-        if (j < m && off[j + 1] < o) *bad = 1;
+        if (j < m) {
+            const uint64_t o1 = off[j + 1];
+            if (o1 < o) {
+                *bad = 1;
+                continue;
+            }
+            const uint64_t a = o + j, e = o1 + j + 1;  // slots [a, e)
+            for (uint64_t g = (a + 31) >> 5; (g << 5) < e; ++g) gfirst[g] = (uint32_t)j;
+        }
     }
 }
 
-// One thread per 32 slots: two text words + one terminator word.
-__global__ void pack_kernel(const uint8_t* __restrict__ bytes, uint64_t n_bytes,
-                            const uint64_t* __restrict__ slot_off, uint64_t m, uint64_t n_slots,
-                            const uint8_t* __restrict__ code_of, uint32_t* __restrict__ text,
-                            uint32_t* __restrict__ term, unsigned long long* __restrict__ err_pos) {
+// One warp per 1024 slots (32 groups of 32): the warp stages the <= 1024
+// ASCII bytes of its slots in shared memory with 16-byte loads, then each lane
+// packs one group: two text words + one terminator word.
+constexpr int kPackWarps = 8;
+__global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
+    const uint8_t* __restrict__ bytes, uint64_t n_bytes, const uint64_t* __restrict__ slot_off,
+    const uint32_t* __restrict__ gfirst, uint64_t m, uint64_t n_slots,
+    const uint8_t* __restrict__ code_of_g, uint32_t* __restrict__ text, uint32_t* __restrict__ term,
+    unsigned long long* __restrict__ err_pos) {
+    __shared__ __align__(16) uint8_t sbuf[kPackWarps][1024 + 80];
+    __shared__ uint8_t code_of[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) code_of[i] = code_of_g[i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* sb = sbuf[wib];
     const uint64_t n_groups = (n_slots + 31) >> 5;
-    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n_groups;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s0 = g << 5;
-        // largest j with slot_off[j] <= s0
-        uint64_t lo = 0, hi = m;  // invariant: slot_off[lo] <= s0 < slot_off[hi] (when valid)
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (slot_off[mid] <= s0) lo = mid; else hi = mid;
-        }
-        uint64_t j = lo;
-        uint64_t next = slot_off[j + 1];
-        uint32_t w0 = 0, w1 = 0, tw = 0;
-        const int cnt = (int)min((uint64_t)32, n_slots - s0);
-        for (int t = 0; t < cnt; ++t) {
-            const uint64_t s = s0 + t;
-            while (s >= next && j + 1 < m) { ++j; next = slot_off[j + 1]; }
-            uint32_t code = 0;
-            if (s == next - 1) {
-                tw |= 1u << (31 - t);
+    const uint64_t nw = (uint64_t)gridDim.x * kPackWarps;
+    for (uint64_t wbase = ((uint64_t)blockIdx.x * kPackWarps + wib) << 10; wbase < n_slots;
+         wbase += nw << 10) {
+        const uint64_t g = (wbase >> 5) + lane;
+        const bool gv = g < n_groups;
+        uint64_t j = gv ? min((uint64_t)gfirst[g], m - 1) : 0;
+        const uint64_t j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
+        const uint64_t bp_first = wbase - min(j0, wbase);
+        const uint64_t al = bp_first & ~15ull;
+        for (uint32_t k = lane; k < (1024 + 80) / 16; k += 32) {
+            const uint64_t a = al + 16ull * k;
+            if (a + 16 <= n_bytes) {
+                *reinterpret_cast<uint4*>(sb + 16 * k) = __ldg(reinterpret_cast<const uint4*>(bytes + a));
             } else {
-                const uint64_t bp = s - j;  // byte position: slots minus terminators before
-                if (bp < n_bytes) {
-                    const uint8_t c = code_of[bytes[bp]];
-                    if (c > 3) atomicMin(err_pos, (unsigned long long)bp); else code = c;
-                }
+                for (int q = 0; q < 16; ++q) sb[16 * k + q] = a + q < n_bytes ? bytes[a + q] : 0;
             }
-            if (t < 16) w0 |= code << (30 - 2 * t); else w1 |= code << (30 - 2 * (t - 16));
         }
-        text[2 * g] = w0;
-        text[2 * g + 1] = w1;
-        term[g] = tw;
+        __syncwarp();
+        if (gv) {
+            const uint64_t s0 = g << 5;
+            uint64_t next = slot_off[j + 1];
+            uint32_t w0 = 0, w1 = 0, tw = 0;
+            const int cnt = (int)min((uint64_t)32, n_slots - s0);
+            for (int t = 0; t < cnt; ++t) {
+                const uint64_t s = s0 + t;
+                while (s >= next && j + 1 < m) {
+                    ++j;
+                    next = slot_off[j + 1];
+                }
+                uint32_t code = 0;
+                if (s == next - 1) {
+                    tw |= 1u << (31 - t);
+                } else {
+                    const uint64_t bp = s - j;  // byte position: slots minus terminators before
+                    const uint64_t li = bp - al;
+                    if (bp < n_bytes && li < 1024 + 80) {
+                        const uint8_t c = code_of[sb[li]];
+                        if (c > 3) atomicMin(err_pos, (unsigned long long)bp); else code = c;
+                    }
+                }
+                if (t < 16) w0 |= code << (30 - 2 * t); else w1 |= code << (30 - 2 * (t - 16));
+            }
+            text[2 * g] = w0;
+            text[2 * g + 1] = w1;
+            term[g] = tw;
+        }
+        __syncwarp();
     }
 }
 
@@ -67,17 +103,18 @@ cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
                         int* d_bad_offsets) {
     SB_LAUNCH(prof, s, "slot_offsets", 16.0 * (m + 1), m + 1,
               slot_off_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(d_off, m, n_bytes, pk.slot_off,
-                                                                   d_bad_offsets));
+                                                                   pk.gfirst, d_bad_offsets));
     SB_CHECK(cudaGetLastError());
     const uint64_t n_groups = (pk.n_slots + 31) >> 5;
     // padding words past the end must read as zero
     SB_CHECK(cudaMemsetAsync(pk.text + 2 * n_groups, 0, 4 * sizeof(uint32_t), s));
     SB_CHECK(cudaMemsetAsync(pk.term + n_groups, 0, 4 * sizeof(uint32_t), s));
     // algorithmic bytes: 1 B read per base + 3 bits written per slot
+    const uint64_t n_warps = (pk.n_slots + 1023) >> 10;
     SB_LAUNCH(prof, s, "pack", (double)n_bytes + 0.375 * pk.n_slots, n_bytes,
-              pack_kernel<<<grid_for(n_groups, 256, 148u * 64u), 256, 0, s>>>(
-                  d_bytes, n_bytes, pk.slot_off, m, pk.n_slots, d_code_of, pk.text, pk.term,
-                  d_err_pos));
+              pack_kernel<<<grid_for(n_warps, kPackWarps, 148u * 16u), kPackWarps * 32, 0, s>>>(
+                  d_bytes, n_bytes, pk.slot_off, pk.gfirst, m, pk.n_slots, d_code_of, pk.text,
+                  pk.term, d_err_pos));
     return cudaGetLastError();
 }
 

@@ -108,28 +108,54 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
     return cudaGetLastError();
 }
 
+// Fused A2 + A4 (+ the superblock slices Insert needs): pos[i], B_int[i], and
+// sb_start[s] = first i with pos[i] >= s * 2^16 (the "vectorised binary
+// search" of P:158 as one pass: every superblock boundary has one writer).
 template <class G>
 __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
                               uint64_t slot_base, const uint32_t* __restrict__ sa,
                               const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
-                              uint8_t* __restrict__ bint) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_suf;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        // streaming (evict-first) accesses for SA / pos / B_int keep the
-        // just-written g resident in L2 for the random gather
-        const uint32_t sl = __ldcs(sa + i);
-        const uint64_t p = slot_base + sl;
-        __stcs(pos + i, (G)((g ? (uint64_t)__ldg(g + sl) : 0ull) + i));
-        uint8_t b;
-        if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
-        else b = (uint8_t)text_sym(text, p - 1);
-        __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
+                              uint8_t* __restrict__ bint, uint64_t* __restrict__ sb_start,
+                              uint64_t nsb) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t iters = (n_suf + stride - 1) / stride;  // warp-uniform trip count
+    for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t i = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        const bool v = i < n_suf;
+        uint64_t pv = 0;
+        if (v) {
+            // streaming (evict-first) SA / pos / B_int accesses leave L2 to g
+            const uint32_t sl = __ldcs(sa + i);
+            const uint64_t p = slot_base + sl;
+            pv = (g ? (uint64_t)__ldg(g + sl) : 0ull) + i;
+            __stcs(pos + i, (G)pv);
+            uint8_t b;
+            if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
+            else b = (uint8_t)text_sym(text, p - 1);
+            __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
+        }
+        if (sb_start) {
+            uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
+            if (v) {
+                if (lane == 0 && i > 0) {
+                    const uint32_t sl1 = sa[i - 1];
+                    prev = (g ? (uint64_t)__ldg(g + sl1) : 0ull) + (i - 1);
+                }
+                const uint64_t cur = pv >> kSbShift;
+                const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
+                for (uint64_t s = first; s <= cur && s <= nsb; ++s) sb_start[s] = i;
+                if (i + 1 == n_suf)
+                    for (uint64_t s = cur + 1; s <= nsb; ++s) sb_start[s] = n_suf;
+            }
+        }
     }
 }
 
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
-                          const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint) {
+                          const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
+                          uint64_t* sb_start, uint64_t nsb) {
     // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol + term bit)
     const double bytes = (5.375 + 2.0 * gw) * n_suf;
     const unsigned grid = grid_for(n_suf, 256, 148u * 64u);
@@ -137,12 +163,12 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint32_t*)g, n_suf,
-                                                               (uint32_t*)pos, bint));
+                                                               (uint32_t*)pos, bint, sb_start, nsb));
     } else {
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint64_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint64_t*)g, n_suf,
-                                                               (uint64_t*)pos, bint));
+                                                               (uint64_t*)pos, bint, sb_start, nsb));
     }
     return cudaGetLastError();
 }

@@ -290,9 +290,13 @@ __global__ void keygen_kernel(const uint32_t* __restrict__ text, const uint32_t*
 // ---------------------------------------------------------------------------
 __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ saf, uint32_t n,
                             Lists in, Lists out, uint32_t* misc) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        sa0[i] = (uint32_t)i;
+    // a LARGE first segment reads its slots as "iota" (meta bit) and never
+    // needs them materialised; smaller blocks go straight to the segment sorts
+    if (n <= kCapM) {
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            sa0[i] = (uint32_t)i;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         for (int c = 0; c < NCLASS; ++c) {
             in.cnt[c] = 0;
@@ -300,7 +304,7 @@ __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ s
         }
         for (int c = 0; c < M_N; ++c) misc[c] = 0;
         if (n == 1) saf[0] = 0;
-        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 1, 1)});
+        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 1, n > kCapM ? 1u : 0u)});
     }
 }
 
@@ -406,7 +410,8 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
                     const uint32_t p = p0 + u * kDigNt + tid;
                     key[u] = 0;
                     if (p < ch.end) {
-                        key[u] = suffix_key(B.text, B.term, B.base + __ldg(S + p), s.word);
+                        const uint32_t sl = meta_iota(s.meta) ? p : __ldg(S + p);
+                        key[u] = suffix_key(B.text, B.term, B.base + sl, s.word);
                         K[p] = key[u];
                     }
                 }
@@ -505,14 +510,15 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
                 flag = 0x80000000u;
             } else {
                 const uint32_t cbuf = all_one ? buf : 1u - buf;
+                const uint32_t ciota = all_one ? meta_iota(s.meta) : 0u;  // data not moved
                 c.start = s.start + excl;
                 c.len = total;
                 if (shift == 0) {
                     c.word = s.word + 1;
-                    c.meta = make_meta(24, cbuf, 0);
+                    c.meta = make_meta(24, cbuf, 0, ciota);
                 } else {
                     c.word = s.word;
-                    c.meta = make_meta(shift - 8, cbuf, 1);
+                    c.meta = make_meta(shift - 8, cbuf, 1, ciota);
                 }
                 cls = class_of(c);
                 local = atomicAdd(&ccount[cls], 1u);
@@ -694,35 +700,53 @@ __device__ __forceinline__ void warp_tail(const uint2* buf, const Seg& s, const 
 // BIT2..BIT16: one warp per segment, register bitonic network
 // ---------------------------------------------------------------------------
 // Ascending bitonic sort of N = 32*NIT values, lane-major (element e = lane*NIT
-// + r lives in register v[r] of lane e/NIT): strides below NIT stay in
-// registers, larger ones are one shuffle per value.
+// + r lives in register v[r] of lane e/NIT).  Each merge stage starts with the
+// "mirror" comparator e <-> e^(k-1), so every comparator sorts ascending and no
+// direction selects are needed; strides below NIT stay in registers, larger
+// ones are one shuffle per value.
 template <int NIT>
 __device__ __forceinline__ void warp_bitonic(uint32_t (&v)[NIT]) {
     constexpr int N = 32 * NIT;
     const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 2; k <= N; k <<= 1) {
+        if (k <= NIT) {
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int r = 0; r < NIT; ++r) {
+                const int q = r ^ (k - 1);
+                if (r < q) {
+                    const uint32_t a = v[r], b = v[q];
+                    v[r] = min(a, b);
+                    v[q] = max(a, b);
+                }
+            }
+        } else {
+            const int lm = k / NIT - 1;
+            const bool lower = (lane & (uint32_t)(k / NIT / 2)) == 0;
+            uint32_t o[NIT];
+#pragma unroll
+            for (int r = 0; r < NIT; ++r) o[r] = __shfl_xor_sync(0xFFFFFFFFu, v[NIT - 1 - r], lm);
+#pragma unroll
+            for (int r = 0; r < NIT; ++r) v[r] = lower ? min(v[r], o[r]) : max(v[r], o[r]);
+        }
+#pragma unroll
+        for (int j = k >> 2; j > 0; j >>= 1) {
             if (j < NIT) {
 #pragma unroll
                 for (int r = 0; r < NIT; ++r) {
                     if ((r & j) == 0) {
-                        const bool up = (((lane * NIT + r) & k) == 0);
                         const uint32_t a = v[r], b = v[r | j];
-                        const uint32_t mn = min(a, b), mx = max(a, b);
-                        v[r] = up ? mn : mx;
-                        v[r | j] = up ? mx : mn;
+                        v[r] = min(a, b);
+                        v[r | j] = max(a, b);
                     }
                 }
             } else {
                 const int lj = j / NIT;
-                const bool lower = (lane & lj) == 0;
+                const bool lower = (lane & (uint32_t)lj) == 0;
 #pragma unroll
                 for (int r = 0; r < NIT; ++r) {
                     const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v[r], lj);
-                    const bool up = (((lane * NIT + r) & k) == 0);
-                    v[r] = (lower == up) ? min(v[r], o) : max(v[r], o);
+                    v[r] = lower ? min(v[r], o) : max(v[r], o);
                 }
             }
         }

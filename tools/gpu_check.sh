@@ -11,3 +11,6 @@ print('kernels', d['kernel_ms_per_step'])
 print('roofline', d['roofline']['kernel'], d['roofline']['frac'])
 PY
 tail -2 gpurun_out/bench_$tag.err
+# serialized per-kernel times of one c2 build (ncu launch list)
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv python tools/run_once.py > /dev/null 2>&1
+python tools/summarize_launches.py gpurun_out/launches_$tag.csv | head -30

@@ -26,7 +26,8 @@ for r in rows[hi + 1:]:
     cur.append((short, us))
 if cur:
     steps.append(cur)
-step = max((st for st in steps if not any(n.startswith("decode") for n, _ in st)), key=len)
+cands = [st for st in steps if not any(n.startswith("decode") for n, _ in st)] or steps
+step = max(cands, key=len)
 agg = collections.OrderedDict()
 for n, us in step:
     a = agg.setdefault(n, [0, 0.0])
