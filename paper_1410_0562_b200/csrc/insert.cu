@@ -47,6 +47,63 @@ __device__ __forceinline__ uint32_t warp_incl(uint32_t v, uint32_t lane) {
     return v;
 }
 
+// Merge one 64-symbol output word: the inserted symbols (offset t in the word,
+// code+$ bits b) in order, the external symbols (window x*, 64 consecutive
+// external symbols) filling the other positions; one 32-symbol half at a time
+// so every shift is 32-bit.  STAGED: entries come from shared memory.
+template <bool STAGED, class G>
+__device__ __forceinline__ void merge_word(uint32_t (&oo)[2][3], uint64_t xl, uint64_t xh,
+                                           uint64_t xd, uint32_t lim, uint32_t cnt,
+                                           const uint16_t* ent, const G* __restrict__ pos,
+                                           const uint8_t* __restrict__ bint, uint64_t a,
+                                           uint64_t ow0) {
+    uint32_t k = 0, used = 0;  // inserted consumed, external bits consumed
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+        const uint32_t base = 32u * hf;
+        const uint32_t wl = (uint32_t)(xl >> used), wh = (uint32_t)(xh >> used),
+                       wd = (uint32_t)(xd >> used);
+        uint32_t al = 0, ah = 0, ad = 0, filled = 0, u = 0;
+        const uint32_t hl = lim > base ? min(lim - base, 32u) : 0u;
+        while (k < cnt) {
+            uint32_t t, b;
+            if (STAGED) {
+                const uint32_t e = ent[k];
+                t = e & 63u;
+                b = e >> 6;
+            } else {
+                t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
+                b = __ldg(bint + a + k);
+            }
+            if (t >= base + 32u) break;
+            const uint32_t tt = t - base;
+            const uint32_t run = tt - filled;
+            const uint32_t m = (1u << run) - 1u;  // run <= 31
+            al |= ((wl >> u) & m) << filled;
+            ah |= ((wh >> u) & m) << filled;
+            ad |= ((wd >> u) & m) << filled;
+            u += run;
+            al |= (b & 1u) << tt;
+            ah |= ((b >> 1) & 1u) << tt;
+            ad |= ((b >> 2) & 1u) << tt;
+            filled = tt + 1;
+            ++k;
+        }
+        if (hl > filled) {
+            const uint32_t run = hl - filled;
+            const uint32_t m = run == 32 ? ~0u : (1u << run) - 1u;
+            al |= ((wl >> u) & m) << filled;
+            ah |= ((wh >> u) & m) << filled;
+            ad |= ((wd >> u) & m) << filled;
+            u += run;
+        }
+        used += u;
+        oo[hf][0] = al;
+        oo[hf][1] = ah;
+        oo[hf][2] = ad;
+    }
+}
+
 constexpr uint32_t kStage = 16384;  // inserted entries staged in shared memory per superblock
 
 template <class G>
@@ -110,53 +167,10 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
             const uint64_t span = n_out - ow0;
             const uint32_t lim = span >= 64 ? 64u : (uint32_t)span;
             uint32_t oo[2][3];
-            uint32_t k = 0, used = 0;  // inserted consumed, external bits consumed
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const uint32_t base = 32u * hf;
-                const uint32_t wl = (uint32_t)(xl >> used), wh = (uint32_t)(xh >> used),
-                               wd = (uint32_t)(xd >> used);
-                uint32_t al = 0, ah = 0, ad = 0, filled = 0, u = 0;
-                const uint32_t hl = lim > base ? min(lim - base, 32u) : 0u;
-                while (k < cnt) {
-                    uint32_t t, b;
-                    if (staged) {
-                        const uint32_t e = ent[arel + k];
-                        t = e & 63u;
-                        b = e >> 6;
-                    } else {
-                        t = (uint32_t)((uint64_t)__ldg(pos + a + k) - ow0);
-                        b = __ldg(bint + a + k);
-                    }
-                    if (t >= base + 32u) break;
-                    const uint32_t tt = t - base;
-                    const uint32_t run = tt - filled;
-                    if (run) {
-                        const uint32_t m = (1u << run) - 1u;
-                        al |= ((wl >> u) & m) << filled;
-                        ah |= ((wh >> u) & m) << filled;
-                        ad |= ((wd >> u) & m) << filled;
-                        u += run;
-                    }
-                    al |= (b & 1u) << tt;
-                    ah |= ((b >> 1) & 1u) << tt;
-                    ad |= ((b >> 2) & 1u) << tt;
-                    filled = tt + 1;
-                    ++k;
-                }
-                if (hl > filled) {
-                    const uint32_t run = hl - filled;
-                    const uint32_t m = run == 32 ? ~0u : (1u << run) - 1u;
-                    al |= ((wl >> u) & m) << filled;
-                    ah |= ((wh >> u) & m) << filled;
-                    ad |= ((wd >> u) & m) << filled;
-                    u += run;
-                }
-                used += u;
-                oo[hf][0] = al;
-                oo[hf][1] = ah;
-                oo[hf][2] = ad;
-            }
+            if (staged)
+                merge_word<true, G>(oo, xl, xh, xd, lim, cnt, ent + arel, pos, bint, a, ow0);
+            else
+                merge_word<false, G>(oo, xl, xh, xd, lim, cnt, ent, pos, bint, a, ow0);
             ol = (uint64_t)oo[0][0] | ((uint64_t)oo[1][0] << 32);
             oh = (uint64_t)oo[0][1] | ((uint64_t)oo[1][1] << 32);
             od = (uint64_t)oo[0][2] | ((uint64_t)oo[1][2] << 32);
