@@ -273,10 +273,10 @@ __global__ void keygen_kernel(const uint32_t* __restrict__ text, const uint32_t*
         const uint32_t i0 = 16 * g;
         if (i0 + 16 <= n) {
             uint4* dst = reinterpret_cast<uint4*>(key + i0);
-            dst[0] = make_uint4(k[0], k[1], k[2], k[3]);
-            dst[1] = make_uint4(k[4], k[5], k[6], k[7]);
-            dst[2] = make_uint4(k[8], k[9], k[10], k[11]);
-            dst[3] = make_uint4(k[12], k[13], k[14], k[15]);
+            __stcs(dst + 0, make_uint4(k[0], k[1], k[2], k[3]));
+            __stcs(dst + 1, make_uint4(k[4], k[5], k[6], k[7]));
+            __stcs(dst + 2, make_uint4(k[8], k[9], k[10], k[11]));
+            __stcs(dst + 3, make_uint4(k[12], k[13], k[14], k[15]));
         } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     const uint32_t p = p0 + (u * kDigNt + tid) * 4;
-                    q[u] = p < ch.end ? __ldg(reinterpret_cast<const uint4*>(K + p))
+                    q[u] = p < ch.end ? __ldcs(reinterpret_cast<const uint4*>(K + p))
                                       : make_uint4(0, 0, 0, 0);
                 }
 #pragma unroll
@@ -573,8 +573,8 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
             for (int it = 0; it < kDigIpt; ++it) {
                 const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
                 const bool valid = e < tn;
-                key[it] = valid ? K[t0 + e] : 0u;
-                slot[it] = valid ? (iota ? t0 + e : S[t0 + e]) : 0u;
+                key[it] = valid ? __ldcs(K + t0 + e) : 0u;
+                slot[it] = valid ? (iota ? t0 + e : __ldcs(S + t0 + e)) : 0u;
                 dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
             }
             block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
@@ -593,10 +593,10 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
                 const uint32_t d = (k >> shift) & 0xFFu;
                 const uint32_t gp = run_base[d] + (i - dstart[d]);
                 if (fin[d]) {
-                    B.saf[gp] = s_slot[i];
+                    __stcs(B.saf + gp, s_slot[i]);
                 } else {
-                    S2[gp] = s_slot[i];
-                    K2[gp] = k;
+                    __stcs(S2 + gp, s_slot[i]);
+                    __stcs(K2 + gp, k);
                 }
             }
             __syncthreads();
@@ -645,7 +645,7 @@ __device__ __forceinline__ void warp_tail(const uint2* buf, const Seg& s, const 
     const uint32_t L = s.len;
     const uint32_t nit = (L + 31) >> 5;
     const uint32_t bid = meta_buf(s.meta);
-    for (uint32_t e = lane; e < L; e += 32) B.saf[s.start + e] = buf[e].y;
+    for (uint32_t e = lane; e < L; e += 32) __stcs(B.saf + s.start + e, buf[e].y);
         uint32_t lb = 0, my_pos = 0, my_grp = 0;
         bool mine = false;
         for (uint32_t it = 0; it < nit; ++it) {
