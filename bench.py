@@ -197,6 +197,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     stream = torch.cuda.current_stream(dev)
 
     idx = SetBWTE("ACGT", block_suffixes=M, profile=True)
+    for kv in args.option:
+        k, v = kv.split("=", 1)
+        idx.set_option(k, int(v))
     idx.set_stream(stream)
     if world > 1:
         from paper_1410_0562_b200.dist import make_allgather
@@ -367,6 +370,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-reads", type=int, default=1_000_000)
     ap.add_argument("--ref-sample-reads", type=int, default=100_000)
+    ap.add_argument("--option", action="append", default=[],
+                    help="library option key=value (setbwte_set_option), repeatable")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -150,6 +150,7 @@ struct setbwte_s {
     // options
     uint64_t M = 1ull << 24;
     int rank_ilp = 1;
+    int sort_lanes = 2;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
 
     // data-parallel ComputeRanks
     int rank = 0, world = 1;
@@ -347,7 +348,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         max_suf = std::max(max_suf, b.S1 - b.S0);
         total += b.S1 - b.S0;
     }
-    const int NL = K >= 2 ? 2 : 1;  // sort lanes
+    const int NL = (K >= 2 && h->sort_lanes >= 2) ? 2 : 1;  // sort lanes
     // reserve everything up front: a cudaFree/cudaMalloc mid-loop would
     // serialise the streams
     uint32_t* saf2;
@@ -363,7 +364,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
     API_CHECK(h, ensure(h->sb_tot, ((n_final >> kSbShift) + 1) * 5 + 8, &tmp));
     SortLane lanes[2];
     for (int l = 0; l < NL; ++l) {
-        lanes[l].stream = l == 0 ? h->sort_stream : h->sort_stream2;
+        lanes[l].stream = h->sort_lanes == 0 ? h->stream : l == 0 ? h->sort_stream : h->sort_stream2;
         lanes[l].ws = l == 0 ? &h->sort : &h->sort2;
         lanes[l].saf = saf2 + l * (max_suf + 32);
         lanes[l].ev_sorted = h->ev_sorted[l];
@@ -823,6 +824,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "profile")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->prof.on = value == 1;
+    } else if (!strcmp(key, "sort_lanes")) {
+        if (value > 2) return SETBWTE_E_INVALID_ARG;
+        h->sort_lanes = (int)value;
     } else if (!strcmp(key, "rank_ilp")) {
         if (value < 1 || value > 4) return SETBWTE_E_INVALID_ARG;
         h->rank_ilp = (int)value;
