@@ -51,7 +51,7 @@ constexpr int kDigTile = kDigNt * kDigIpt;
 // BIT2..BIT16: 33..512 members whose unknown key bits fit in 16 (keys valid,
 // shift <= 8): one warp sorts 32*NIT packed (key bits, index) u32 values with a
 // register bitonic network.  SMALL: the other 33..512 segments (warp LSD radix).
-enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MEDIUM, LARGE, NCLASS };
+enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, NCLASS };
 // misc counters
 enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_N };
 
@@ -95,7 +95,10 @@ __host__ __device__ __forceinline__ int class_of(const Seg& c) {
             return c.len <= 64 ? BIT2 : c.len <= 128 ? BIT4 : c.len <= 256 ? BIT8 : BIT16;
         return SMALL;
     }
-    return c.len <= kCapM ? MEDIUM : LARGE;
+    // > 512 with valid keys: one more digit pass is cheaper than a CTA-wide
+    // sort (measured on c3's ~2048-member second-pass buckets)
+    if ((c.meta >> 9) & 1) return LARGE;
+    return c.len <= 1024 ? MED1K : c.len <= 2048 ? MED2K : c.len <= kCapM ? MEDIUM : LARGE;
 }
 __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
     const int k = class_of(c);
@@ -209,29 +212,43 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
         __syncwarp();
     }
     __syncthreads();
-    uint32_t tot = 0;
-    if (tid < 256) {
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t t = wcnt[w * 256 + tid];
-            wcnt[w * 256 + tid] = tot;
-            tot += t;
-        }
-        // exclusive scan of tot over the 256 digits (8 warps)
-        uint32_t incl = tot;
+    // per digit: prefix over the warps, then an exclusive scan over the 256
+    // digits; thread tid owns digits [tid*DPT, tid*DPT+DPT) (NT >= 256: DPT = 1)
+    constexpr int DPT = NT >= 256 ? 1 : 256 / NT;
+    constexpr int NACT = NT >= 256 ? 256 : NT;  // threads owning digits
+    uint32_t tot[DPT];
+    uint32_t local = 0;
+    if (tid < NACT) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
+        for (int q = 0; q < DPT; ++q) {
+            const uint32_t d = tid * DPT + q;
+            uint32_t acc = 0;
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t t = wcnt[w * 256 + d];
+                wcnt[w * 256 + d] = acc;
+                acc += t;
+            }
+            tot[q] = acc;
+            local += acc;
         }
-        if (lane == 31) tmp[warp] = incl;
-        dstart[tid] = incl - tot;  // partial; warp prefix added below
     }
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31 && tid < NACT) tmp[warp] = incl;
     __syncthreads();
-    if (tid < 256) {
-        uint32_t pre = 0;
-        for (uint32_t w = 0; w < warp; ++w) pre += tmp[w];
-        dstart[tid] += pre;
-        if (tid == 255) dstart[256] = dstart[255] + tot;
+    if (tid < NACT) {
+        uint32_t run = incl - local;
+        for (uint32_t w = 0; w < warp; ++w) run += tmp[w];
+#pragma unroll
+        for (int q = 0; q < DPT; ++q) {
+            dstart[tid * DPT + q] = run;
+            run += tot[q];
+        }
+        if (tid == NACT - 1) dstart[256] = run;
     }
     __syncthreads();
 #pragma unroll
@@ -614,22 +631,46 @@ constexpr size_t scatter_smem() {
 // ---------------------------------------------------------------------------
 // TINY: one warp per segment
 // ---------------------------------------------------------------------------
+constexpr uint32_t kTinyPerWarp = 8;  // list entries per warp, packed into shared calls
+
 __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* misc) {
     const uint32_t n = in.cnt[TINY];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
-        const Seg s = in.seg[TINY][i];
-        const uint32_t buf = meta_buf(s.meta);
-        const bool kv = meta_kv(s.meta);
-        uint32_t slot = 0, key = 0;
-        if (lane < s.len) {
-            slot = B.sa[buf][s.start + lane];
-            if (kv) key = B.key[buf][s.start + lane];
+    for (uint32_t i0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kTinyPerWarp; i0 < n;
+         i0 += nw * kTinyPerWarp) {
+        const uint32_t i1 = min(n, i0 + kTinyPerWarp);
+        // pack consecutive segments into the 32 lanes; each lane remembers its
+        // segment's output position, start word and key
+        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0;
+        bool mine = false, kv = false;
+        for (uint32_t i = i0; i <= i1; ++i) {
+            Seg sg;
+            if (i < i1) sg = in.seg[TINY][i];
+            if (i == i1 || lb + sg.len > 32) {
+                if (lb) {
+                    const uint32_t r = warp_finish(slot, lb, word, key, kv, B, grp);
+                    if (mine) B.saf[dst] = r;
+                }
+                lb = 0;
+                mine = false;
+                if (i == i1) break;
+            }
+            if (lane >= lb && lane < lb + sg.len) {
+                const uint32_t e = lane - lb;
+                const uint32_t bf = meta_buf(sg.meta);
+                mine = true;
+                dst = sg.start + e;
+                word = sg.word;
+                kv = meta_kv(sg.meta);
+                slot = B.sa[bf][dst];
+                key = kv ? B.key[bf][dst] : 0u;
+                grp = lb;
+            }
+            lb += sg.len;
+            elems += sg.len;
         }
-        if (lane == 0) atomicAdd(misc + M_ELEMS_T, s.len);
-        slot = warp_finish(slot, s.len, s.word, key, kv, B);
-        if (lane < s.len) B.saf[s.start + lane] = slot;
+        if (lane == 0) atomicAdd(misc + M_ELEMS_T, elems);
     }
 }
 
@@ -905,6 +946,81 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
 // ---------------------------------------------------------------------------
 // MEDIUM: one CTA per segment, LSD radix in shared memory
 // ---------------------------------------------------------------------------
+// Ascending bitonic sort of N = 8*NT values over the CTA (element e = 8*tid + r
+// in register v[r]): strides < 8 in registers, < 256 by warp shuffles, larger
+// ones through shared memory xs[N] -- a handful of block barriers in all.
+template <int NT>
+__device__ __forceinline__ void block_bitonic(uint32_t (&v)[8], uint32_t* xs) {
+    constexpr int N = 8 * NT;
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+        if (k <= 8) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int q = r ^ (k - 1);
+                if (r < q) {
+                    const uint32_t a = v[r], b = v[q];
+                    v[r] = min(a, b);
+                    v[q] = max(a, b);
+                }
+            }
+        } else if (k <= 256) {
+            const int lm = k / 8 - 1;
+            const bool lower = (lane & (uint32_t)(k / 16)) == 0;
+            uint32_t o[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) o[r] = __shfl_xor_sync(0xFFFFFFFFu, v[7 - r], lm);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = lower ? min(v[r], o[r]) : max(v[r], o[r]);
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 8; ++r) xs[8 * tid + r] = v[r];
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t e = 8 * tid + r;
+                const uint32_t o = xs[e ^ (uint32_t)(k - 1)];
+                v[r] = (e & (uint32_t)(k / 2)) == 0 ? min(v[r], o) : max(v[r], o);
+            }
+        }
+#pragma unroll
+        for (int j = k >> 2; j > 0; j >>= 1) {
+            if (j < 8) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    if ((r & j) == 0) {
+                        const uint32_t a = v[r], b = v[r | j];
+                        v[r] = min(a, b);
+                        v[r | j] = max(a, b);
+                    }
+                }
+            } else if (j < 256) {
+                const int lj = j / 8;
+                const bool lower = (lane & (uint32_t)lj) == 0;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v[r], lj);
+                    v[r] = lower ? min(v[r], o) : max(v[r], o);
+                }
+            } else {
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 8; ++r) xs[8 * tid + r] = v[r];
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint32_t e = 8 * tid + r;
+                    const uint32_t o = xs[e ^ (uint32_t)j];
+                    v[r] = (e & (uint32_t)j) == 0 ? min(v[r], o) : max(v[r], o);
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
 template <int CAP, int NT>
 constexpr size_t local_smem() {
     return (size_t)CAP * 16 + (size_t)(NT / 32) * 256 * 4 + 260 * 4 + 32 * 4 + (CAP / 2) * 8 + 64;
@@ -945,9 +1061,35 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
             keyA[i] = kv ? B.key[buf][s.start + i] : suffix_key(B.text, B.term, B.base + sl, s.word);
         }
         __syncthreads();
-        // LSD passes over the digits not yet known to be equal
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
-        for (uint32_t sh = 0; sh <= top; sh += 8) {
+        if (kv && top <= 8) {
+            // <= 16 unknown key bits: one block bitonic sort of packed
+            // (key bits << 12 | index) values (index = slot order, so stable)
+            static_assert(CAP <= 4096 && IPT == 8, "block bitonic packing");
+            const uint32_t rb = top + 8, rmask = (1u << rb) - 1u;
+            const uint32_t hi = keyA[0] & ~rmask;
+            uint32_t v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t e = 8 * tid + r;
+                v[r] = e < len ? (((keyA[e] & rmask) << 12) | e) : 0xFFFFFFFFu;
+            }
+            block_bitonic<NT>(v, keyB);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t e = 8 * tid + r;
+                if (e < len) {
+                    keyB[e] = hi | (v[r] >> 12);
+                    slotB[e] = slotA[v[r] & 0xFFFu];
+                }
+            }
+            __syncthreads();
+            uint32_t* t;
+            t = keyA; keyA = keyB; keyB = t;
+            t = slotA; slotA = slotB; slotB = t;
+        }
+        // LSD passes over the digits not yet known to be equal
+        for (uint32_t sh = 0; sh <= top && !(kv && top <= 8); sh += 8) {
             if (tid == 0) same_digit = 1;
             __syncthreads();
             const uint32_t d0 = (keyA[0] >> sh) & 0xFFu;
@@ -1020,9 +1162,9 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                        uint32_t* d_sa_final, SortStats* st, bool reserve_only) {
     if (n_suf == 0) return cudaSuccess;
     const size_t n = n_suf;
-    const size_t cap[NCLASS] = {n / 2 + 1,         n / 33 + 1, n / 65 + 1, n / 129 + 1,
-                                n / 257 + 1,       n / 33 + 1, n / (kCapS + 1) + 1,
-                                n / (kCapM + 1) + 1};
+    const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
+                                n / 257 + 1, n / 33 + 1,   n / 513 + 1,  n / 1025 + 1,
+                                n / 2049 + 1, n / (kCapS + 1) + 1};  // LARGE: > 512 (kv)
     const size_t max_large = cap[LARGE];
     const size_t max_chunks = n / kMinChunk + max_large + 1;
     uint32_t *sa0, *sa1, *k0, *k1, *hist, *ctr;
@@ -1073,6 +1215,12 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
+    constexpr size_t sm_m1 = local_smem<1024, 128>();
+    constexpr size_t sm_m2 = local_smem<2048, 256>();
+    SB_CHECK(cudaFuncSetAttribute(local_kernel<1024, 128>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m1));
+    SB_CHECK(cudaFuncSetAttribute(local_kernel<2048, 256>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m2));
     constexpr size_t sm_d = scatter_smem();
     SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
@@ -1116,7 +1264,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         }
         if (h_cnt[TINY]) {
             SB_LAUNCH(prof, s, "sort_tiny", 0, 0,
-                      tiny_kernel<<<grid_for((uint64_t)h_cnt[TINY] * 32, 256, 148u * 16u), 256, 0,
+                      tiny_kernel<<<grid_for(((uint64_t)h_cnt[TINY] + kTinyPerWarp - 1) / kTinyPerWarp * 32,
+                                             256, 148u * 16u), 256, 0,
                                     s>>>(in, B, misc));
             SB_CHECK(cudaGetLastError());
         }
@@ -1125,6 +1274,18 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                       warp_sort_kernel<<<grid_for((uint64_t)h_cnt[SMALL] * 32, kWarpCta * 32,
                                                   148u * 8u),
                                          kWarpCta * 32, 0, s>>>(in, out, B, misc));
+            SB_CHECK(cudaGetLastError());
+        }
+        if (h_cnt[MED1K]) {
+            SB_LAUNCH(prof, s, "sort_medium", 0, 0,
+                      (local_kernel<1024, 128><<<std::min<uint32_t>(h_cnt[MED1K], 148u * 12u), 128,
+                                                  sm_m1, s>>>(in, out, MED1K, B, misc)));
+            SB_CHECK(cudaGetLastError());
+        }
+        if (h_cnt[MED2K]) {
+            SB_LAUNCH(prof, s, "sort_medium", 0, 0,
+                      (local_kernel<2048, 256><<<std::min<uint32_t>(h_cnt[MED2K], 148u * 6u), 256,
+                                                  sm_m2, s>>>(in, out, MED2K, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
         if (h_cnt[MEDIUM]) {
