@@ -133,13 +133,13 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint32_t word,
                                                 uint32_t key0, bool have_key, const Bufs& B,
-                                                uint32_t group0 = 0) {
+                                                uint32_t group0 = 0, bool active0 = true) {
     // Several independent runs may be packed into one call: lanes [g, g+len)
     // of each run carry group0 = g (its first lane); runs never mix because
     // the composite sorts by group first.
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = lane < L;
-    bool active = valid;
+    bool active = valid && active0;
     uint32_t group = group0;
     for (;;) {
         uint32_t key = 0;
@@ -631,7 +631,46 @@ constexpr size_t scatter_smem() {
 // ---------------------------------------------------------------------------
 // TINY: one warp per segment
 // ---------------------------------------------------------------------------
-constexpr uint32_t kTinyPerWarp = 8;  // list entries per warp, packed into shared calls
+constexpr uint32_t kTinyPerWarp = 16;  // list entries per warp, packed into shared calls
+
+// Fast path for packed tiny segments whose unknown key bits fit in 16 (keys
+// valid, shift <= 8): one u32 bitonic over the warp on (group, key bits, lane).
+// Returns the lane's slot in sorted order; `tie` marks lanes that still tie on
+// this word with 14 real symbols and `run` the first lane of their tie run.
+__device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint32_t grp,
+                                                uint32_t key, uint32_t rb, bool& tie,
+                                                uint32_t& run) {
+    const uint32_t lane = threadIdx.x & 31;
+    const bool valid = lane < L;
+    const uint32_t rmask = (1u << rb) - 1u;
+    uint32_t v = valid ? (grp << 26) | ((key & rmask) << 5) | lane : 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+        {
+            const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v, k - 1);
+            const bool lower = (lane & (uint32_t)(k >> 1)) == 0;
+            v = lower ? min(v, o) : max(v, o);
+        }
+#pragma unroll
+        for (int j = k >> 2; j > 0; j >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+            const bool lower = (lane & (uint32_t)j) == 0;
+            v = lower ? min(v, o) : max(v, o);
+        }
+    }
+    const uint32_t src = v & 31u;
+    const uint32_t s2 = __shfl_sync(0xFFFFFFFFu, slot, src);
+    const uint32_t k2 = __shfl_sync(0xFFFFFFFFu, key, src);
+    const uint32_t hi = v >> 5;
+    const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
+    const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, hi, 1);
+    const bool eqp = valid && lane > 0 && prv == hi;
+    const bool eqn = valid && lane + 1 < L && nxt == hi;
+    tie = (eqp || eqn) && ((k2 & 15u) == (uint32_t)kKeySyms);
+    const uint32_t starts = __ballot_sync(0xFFFFFFFFu, tie && !eqp);
+    run = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
+    return s2;
+}
 
 __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* misc) {
     const uint32_t n = in.cnt[TINY];
@@ -641,19 +680,30 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
          i0 += nw * kTinyPerWarp) {
         const uint32_t i1 = min(n, i0 + kTinyPerWarp);
         // pack consecutive segments into the 32 lanes; each lane remembers its
-        // segment's output position, start word and key
-        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0;
-        bool mine = false, kv = false;
+        // segment's output position, start word and key (a segment keeps its
+        // lanes through the sort: the composite sorts by group first)
+        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0, rb = 0;
+        bool mine = false, kv = false, fast = true;
         for (uint32_t i = i0; i <= i1; ++i) {
             Seg sg;
             if (i < i1) sg = in.seg[TINY][i];
             if (i == i1 || lb + sg.len > 32) {
                 if (lb) {
-                    const uint32_t r = warp_finish(slot, lb, word, key, kv, B, grp);
+                    uint32_t r;
+                    if (__all_sync(0xFFFFFFFFu, fast || lane >= lb)) {
+                        bool tie;
+                        uint32_t run;
+                        r = warp_sort16(slot, lb, grp, key, rb, tie, run);
+                        if (__any_sync(0xFFFFFFFFu, tie))
+                            r = warp_finish(r, lb, word + 1, 0u, false, B, run, tie);
+                    } else {
+                        r = warp_finish(slot, lb, word, key, kv, B, grp);
+                    }
                     if (mine) B.saf[dst] = r;
                 }
                 lb = 0;
                 mine = false;
+                fast = true;
                 if (i == i1) break;
             }
             if (lane >= lb && lane < lb + sg.len) {
@@ -666,6 +716,8 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
                 slot = B.sa[bf][dst];
                 key = kv ? B.key[bf][dst] : 0u;
                 grp = lb;
+                rb = meta_shift(sg.meta) + 8;
+                fast = kv && meta_shift(sg.meta) <= 8;
             }
             lb += sg.len;
             elems += sg.len;
