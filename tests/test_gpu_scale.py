@@ -1,0 +1,84 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times: the whole BWT against the oracle where the oracle finishes in seconds
+(c2), otherwise sampled outputs the oracle computes one by one (the SA
+position of a suffix, gives B at that position by Eq.(1)) plus
+properties that hold at any size (B[0..m) = last symbols, m terminators,
+LF inversion recovers reads)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+A = "ACGT"
+
+
+def _sampled_checks(idx, data, offsets, n_samples, seed):
+    from paper_1410_0562_b200 import SetBWTE  # noqa: F401
+    m = len(offsets) - 1
+    n, mm = idx.size()
+    assert mm == m and n == int(offsets[-1]) + m
+    B = np.frombuffer(idx.bwt(), dtype=np.uint8)
+    # B[0..m) = the last symbol of each string (rows 0..m-1 are $_0..$_{m-1})
+    last = data[(offsets[1:] - 1).astype(np.int64)]
+    assert np.array_equal(B[:m], last)
+    # exactly m terminators; symbol multiset = input multiset
+    assert int((B == ord("$")).sum()) == m
+    for c in A:
+        assert int((B == ord(c)).sum()) == int((data == ord(c)).sum())
+    rng = np.random.default_rng(seed)
+    # sampled SA positions by the oracle's counting definition
+    for _ in range(n_samples):
+        j = int(rng.integers(0, m))
+        L = int(offsets[j + 1] - offsets[j])
+        k = int(rng.integers(0, L + 1))
+        r = oracle.suffix_rank(A, data, offsets, j, k, threads=None)
+        want = ord("$") if k == 0 else int(data[int(offsets[j]) + k - 1])
+        assert int(B[r]) == want, (j, k, r)
+    # LF inversion (FM-index backward steps through setbwte_rank) recovers reads
+    C = {}
+    acc = m
+    for c in A:
+        C[c] = acc
+        acc += int((B == ord(c)).sum())
+    for j in rng.integers(0, m, size=3):
+        i = int(j)
+        out = []
+        while B[i] != ord("$"):
+            c = chr(B[i])
+            out.append(c)
+            i = C[c] + idx.rank(c, i)
+        s = "".join(reversed(out))
+        assert s == bytes(data[int(offsets[j]):int(offsets[j + 1])]).decode()
+
+
+def test_c3_full_sampled():
+    """configs[2]: 20M x 100 bp, M = 2^27 (16 blocks)."""
+    from paper_1410_0562_b200 import SetBWTE
+    d, o = synth.uniform(20_000_000, 100, seed=1)
+    idx = SetBWTE(A, block_suffixes=1 << 27)
+    idx.append(d, o)
+    assert idx.stats()["blocks"] == 16
+    _sampled_checks(idx, d, o, n_samples=4, seed=3)
+
+
+def test_c4_scaled_sampled():
+    """configs[3]-shaped: long reads of U[1000, 10000] bp (100k reads, 550 Mbp),
+    M = 2^28; arbitrary-length suffix keys."""
+    from paper_1410_0562_b200 import SetBWTE
+    d, o = synth.uniform_var(100_000, 1000, 10000, seed=1)
+    idx = SetBWTE(A, block_suffixes=1 << 28)
+    idx.append(d, o)
+    _sampled_checks(idx, d, o, n_samples=4, seed=4)
+
+
+def test_genome_sampled_deep_lcp():
+    """Reads sampled from a 4 Mbp genome at ~25x coverage: deep LCPs, many
+    key words per suffix; whole BWT vs the oracle."""
+    from paper_1410_0562_b200 import SetBWTE
+    d, o = synth.genome_sampled(1_000_000, 100, 4_000_000, seed=2)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 24)
+    idx.append(d, o)
+    assert idx.bwt() == want
