@@ -151,6 +151,17 @@ struct setbwte_s {
     uint64_t M = 1ull << 24;
     int rank_ilp = 1;
     int sort_lanes = 2;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
+    uint64_t hbm_budget = ~0ull;  // max bytes of B_ext dictionary kept in HBM
+
+    // host tier: B_ext's dictionary in pinned, mapped
+    // host memory (zero-copy for ComputeRanks / queries), rewritten in place
+    // by Insert through HBM staging, top superblock range first
+    bool host_tier = false;
+    Blk* hdict = nullptr;       // host pointer
+    Blk* hdict_dev = nullptr;   // device alias
+    uint64_t hdict_cap = 0;     // capacity in Blks
+    DevBuf stage_in, stage_out;
+    std::vector<uint64_t> h_sb_start;
 
     // data-parallel ComputeRanks
     int rank = 0, world = 1;
@@ -233,7 +244,9 @@ setbwte_status pack_input(setbwte_t h, const uint8_t* d_bytes, const uint64_t* d
 }
 
 // Dictionary accessors for the current B_ext.
-inline const Blk* cur_blk(setbwte_t h) { return (const Blk*)h->blk[h->cur].p; }
+inline const Blk* cur_blk(setbwte_t h) {
+    return h->host_tier ? h->hdict_dev : (const Blk*)h->blk[h->cur].p;
+}
 inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cur].p; }
 
 // ComputeRanks for strings [j0, j1) of a packed append, into g (block-local
@@ -289,6 +302,75 @@ struct BlockDesc {
     uint64_t j0, j1, S0, S1;
 };
 
+// Pinned mapped host buffer for the dictionary with >= nblk Blks, keeping
+// the first keep_blks of the current content.  Capacity grows 1.5x, so the
+// host memory stays <= 1.5 x 4 bits/symbol = 6 bits = 3 n log(sigma) for
+// sigma = 4.
+setbwte_status host_reserve(setbwte_t h, uint64_t nblk, const Blk* src, bool src_dev,
+                            uint64_t keep_blks) {
+    const uint64_t cap = std::max<uint64_t>(nblk + nblk / 2, 1024);
+    void* p = nullptr;
+    API_CHECK(h, cudaHostAlloc(&p, cap * sizeof(Blk), cudaHostAllocMapped | cudaHostAllocPortable));
+    void* pd = nullptr;
+    API_CHECK(h, cudaHostGetDevicePointer(&pd, p, 0));
+    if (keep_blks)
+        API_CHECK(h, cudaMemcpyAsync(p, src, keep_blks * sizeof(Blk),
+                                     src_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost,
+                                     h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    if (h->hdict) API_CHECK(h, cudaFreeHost(h->hdict));
+    h->hdict = (Blk*)p;
+    h->hdict_dev = (Blk*)pd;
+    h->hdict_cap = cap;
+    return SETBWTE_OK;
+}
+
+// Insert with B_ext in host memory: output superblocks in chunks from the top
+// down; each chunk's external input range is staged into HBM, merged, and
+// written back in place.  A chunk writes [O0, O1) and reads external symbols
+// below O1 only, which no later (lower) chunk has written yet, and every
+// higher chunk's inputs lie at or above O1's chunk boundary -- so one stream
+// in top-down order is safe without extra copies.
+setbwte_status host_insert(setbwte_t h, const void* pos, int gw, const uint8_t* bint,
+                           uint64_t n_suf, uint64_t* osb, uint64_t* tot, uint64_t* sb_start,
+                           uint64_t m_new) {
+    const uint64_t n_in = h->n, n_out = n_in + n_suf;
+    const uint64_t nblk = (n_out >> 6) + 1, nsb = (n_out >> kSbShift) + 1;
+    if (!h->hdict || h->hdict_cap < nblk) {
+        setbwte_status st = host_reserve(h, nblk, h->hdict, false, h->hdict ? (n_in >> 6) + 1 : 0);
+        if (st != SETBWTE_OK) return st;
+    }
+    h->h_sb_start.resize(nsb + 1);
+    API_CHECK(h, cudaMemcpyAsync(h->h_sb_start.data(), sb_start, (nsb + 1) * sizeof(uint64_t),
+                                 cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    constexpr uint64_t CS = 1024;  // superblocks per chunk (2^26 symbols, 32 MB of Blks)
+    Blk *sin, *sout;
+    API_CHECK(h, ensure(h->stage_in, CS * kBlkPerSb + 8, &sin));
+    API_CHECK(h, ensure(h->stage_out, CS * kBlkPerSb + 8, &sout));
+    const uint64_t nin_blk = n_in ? (n_in >> 6) + 1 : 0;
+    for (int64_t c = (int64_t)((nsb - 1) / CS); c >= 0; --c) {
+        const uint64_t sa = (uint64_t)c * CS, sbe = std::min(nsb, sa + CS);
+        const uint64_t O0 = sa << kSbShift, Oe = std::min(sbe << kSbShift, n_out);
+        const uint64_t E0 = O0 - h->h_sb_start[sa];
+        const uint64_t E1 = std::min(n_in, Oe - h->h_sb_start[sbe]);
+        uint64_t bE0 = 0, bE1 = 0;
+        if (E1 > E0) {
+            bE0 = E0 >> 6;
+            bE1 = std::min(((E1 - 1) >> 6) + 2, nin_blk);
+            API_CHECK(h, cudaMemcpyAsync(sin, h->hdict + bE0, (bE1 - bE0) * sizeof(Blk),
+                                         cudaMemcpyHostToDevice, h->stream));
+        }
+        API_CHECK(h, launch_insert_range(h->prof, h->stream, sin - bE0, n_in, pos, gw, bint, n_suf,
+                                         sout - (sa << (kSbShift - 6)), tot, sb_start, sa, sbe));
+        const uint64_t b0 = sa << (kSbShift - 6), b1 = std::min(sbe << (kSbShift - 6), nblk);
+        API_CHECK(h, cudaMemcpyAsync(h->hdict + b0, sout, (b1 - b0) * sizeof(Blk),
+                                     cudaMemcpyDeviceToHost, h->stream));
+    }
+    API_CHECK(h, launch_sb_scan(h->prof, h->stream, tot, nsb, osb, m_new, (uint64_t*)h->d_C.p));
+    return SETBWTE_OK;
+}
+
 // ComputeRanks, B_int + g_sa gather, Insert; on the main stream.
 setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc& b,
                                  const uint32_t* saf) {
@@ -306,9 +388,18 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     const uint64_t nblk = (n_out >> 6) + 1;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
     const int nxt = 1 - h->cur;
-    Blk* ob;
+    Blk* ob = nullptr;
     uint64_t *osb, *tot;
-    API_CHECK(h, ensure(h->blk[nxt], nblk, &ob));
+    if (!h->host_tier && nblk * sizeof(Blk) > h->hbm_budget) {
+        // the dictionary outgrows its HBM budget: move B_ext to the host tier
+        // (after this block's ComputeRanks, which still reads the HBM copy)
+        setbwte_status st2 = host_reserve(h, nblk, cur_blk(h), true, h->n ? (h->n >> 6) + 1 : 0);
+        if (st2 != SETBWTE_OK) return st2;
+        h->host_tier = true;
+        free_buf(h->blk[0]);
+        free_buf(h->blk[1]);
+    }
+    if (!h->host_tier) API_CHECK(h, ensure(h->blk[nxt], nblk, &ob));
     API_CHECK(h, ensure(h->sb[nxt], nsb * 4, &osb));
     API_CHECK(h, ensure(h->sb_tot, nsb * 5 + 8, &tot));  // totals + sb_start
     uint64_t* sb_start = tot + 4 * (nsb + 1);
@@ -317,8 +408,13 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
                                (uint32_t)n_suf, pos, gw, bint, sb_start, nsb));
     const uint64_t m_new = h->m + (b.j1 - b.j0);
-    API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_suf, ob, osb,
-                               tot, sb_start, m_new, (uint64_t*)h->d_C.p));
+    if (h->host_tier) {
+        st = host_insert(h, pos, gw, bint, n_suf, osb, tot, sb_start, m_new);
+        if (st != SETBWTE_OK) return st;
+    } else {
+        API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_suf, ob,
+                                   osb, tot, sb_start, m_new, (uint64_t*)h->d_C.p));
+    }
     h->cur = nxt;
     h->n = n_out;
     h->m = m_new;
@@ -469,11 +565,13 @@ void build_stats(setbwte_t h) {
     char buf[512];
     snprintf(buf, sizeof(buf),
              "\"n\": %llu, \"m\": %llu, \"blocks\": %llu, \"bases\": %llu, \"strings\": %llu, "
-             "\"launches\": %llu, \"profile\": %d, \"block_suffixes\": %llu, ",
+             "\"launches\": %llu, \"profile\": %d, \"block_suffixes\": %llu, "
+             "\"host_tier\": %d, \"host_dict_bytes\": %llu, ",
              (unsigned long long)h->n, (unsigned long long)h->m,
              (unsigned long long)h->last_blocks, (unsigned long long)h->last_bases,
              (unsigned long long)h->last_m, (unsigned long long)h->prof.total_launches,
-             h->prof.on ? 1 : 0, (unsigned long long)h->M);
+             h->prof.on ? 1 : 0, (unsigned long long)h->M, h->host_tier ? 1 : 0,
+             (unsigned long long)(h->hdict_cap * sizeof(Blk)));
     s += buf;
     s += "\"sort\": {\"digit_passes\": " + std::to_string(h->sstats.digit_passes) +
          ", \"active_per_pass\": [";
@@ -625,6 +723,9 @@ void setbwte_destroy(setbwte_t h) {
                       &h->sort2.small_a, &h->sort2.small_b, &h->sort2.chunks, &h->sort2.hist,
                       &h->sort2.ctr, &h->sort2.gtot, &h->sort2.groups};
     for (DevBuf* b : bufs) free_buf(*b);
+    free_buf(h->stage_in);
+    free_buf(h->stage_out);
+    if (h->hdict) cudaFreeHost(h->hdict);
     if (h->sort_stream) cudaStreamSynchronize(h->sort_stream);
     if (h->sort_stream2) cudaStreamSynchronize(h->sort_stream2);
     for (cudaEvent_t ev : {h->ev_start, h->ev_sorted[0], h->ev_sorted[1], h->ev_used[0],
@@ -824,6 +925,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "profile")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->prof.on = value == 1;
+    } else if (!strcmp(key, "hbm_budget_bytes")) {
+        if (value < 1) return SETBWTE_E_INVALID_ARG;
+        h->hbm_budget = value;
     } else if (!strcmp(key, "sort_lanes")) {
         if (value > 2) return SETBWTE_E_INVALID_ARG;
         h->sort_lanes = (int)value;

@@ -110,13 +110,15 @@ template <class G>
 __global__ void __launch_bounds__(kInsNt) insert_kernel(
     const Blk* __restrict__ in_blk, uint64_t n_in, const G* __restrict__ pos,
     const uint8_t* __restrict__ bint, uint64_t n_ins, Blk* __restrict__ out_blk, uint64_t n_out,
-    uint64_t* __restrict__ sb_tot, const uint64_t* __restrict__ sb_start) {
+    uint64_t* __restrict__ sb_tot, const uint64_t* __restrict__ sb_start, uint64_t sb_begin,
+    uint64_t sb_end) {
+    // in_blk / out_blk are indexed by absolute Blk number; the host-tier path
+    // passes pointers biased by its staging window (only the window is touched)
     __shared__ uint32_t wcnt[kBlkPerSb];
     __shared__ uint16_t ent[kStage];  // (offset in word) | (B_int code+$ << 6)
     __shared__ uint32_t wsum[4][kInsWarps];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t nsb = (n_out >> kSbShift) + 1;
-    for (uint64_t sbi = blockIdx.x; sbi < nsb; sbi += gridDim.x) {
+    for (uint64_t sbi = sb_begin + blockIdx.x; sbi < sb_end; sbi += gridDim.x) {
         const uint64_t o0 = sbi << kSbShift;
         wcnt[tid] = 0;
         __syncthreads();
@@ -245,30 +247,50 @@ __global__ void __launch_bounds__(1024) sb_scan_kernel(const uint64_t* __restric
     }
 }
 
+cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+                                const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
+                                Blk* out_blk, uint64_t* sb_tot, const uint64_t* sb_start,
+                                uint64_t sb_begin, uint64_t sb_end) {
+    const uint64_t n_out = n_in + n_ins;
+    const uint64_t nsb_r = sb_end - sb_begin;
+    if (nsb_r == 0) return cudaSuccess;
+    // algorithmic bytes of the range: its share of B_ext read + B_ext' written
+    // (4 bits/symbol each) + (gw + 1) B per inserted symbol of the range
+    const double frac = (double)nsb_r / (double)((n_out >> kSbShift) + 1);
+    const double bytes = frac * (0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins);
+    const unsigned grid = (unsigned)(nsb_r < 148u * 64u ? nsb_r : 148u * 64u);
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
+                  insert_kernel<uint32_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint32_t*)pos,
+                                                                   bint, n_ins, out_blk, n_out,
+                                                                   sb_tot, sb_start, sb_begin,
+                                                                   sb_end));
+    } else {
+        SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
+                  insert_kernel<uint64_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint64_t*)pos,
+                                                                   bint, n_ins, out_blk, n_out,
+                                                                   sb_tot, sb_start, sb_begin,
+                                                                   sb_end));
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_tot, uint64_t nsb,
+                           uint64_t* out_sb, uint64_t m_new, uint64_t* d_C) {
+    SB_LAUNCH(prof, s, "sb_scan", 64.0 * nsb, nsb,
+              sb_scan_kernel<<<1, 1024, 0, s>>>(sb_tot, nsb, out_sb, m_new, d_C));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
                           const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C) {
     const uint64_t n_out = n_in + n_ins;
     const uint64_t nsb = (n_out >> kSbShift) + 1;
-    // algorithmic bytes: read n_in/2 + write n_out/2 (4 bits/symbol) + (gw + 1) B per inserted
-    const double bytes = 0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins;
-    const unsigned grid = (unsigned)(nsb < 148u * 64u ? nsb : 148u * 64u);
-    if (gw == 4) {
-        SB_LAUNCH(prof, s, "insert", bytes, n_out,
-                  insert_kernel<uint32_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint32_t*)pos,
-                                                                   bint, n_ins, out_blk, n_out,
-                                                                   sb_tot, sb_start));
-    } else {
-        SB_LAUNCH(prof, s, "insert", bytes, n_out,
-                  insert_kernel<uint64_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint64_t*)pos,
-                                                                   bint, n_ins, out_blk, n_out,
-                                                                   sb_tot, sb_start));
-    }
-    SB_CHECK(cudaGetLastError());
-    SB_LAUNCH(prof, s, "sb_scan", 64.0 * nsb, nsb,
-              sb_scan_kernel<<<1, 1024, 0, s>>>(sb_tot, nsb, out_sb, m_new, d_C));
-    return cudaGetLastError();
+    SB_CHECK(launch_insert_range(prof, s, in_blk, n_in, pos, gw, bint, n_ins, out_blk, sb_tot,
+                                 sb_start, 0, nsb));
+    return launch_sb_scan(prof, s, sb_tot, nsb, out_sb, m_new, d_C);
 }
 
 __global__ void rank_batch_kernel(const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,

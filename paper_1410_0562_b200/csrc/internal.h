@@ -141,6 +141,14 @@ cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uin
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
                           const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C);
+// Insert restricted to output superblocks [sb_begin, sb_end) (host tier)
+// and the closing superblock scan.
+cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+                                const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
+                                Blk* out_blk, uint64_t* sb_tot, const uint64_t* sb_start,
+                                uint64_t sb_begin, uint64_t sb_end);
+cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_tot, uint64_t nsb,
+                           uint64_t* out_sb, uint64_t m_new, uint64_t* d_C);
 cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
                               uint64_t n, const uint8_t* code_of, const uint8_t* c,
                               const uint64_t* k, uint64_t q, uint64_t* out);

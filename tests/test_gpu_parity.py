@@ -279,3 +279,49 @@ def test_c2_full_vs_oracle(SetBWTE):
     idx = build(SetBWTE, d, o, M=1 << 24)
     assert idx.stats()["blocks"] == 7
     assert idx.bwt() == want
+
+
+# --- host-tiered B_ext (A6 variant, c5 path) -----------------------------------
+
+@pytest.mark.parametrize("budget", [1, 20000, 1 << 40])
+def test_host_tier_c1(SetBWTE, c1, budget):
+    """B_ext in pinned host memory (hbm_budget_bytes=1: from the first block;
+    20000: moves to the host mid-append), bit-exact vs the oracle."""
+    d, o, want = c1
+    idx = SetBWTE(A, block_suffixes=25250)
+    idx.set_option("hbm_budget_bytes", budget)
+    idx.append(d, o)
+    assert idx.stats()["host_tier"] == (1 if budget < (1 << 40) else 0)
+    assert idx.bwt() == want
+    n = len(want)
+    for c in "$ACGT":
+        for k in (0, 1, 64, 65537, n):
+            assert idx.rank(c, k) == oracle.rank(want, c, k)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_host_tier_random_appends(SetBWTE, seed):
+    d, o = synth.random_set(900 + seed, max_m=64, max_len=50)
+    want = oracle.bwt(A, d, o)
+    idx = SetBWTE(A, block_suffixes=int(np.random.default_rng(seed).integers(20, 400)))
+    idx.set_option("hbm_budget_bytes", 1)
+    m = len(o) - 1
+    cuts = sorted(set(np.random.default_rng(seed).integers(0, m + 1, size=3).tolist()))
+    prev = 0
+    for c in cuts + [m]:
+        if c > prev:
+            oo = np.asarray(o[prev:c + 1], dtype=np.uint64)
+            idx.append(d[int(oo[0]):int(oo[-1])], oo - oo[0])
+            prev = c
+    assert idx.bwt() == want
+
+
+def test_host_tier_multichunk(SetBWTE):
+    """More than one 2^26-symbol staging chunk: 1M x 100 bp (101 M symbols)."""
+    d, o = synth.uniform(700_000, 100, seed=21)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 24)
+    idx.set_option("hbm_budget_bytes", 1 << 20)
+    idx.append(d, o)
+    assert idx.stats()["host_tier"] == 1
+    assert idx.bwt() == want
