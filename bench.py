@@ -41,6 +41,9 @@ WORKLOADS = {
            dict(m=20_000_000, L=100), 1 << 27),
     "c4": ("c4: 1M uniform reads of length U[1000,10000] (~5.5 Gbp), M=2^30-suffix blocks",
            dict(m=1_000_000, lo=1000, hi=10000), 1 << 30),
+    "c5": ("c5: append 10M uniform reads x 100 bp (seed 2) into an existing 50M-read index "
+           "(seed 1) whose B_ext is host-tiered (pinned host memory), M=2^27-suffix blocks",
+           dict(m=10_000_000, L=100, base_m=50_000_000), 1 << 27),
 }
 
 # which library kernels make up which stage of Table 2's taxonomy
@@ -57,6 +60,8 @@ STAGE_OF = {
 def gen(workload: str, seed: int = 1):
     import synth
     _, kw, _ = WORKLOADS[workload]
+    if "base_m" in kw:  # c5: the appended reads (the base index is built untimed)
+        return synth.uniform(kw["m"], kw["L"], seed=2)
     if "L" in kw:
         return synth.uniform(kw["m"], kw["L"], seed=seed)
     return synth.uniform_var(kw["m"], kw["lo"], kw["hi"], seed=seed)
@@ -93,9 +98,18 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    paused = False
+
+    def pause(self):
+        self.paused = True
+
+    def resume(self):
+        self.paused = False
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            if not self.paused:
+                self.lines.append(line.strip())
 
     def stop(self):
         if self.proc is None:
@@ -196,22 +210,45 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
     stream = torch.cuda.current_stream(dev)
 
-    idx = SetBWTE("ACGT", block_suffixes=M, profile=True)
-    for kv in args.option:
-        k, v = kv.split("=", 1)
-        idx.set_option(k, int(v))
-    idx.set_stream(stream)
-    if world > 1:
-        from paper_1410_0562_b200.dist import make_allgather
-        idx.set_partition(rank, world, make_allgather())
+    def new_index():
+        ix = SetBWTE("ACGT", block_suffixes=M, profile=True)
+        for kv in args.option:
+            k, v = kv.split("=", 1)
+            ix.set_option(k, int(v))
+        ix.set_stream(stream)
+        if world > 1:
+            from paper_1410_0562_b200.dist import make_allgather
+            ix.set_partition(rank, world, make_allgather())
+        return ix
+
+    base = None
+    if "base_m" in WORKLOADS[wl][1]:
+        import synth
+        bd, bo = synth.uniform(WORKLOADS[wl][1]["base_m"], WORKLOADS[wl][1]["L"], seed=1)
+        base = (torch.from_numpy(bd).to(dev), torch.from_numpy(bo.view(np.int64)).to(dev),
+                len(bo) - 1, bd, bo)
+
+    idx = new_index()
+
+    def prepare():
+        """Untimed: the index the step appends to (empty, or c5's host-tiered base)."""
+        nonlocal idx
+        if base is None:
+            idx.clear()
+        else:
+            idx.close()
+            idx = new_index()
+            idx.append_device(base[0], base[1], base[2])
+            idx.set_option("host_tier", 1)
+        torch.cuda.synchronize(dev)
 
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
-        idx.clear()
         idx.append_device(d_data, d_off, m)
 
     for _ in range(args.warmup):
+        prepare()
         l2_flush.zero_()
         step()
     torch.cuda.synchronize(dev)
@@ -226,6 +263,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     sampler.start()
     times = []
     for _ in range(args.steps):
+        if base is not None:
+            sampler.pause()
+        prepare()                            # untimed
+        if base is not None:
+            sampler.resume()
         l2_flush.zero_()                     # flush L2 between timed iterations (untimed)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -257,12 +299,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- end to end through the public API: pinned host in, BWT back out ----
     pin_data = torch.from_numpy(data).pin_memory()
     pin_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
-    n_total = bases + m
+    n_total = bases + m + (int(base[4][-1]) + base[2] if base is not None else 0)
     pin_out = torch.empty(n_total, dtype=torch.uint8).pin_memory()
     np_data = pin_data.numpy()
     np_off = pin_off.numpy().view(np.uint64)
     e2e_times = []
     for i in range(args.warmup + args.steps):
+        prepare()
         l2_flush.zero_()
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -270,7 +313,6 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        idx.clear()
         idx.append(np_data, np_off)          # H2D of the step's inputs inside
         idx.bwt(pin_out)                      # D2H of the step's result
         e1.record(stream)
@@ -321,7 +363,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # ---- oracle beside it (rank 0, N = 1 only), + parity of this run ----
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and base is None:
         import oracle
         cores = cpu_count()
         m_s = min(args.cpu_sample_reads, m)
@@ -342,6 +384,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "ms_per_step": round(1000.0 * t / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": desc, "reads": m, "bases": bases, "block_suffixes": M,
+                       "host_tier": bool(idx.stats().get("host_tier")),
                        "blocks": blocks, "parallelism": "dp%d (ComputeRanks split by string)" % world,
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
             "compute_ranks_queries_per_s": qps, "stage_ms_per_step": stages,

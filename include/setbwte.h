@@ -148,7 +148,17 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     Default 2^24.
  *   "profile"         1: time every kernel launch with CUDA events on the
  *                     handle's stream (reported by setbwte_stats); 0: off.
- *   "rank_ilp"        strings per thread in the ComputeRanks kernel (1..4). */
+ *   "rank_ilp"        strings per thread in the ComputeRanks kernel (1..4).
+ *   "sort_lanes"      host threads (each with its own CUDA stream) running
+ *                     ConstructSA of upcoming blocks ahead of the in-order
+ *                     rank/insert stage (the stage pipeline of P:190-191):
+ *                     2 (default), 1, or 0 = every stage on the main stream.
+ *   "hbm_budget_bytes" largest B_ext dictionary kept in HBM; beyond it B_ext
+ *                     moves to pinned, mapped host memory ("host tier", P:12,
+ *                     <= 3 n log(sigma) bits of system
+ *                     memory) and Insert rewrites it in place through HBM
+ *                     staging.  Default: unlimited.
+ *   "host_tier"       1: move B_ext to the host tier now (and keep it there). */
 setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value);
 
 /* Use cuda_stream (a cudaStream_t on the handle's device) for all further

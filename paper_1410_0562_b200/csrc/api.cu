@@ -925,6 +925,20 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "profile")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->prof.on = value == 1;
+    } else if (!strcmp(key, "host_tier")) {
+        // 1: move B_ext's dictionary to pinned host memory now (and keep it there)
+        if (value != 1) return SETBWTE_E_INVALID_ARG;
+        h->hbm_budget = 0;
+        if (!h->host_tier) {
+            cudaError_t e = cudaSetDevice(h->device);
+            if (e != cudaSuccess) return from_cuda(h, e);
+            const uint64_t nblk = (h->n >> 6) + 1;
+            setbwte_status st = host_reserve(h, nblk, cur_blk(h), true, h->n ? nblk : 0);
+            if (st != SETBWTE_OK) return st;
+            h->host_tier = true;
+            free_buf(h->blk[0]);
+            free_buf(h->blk[1]);
+        }
     } else if (!strcmp(key, "hbm_budget_bytes")) {
         if (value < 1) return SETBWTE_E_INVALID_ARG;
         h->hbm_budget = value;
