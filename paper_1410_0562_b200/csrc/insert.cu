@@ -326,24 +326,41 @@ cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, co
     return cudaGetLastError();
 }
 
+// BWT decode: one thread per 64-symbol Blk, 4 x 16-byte stores of ASCII.
 __global__ void decode_kernel(const Blk* __restrict__ blk, uint64_t n,
                               const uint8_t* __restrict__ sym_ascii, uint8_t* __restrict__ out) {
-    const uint8_t a0 = sym_ascii[0], a1 = sym_ascii[1], a2 = sym_ascii[2], a3 = sym_ascii[3];
+    // code -> byte lookup via byte_perm: selector nibble c picks sym[c]
+    const uint32_t tab = (uint32_t)sym_ascii[0] | ((uint32_t)sym_ascii[1] << 8) |
+                         ((uint32_t)sym_ascii[2] << 16) | ((uint32_t)sym_ascii[3] << 24);
     const uint64_t nb = (n + 63) >> 6;
     for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
          b += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t lo = blk[b].lo, hi = blk[b].hi, dl = blk[b].dol;
-        const uint64_t base = b << 6;
-        const uint32_t cnt = (uint32_t)min((uint64_t)64, n - base);
-        for (uint32_t t = 0; t < cnt; ++t) {
-            uint8_t ch;
-            if ((dl >> t) & 1ull) {
-                ch = '$';
-            } else {
-                const uint32_t c = (uint32_t)(((lo >> t) & 1ull) | (((hi >> t) & 1ull) << 1));
-                ch = c == 0 ? a0 : c == 1 ? a1 : c == 2 ? a2 : a3;
+        uint64_t w[4];
+        asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+            : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(blk + b));
+        const uint64_t lo = w[1], hi = w[2], dl = w[3];
+        uint32_t o[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int p = 4 * q + t;
+                const uint32_t c = (uint32_t)(((lo >> p) & 1ull) | (((hi >> p) & 1ull) << 1));
+                uint32_t ch = __byte_perm(tab, 0, c);  // sym_ascii[c] in byte 0
+                if ((dl >> p) & 1ull) ch = '$';
+                v |= (ch & 0xFFu) << (8 * t);
             }
-            out[base + t] = ch;
+            o[q] = v;
+        }
+        const uint64_t base = b << 6;
+        if (base + 64 <= n && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+            uint4* dst = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+            const uint32_t cnt = (uint32_t)min((uint64_t)64, n - base);
+            for (uint32_t t = 0; t < cnt; ++t) out[base + t] = (uint8_t)(o[t >> 2] >> (8 * (t & 3)));
         }
     }
 }

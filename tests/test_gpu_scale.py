@@ -53,6 +53,7 @@ def _sampled_checks(idx, data, offsets, n_samples, seed):
         assert s == bytes(data[int(offsets[j]):int(offsets[j + 1])]).decode()
 
 
+@pytest.mark.slow
 def test_c3_full_sampled():
     """configs[2]: 20M x 100 bp, M = 2^27 (16 blocks)."""
     from paper_1410_0562_b200 import SetBWTE
@@ -63,6 +64,7 @@ def test_c3_full_sampled():
     _sampled_checks(idx, d, o, n_samples=4, seed=3)
 
 
+@pytest.mark.slow
 def test_c4_scaled_sampled():
     """configs[3]-shaped: long reads of U[1000, 10000] bp (100k reads, 550 Mbp),
     M = 2^28; arbitrary-length suffix keys."""
