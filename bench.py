@@ -211,7 +211,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     stream = torch.cuda.current_stream(dev)
 
     def new_index():
-        ix = SetBWTE("ACGT", block_suffixes=M, profile=True)
+        ix = SetBWTE("ACGT", block_suffixes=M)
         for kv in args.option:
             k, v = kv.split("=", 1)
             ix.set_option(k, int(v))
@@ -247,11 +247,25 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     def step():
         idx.append_device(d_data, d_off, m)
 
+    # warm-up: every launch timed once to find the dominant kernel; the timed
+    # steps then put CUDA events around that kernel's launches only (events
+    # around every launch perturb the two-stream pipeline by ~20 %)
+    warm_kern = {}
     for _ in range(args.warmup):
         prepare()
+        idx.set_profile(1)
         l2_flush.zero_()
         step()
+        for k, v in idx.stats()["kernels"].items():
+            a = warm_kern.setdefault(k, {"launches": 0, "ms": 0.0, "bytes": 0.0, "units": 0})
+            for f in a:
+                a[f] += v[f]
     torch.cuda.synchronize(dev)
+    dom_name = max(warm_kern.items(), key=lambda kv: kv[1]["ms"])[0] if warm_kern else None
+
+    def set_timed_profile():
+        if dom_name:
+            idx.set_profile(2, dom_name)
 
     kern = {}
     launches = 0
@@ -266,6 +280,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if base is not None:
             sampler.pause()
         prepare()                            # untimed
+        set_timed_profile()
         if base is not None:
             sampler.resume()
         l2_flush.zero_()                     # flush L2 between timed iterations (untimed)
@@ -306,6 +321,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e_times = []
     for i in range(args.warmup + args.steps):
         prepare()
+        idx.set_profile(0)
         l2_flush.zero_()
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -330,8 +346,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ---- roofline of the dominant kernel ----
     peak, peak_src = load_peaks()
-    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
-    dname, dk = dom
+    dname = dom_name
+    dk = kern[dname]
     per_launch_bytes = dk["bytes"] / max(dk["launches"], 1)
     avg_ms = dk["ms"] / max(dk["launches"], 1)
     achieved = per_launch_bytes / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else None
@@ -353,11 +369,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "bytes_per_launch": per_launch_bytes, "avg_launch_ms": round(avg_ms, 5),
             "share_of_step": round(dk["ms"] / (t_local * 1000.0), 4), "peak_source": peak_src}
     stages = {}
-    for k, v in kern.items():
+    for k, v in warm_kern.items():
         sname = STAGE_OF.get(k) or ("sort" if k.startswith(("sort_", "digit_")) else
                                     "insert" if k.startswith("insert") else "other")
-        stages[sname] = stages.get(sname, 0.0) + v["ms"] / args.steps
-    cr = kern.get("compute_ranks")
+        stages[sname] = stages.get(sname, 0.0) + v["ms"] / max(args.warmup, 1)
+    cr = warm_kern.get("compute_ranks")
     qps = (cr["units"] / (cr["ms"] / 1000.0)) if cr and cr["ms"] > 0 else None
 
     # ---- oracle beside it (rank 0, N = 1 only), + parity of this run ----
@@ -388,8 +404,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "blocks": blocks, "parallelism": "dp%d (ComputeRanks split by string)" % world,
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
             "compute_ranks_queries_per_s": qps, "stage_ms_per_step": stages,
-            "kernel_ms_per_step": {k: round(v["ms"] / args.steps, 4) for k, v in
-                                   sorted(kern.items(), key=lambda kv: -kv[1]["ms"])},
+            "profile_note": "stage/kernel ms and queries/s from warm-up steps with every launch "
+                            "timed; roofline from the timed steps (events on the dominant kernel only)",
+            "kernel_ms_per_step": {k: round(v["ms"] / max(args.warmup, 1), 4) for k, v in
+                                   sorted(warm_kern.items(), key=lambda kv: -kv[1]["ms"])},
             "roofline": roof, "cpu_baseline": cpu, "parity_vs_oracle": parity,
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},

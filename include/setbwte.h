@@ -161,6 +161,11 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *   "host_tier"       1: move B_ext to the host tier now (and keep it there). */
 setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value);
 
+/* Kernel timing for setbwte_stats: mode 0 = off, 1 = every launch, 2 = only
+ * launches of the kernel named `kernel` (CUDA events on the launching stream
+ * around each timed launch; fewer events perturb the pipeline less). */
+setbwte_status setbwte_set_profile(setbwte_t h, int mode, const char* kernel);
+
 /* Use cuda_stream (a cudaStream_t on the handle's device) for all further
  * work instead of the private stream; NULL restores the private stream. */
 setbwte_status setbwte_set_stream(setbwte_t h, void* cuda_stream);

@@ -32,7 +32,8 @@ EXPORTS = [
     "setbwte_create", "setbwte_destroy", "setbwte_strerror", "setbwte_append",
     "setbwte_append_device", "setbwte_clear", "setbwte_size", "setbwte_bwt", "setbwte_bwt_device",
     "setbwte_rank", "setbwte_rank_batch", "setbwte_construct_sa", "setbwte_compute_ranks",
-    "setbwte_set_option", "setbwte_set_stream", "setbwte_set_partition", "setbwte_stats",
+    "setbwte_set_option", "setbwte_set_profile", "setbwte_set_stream", "setbwte_set_partition",
+    "setbwte_stats",
     "setbwte_last_error",
 ]
 
@@ -72,6 +73,7 @@ def load_library(path: str = LIB_PATH):
         "setbwte_compute_ranks": ([vp, _u8p, _u64p, c64, _u64p], ctypes.c_int),
         "setbwte_set_option": ([vp, ctypes.c_char_p, c64], ctypes.c_int),
         "setbwte_set_stream": ([vp, vp], ctypes.c_int),
+        "setbwte_set_profile": ([vp, ctypes.c_int, ctypes.c_char_p], ctypes.c_int),
         "setbwte_set_partition": ([vp, ctypes.c_int, ctypes.c_int, ALLGATHER_FN, vp],
                                   ctypes.c_int),
         "setbwte_stats": ([vp, ctypes.c_char_p, c64, _u64p], ctypes.c_int),
@@ -148,6 +150,12 @@ class SetBWTE:
     # -- options -------------------------------------------------------------
     def set_option(self, key: str, value: int):
         self._check(self._lib.setbwte_set_option(self._h, key.encode(), int(value)), "set_option")
+
+    def set_profile(self, mode: int, kernel: str | None = None):
+        """0 off, 1 time every launch, 2 time only launches of `kernel`."""
+        self._check(self._lib.setbwte_set_profile(self._h, mode,
+                                                  kernel.encode() if kernel else None),
+                    "set_profile")
 
     def set_stream(self, stream):
         """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""

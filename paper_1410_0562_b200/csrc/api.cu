@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -64,7 +65,7 @@ void Profiler::begin(const char* name, cudaStream_t s, double bytes, uint64_t un
     ks.bytes += bytes;
     ks.units += units;
     total_launches++;
-    if (on) {
+    if (on && (only.empty() || only == name)) {
         *ev = get_event();
         cudaEventRecord(*ev, s);
     }
@@ -126,6 +127,9 @@ struct setbwte_s {
     cudaStream_t stream = nullptr;       // main stream (user's, or own_stream)
     cudaStream_t sort_stream = nullptr;   // ConstructSA of upcoming blocks (lane 0)
     cudaStream_t sort_stream2 = nullptr;  // lane 1
+    cudaStream_t copy_stream = nullptr;   // H2D of an append's bytes + packing, block by block
+    std::vector<cudaEvent_t> ev_packed;   // per block: its slots (and the next block's first group) packed
+    DevErr* derr_host = nullptr;          // pinned landing spot for the validation result
     cudaEvent_t ev_start = nullptr, ev_sorted[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     Profiler prof;
     bool failed = false;
@@ -436,7 +440,10 @@ struct SortLane {
     cudaEvent_t ev_sorted = nullptr;
 };
 
-setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<BlockDesc>& blocks) {
+// validate(): called on the main thread before the first Insert (the index is
+// untouched until then); a non-OK status aborts the append.
+setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<BlockDesc>& blocks,
+                          const std::function<setbwte_status()>& validate) {
     const size_t K = blocks.size();
     if (K == 0) return SETBWTE_OK;
     uint64_t max_suf = 0, total = 0;
@@ -465,6 +472,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         lanes[l].saf = saf2 + l * (max_suf + 32);
         lanes[l].ev_sorted = h->ev_sorted[l];
         lanes[l].prof.on = h->prof.on;
+        lanes[l].prof.only = h->prof.only;
     }
     // the sort lanes start after everything queued on the main stream so far
     API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
@@ -479,6 +487,9 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         SortLane& L = lanes[l];
         cudaError_t e = cudaSetDevice(h->device);
         for (size_t k = l; k < K && e == cudaSuccess; k += NL) {
+            // this block's slots and the group straddling into the next block
+            e = cudaStreamWaitEvent(L.stream, h->ev_packed[std::min(k + 1, K - 1)], 0);
+            if (e != cudaSuccess) break;
             if (k >= (size_t)NL) {
                 // SA_int buffer of this lane is free once block k-NL's gather ran
                 std::unique_lock<std::mutex> lk(mu);
@@ -504,8 +515,13 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
     std::vector<std::thread> threads;
     for (int l = 0; l < NL; ++l) threads.emplace_back(lane_main, l);
 
-    setbwte_status st = SETBWTE_OK;
-    for (size_t k = 0; k < K; ++k) {
+    setbwte_status st = validate();
+    if (st != SETBWTE_OK) {
+        std::lock_guard<std::mutex> lk(mu);
+        abort = true;
+        cv.notify_all();
+    }
+    for (size_t k = 0; k < K && st == SETBWTE_OK; ++k) {
         {
             std::unique_lock<std::mutex> lk(mu);
             cv.wait(lk, [&] { return sorted[k] || abort; });
@@ -594,8 +610,14 @@ void build_stats(setbwte_t h) {
     h->stats_json = s;
 }
 
-setbwte_status append_impl(setbwte_t h, const uint8_t* d_bytes, const uint64_t* d_off,
-                           uint64_t m) {
+// One append (Algorithm 1 over its blocks).  Host input (host_bytes != NULL):
+// the bytes travel block by block on the copy stream and each block is packed
+// as soon as its bytes are on the device, so sorting starts while later blocks
+// are still in flight; the whole input is validated before the first Insert
+// (all-or-nothing).  Device input: d_bytes already holds everything.
+setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_t* host_off,
+                           const uint8_t* d_bytes, const uint64_t* d_off, uint64_t m,
+                           uint64_t n_bytes) {
     h->prof.reset();
     h->sstats = SortStats();
     h->last_blocks = 0;
@@ -606,31 +628,91 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* d_bytes, const uint64_t* 
         return SETBWTE_OK;
     }
     if (m >= 0xFFFFFFFFull) return SETBWTE_E_UNSUPPORTED;  // u32 string ids in the packer
-    PackOut po;
-    setbwte_status st = pack_input(h, d_bytes, d_off, m, &po);
-    if (st != SETBWTE_OK) return st;
-    h->last_bases = po.n_bytes;
+    if (n_bytes == ~0ull) {
+        API_CHECK(h, cudaMemcpyAsync(&n_bytes, d_off + m, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                     h->stream));
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+    }
+    const uint64_t n_slots = n_bytes + m;
+    const uint64_t n_groups = (n_slots + 31) / 32;
+    Packed pk;
+    pk.n_slots = n_slots;
+    API_CHECK(h, ensure(h->text, 2 * n_groups + 8, &pk.text));
+    API_CHECK(h, ensure(h->term, n_groups + 8, &pk.term));
+    API_CHECK(h, ensure(h->slot_off, m + 2, &pk.slot_off));
+    API_CHECK(h, ensure(h->gfirst, n_groups + 2, &pk.gfirst));
+    DevErr* derr;
+    API_CHECK(h, ensure(h->err, 1, &derr));
+    *h->derr_host = DevErr{~0ull, 0, 0};
+    API_CHECK(h, cudaMemcpyAsync(derr, h->derr_host, sizeof(DevErr), cudaMemcpyHostToDevice,
+                                 h->stream));
+    API_CHECK(h, launch_pack_prepare(h->prof, h->stream, d_off, m, n_bytes, pk, &derr->bad_offsets));
     // partition into blocks of >= M suffixes
     uint64_t* d_bounds;
     API_CHECK(h, ensure(h->bounds, 2 * (m + 2) + 2, &d_bounds));
     uint64_t* d_k = d_bounds + 2 * (m + 2);
-    API_CHECK(h, launch_partition(h->prof, h->stream, po.pk.slot_off, m, h->M, d_bounds, d_k));
+    API_CHECK(h, launch_partition(h->prof, h->stream, pk.slot_off, m, h->M, d_bounds, d_k));
     uint64_t K = 0;
     API_CHECK(h, cudaMemcpyAsync(&K, d_k, sizeof(K), cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaMemcpyAsync(h->derr_host, derr, sizeof(DevErr), cudaMemcpyDeviceToHost,
+                                 h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
+    if (h->derr_host->bad_offsets) return SETBWTE_E_INVALID_ARG;
     std::vector<uint64_t> bounds(2 * (K + 1));
     API_CHECK(h, cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(uint64_t) * 2 * (K + 1),
                                  cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
-    // validate every block before touching the index (all-or-nothing)
     for (uint64_t b = 0; b < K; ++b) {
         if (bounds[2 * b + 3] - bounds[2 * b + 1] >= (1ull << 31)) return SETBWTE_E_UNSUPPORTED;
     }
+    h->last_bases = n_bytes;
     h->last_blocks = K;
     std::vector<BlockDesc> blocks(K);
     for (uint64_t b = 0; b < K; ++b)
         blocks[b] = BlockDesc{bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1], bounds[2 * b + 3]};
-    st = run_blocks(h, po.pk, blocks);
+    // bytes in (host input) and packing, block by block on the copy stream
+    while (h->ev_packed.size() < K) {
+        cudaEvent_t ev;
+        API_CHECK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        h->ev_packed.push_back(ev);
+    }
+    API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
+    API_CHECK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_start, 0));
+    for (uint64_t k = 0; k < K; ++k) {
+        if (host_bytes) {
+            const uint64_t b0 = host_off[blocks[k].j0], b1 = host_off[blocks[k].j1];
+            if (b1 > b0)
+                API_CHECK(h, cudaMemcpyAsync(const_cast<uint8_t*>(d_bytes) + b0, host_bytes + b0,
+                                             b1 - b0, cudaMemcpyHostToDevice, h->copy_stream));
+        }
+        const uint64_t g0 = k == 0 ? 0 : blocks[k].S0 >> 5;
+        const uint64_t g1 = k + 1 < K ? blocks[k + 1].S0 >> 5 : n_groups;
+        API_CHECK(h, launch_pack_range(h->prof, h->copy_stream, d_bytes, m, n_bytes,
+                                       (const uint8_t*)h->d_code_of.p, pk, g0, g1, &derr->err_pos));
+        API_CHECK(h, cudaEventRecord(h->ev_packed[k], h->copy_stream));
+    }
+    API_CHECK(h, cudaMemcpyAsync(h->derr_host, derr, sizeof(DevErr), cudaMemcpyDeviceToHost,
+                                 h->copy_stream));
+    auto validate = [&]() -> setbwte_status {
+        cudaError_t e = cudaStreamSynchronize(h->copy_stream);
+        if (e != cudaSuccess) return from_cuda(h, e);
+        const uint64_t ep = h->derr_host->err_pos;
+        if (ep == ~0ull) return SETBWTE_OK;
+        h->err_pos = ep;
+        uint8_t byte = 0;
+        if (host_bytes) {
+            byte = host_bytes[ep];
+        } else {
+            e = cudaMemcpy(&byte, d_bytes + ep, 1, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return from_cuda(h, e);
+        }
+        h->err_byte = byte;
+        return SETBWTE_E_INVALID_CHAR;
+    };
+    setbwte_status st = run_blocks(h, pk, blocks, validate);
+    // the main stream joins the copy stream (the bytes buffer is reused later)
+    API_CHECK(h, cudaEventRecord(h->ev_start, h->copy_stream));
+    API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
     if (st != SETBWTE_OK) return st;
     API_CHECK(h, cudaStreamSynchronize(h->stream));
     API_CHECK(h, h->prof.resolve());
@@ -683,6 +765,8 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->derr_host, sizeof(DevErr), cudaHostAllocDefault);
     for (cudaEvent_t* ev : {&h->ev_start, &h->ev_sorted[0], &h->ev_sorted[1], &h->ev_used[0],
                             &h->ev_used[1]})
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
@@ -733,6 +817,12 @@ void setbwte_destroy(setbwte_t h) {
         if (ev) cudaEventDestroy(ev);
     if (h->sort_stream) cudaStreamDestroy(h->sort_stream);
     if (h->sort_stream2) cudaStreamDestroy(h->sort_stream2);
+    if (h->copy_stream) {
+        cudaStreamSynchronize(h->copy_stream);
+        cudaStreamDestroy(h->copy_stream);
+    }
+    for (cudaEvent_t ev : h->ev_packed) cudaEventDestroy(ev);
+    if (h->derr_host) cudaFreeHost(h->derr_host);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }
@@ -741,24 +831,26 @@ setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,
                                      const uint64_t* d_offsets, uint64_t m) {
     API_ENTER(h);
     if (m > 0 && !d_offsets) return SETBWTE_E_INVALID_ARG;
-    return append_impl(h, d_strings, d_offsets, m);
+    return append_impl(h, nullptr, nullptr, d_strings, d_offsets, m, ~0ull);
 }
 
 setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
                               uint64_t m) {
     API_ENTER(h);
-    if (m == 0) return append_impl(h, nullptr, nullptr, 0);
+    if (m == 0) return append_impl(h, nullptr, nullptr, nullptr, nullptr, 0, 0);
     if (!offsets) return SETBWTE_E_INVALID_ARG;
     const uint64_t nb = offsets[m];
     if (nb > 0 && !strings) return SETBWTE_E_INVALID_ARG;
+    // CSR validity is checked on the device before any byte is copied (the
+    // copies index the host buffer by block boundaries only)
+    if (offsets[0] != 0) return SETBWTE_E_INVALID_ARG;
     uint8_t* db;
     uint64_t* dof;
     API_CHECK(h, ensure(h->in_bytes, nb + 16, &db));
     API_CHECK(h, ensure(h->in_off, m + 1, &dof));
-    if (nb) API_CHECK(h, cudaMemcpyAsync(db, strings, nb, cudaMemcpyHostToDevice, h->stream));
     API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                  h->stream));
-    return append_impl(h, db, dof, m);
+    return append_impl(h, strings, offsets, db, dof, m, nb);
 }
 
 setbwte_status setbwte_clear(setbwte_t h) {
@@ -925,6 +1017,7 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "profile")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->prof.on = value == 1;
+        h->prof.only.clear();
     } else if (!strcmp(key, "host_tier")) {
         // 1: move B_ext's dictionary to pinned host memory now (and keep it there)
         if (value != 1) return SETBWTE_E_INVALID_ARG;
@@ -951,6 +1044,13 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else {
         return SETBWTE_E_INVALID_ARG;
     }
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_set_profile(setbwte_t h, int mode, const char* kernel) {
+    if (!h || mode < 0 || mode > 2 || (mode == 2 && !kernel)) return SETBWTE_E_INVALID_ARG;
+    h->prof.on = mode != 0;
+    h->prof.only = mode == 2 ? std::string(kernel) : std::string();
     return SETBWTE_OK;
 }
 

@@ -37,6 +37,7 @@ struct KStat {
 
 struct Profiler {
     bool on = false;
+    std::string only;  // when set, only launches of this kernel name are timed
     struct Rec {
         std::string name;
         cudaEvent_t a, b;
@@ -97,6 +98,14 @@ cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
                         const uint64_t* d_off, uint64_t m, uint64_t n_bytes,
                         const uint8_t* d_code_of, Packed pk, unsigned long long* d_err_pos,
                         int* d_bad_offsets);
+// The two halves of launch_pack, so an append can pack block by block as its
+// bytes arrive: slot offsets + group map + CSR check, then the 32-slot groups
+// [g_begin, g_end).
+cudaError_t launch_pack_prepare(Profiler& prof, cudaStream_t s, const uint64_t* d_off, uint64_t m,
+                                uint64_t n_bytes, Packed pk, int* d_bad_offsets);
+cudaError_t launch_pack_range(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
+                              uint64_t m, uint64_t n_bytes, const uint8_t* d_code_of, Packed pk,
+                              uint64_t g_begin, uint64_t g_end, unsigned long long* d_err_pos);
 // Greedy block partition (reading R8): blocks end at the first
 // string boundary where the block holds >= M suffixes.  Writes K+1 pairs
 // (string index, slot offset) into d_bounds and K into *d_k.

@@ -4,6 +4,8 @@
 // Alg.1 P:55 iterates "for each block S_jk"; P:46-49 partitions the strings
 // into K blocks of roughly M suffixes (reading R8: a block ends at the first
 // string boundary where it holds >= M suffixes).
+#include <algorithm>
+
 #include "internal.h"
 
 namespace setbwte {
@@ -39,19 +41,18 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
     const uint8_t* __restrict__ bytes, uint64_t n_bytes, const uint64_t* __restrict__ slot_off,
     const uint32_t* __restrict__ gfirst, uint64_t m, uint64_t n_slots,
     const uint8_t* __restrict__ code_of_g, uint32_t* __restrict__ text, uint32_t* __restrict__ term,
-    unsigned long long* __restrict__ err_pos) {
+    unsigned long long* __restrict__ err_pos, uint64_t g_begin, uint64_t g_end) {
     __shared__ __align__(16) uint8_t sbuf[kPackWarps][1024 + 80];
     __shared__ uint8_t code_of[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) code_of[i] = code_of_g[i];
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint8_t* sb = sbuf[wib];
-    const uint64_t n_groups = (n_slots + 31) >> 5;
     const uint64_t nw = (uint64_t)gridDim.x * kPackWarps;
-    for (uint64_t wbase = ((uint64_t)blockIdx.x * kPackWarps + wib) << 10; wbase < n_slots;
-         wbase += nw << 10) {
+    for (uint64_t wbase = (g_begin << 5) + (((uint64_t)blockIdx.x * kPackWarps + wib) << 10);
+         wbase < (g_end << 5); wbase += nw << 10) {
         const uint64_t g = (wbase >> 5) + lane;
-        const bool gv = g < n_groups;
+        const bool gv = g < g_end;
         uint64_t j = gv ? min((uint64_t)gfirst[g], m - 1) : 0;
         const uint64_t j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
         const uint64_t bp_first = wbase - min(j0, wbase);
@@ -97,10 +98,8 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
     }
 }
 
-cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
-                        const uint64_t* d_off, uint64_t m, uint64_t n_bytes,
-                        const uint8_t* d_code_of, Packed pk, unsigned long long* d_err_pos,
-                        int* d_bad_offsets) {
+cudaError_t launch_pack_prepare(Profiler& prof, cudaStream_t s, const uint64_t* d_off, uint64_t m,
+                                uint64_t n_bytes, Packed pk, int* d_bad_offsets) {
     SB_LAUNCH(prof, s, "slot_offsets", 16.0 * (m + 1), m + 1,
               slot_off_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(d_off, m, n_bytes, pk.slot_off,
                                                                    pk.gfirst, d_bad_offsets));
@@ -109,13 +108,30 @@ cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
     // padding words past the end must read as zero
     SB_CHECK(cudaMemsetAsync(pk.text + 2 * n_groups, 0, 4 * sizeof(uint32_t), s));
     SB_CHECK(cudaMemsetAsync(pk.term + n_groups, 0, 4 * sizeof(uint32_t), s));
+    return cudaSuccess;
+}
+
+cudaError_t launch_pack_range(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
+                              uint64_t m, uint64_t n_bytes, const uint8_t* d_code_of, Packed pk,
+                              uint64_t g_begin, uint64_t g_end, unsigned long long* d_err_pos) {
+    if (g_end <= g_begin) return cudaSuccess;
+    const uint64_t slots = std::min(g_end << 5, pk.n_slots) - (g_begin << 5);
     // algorithmic bytes: 1 B read per base + 3 bits written per slot
-    const uint64_t n_warps = (pk.n_slots + 1023) >> 10;
-    SB_LAUNCH(prof, s, "pack", (double)n_bytes + 0.375 * pk.n_slots, n_bytes,
+    const uint64_t n_warps = ((g_end - g_begin) + 31) >> 5;
+    SB_LAUNCH(prof, s, "pack", 1.375 * (double)slots, slots,
               pack_kernel<<<grid_for(n_warps, kPackWarps, 148u * 16u), kPackWarps * 32, 0, s>>>(
                   d_bytes, n_bytes, pk.slot_off, pk.gfirst, m, pk.n_slots, d_code_of, pk.text,
-                  pk.term, d_err_pos));
+                  pk.term, d_err_pos, g_begin, g_end));
     return cudaGetLastError();
+}
+
+cudaError_t launch_pack(Profiler& prof, cudaStream_t s, const uint8_t* d_bytes,
+                        const uint64_t* d_off, uint64_t m, uint64_t n_bytes,
+                        const uint8_t* d_code_of, Packed pk, unsigned long long* d_err_pos,
+                        int* d_bad_offsets) {
+    SB_CHECK(launch_pack_prepare(prof, s, d_off, m, n_bytes, pk, d_bad_offsets));
+    return launch_pack_range(prof, s, d_bytes, m, n_bytes, d_code_of, pk, 0,
+                             (pk.n_slots + 31) >> 5, d_err_pos);
 }
 
 __global__ void partition_kernel(const uint64_t* __restrict__ slot_off, uint64_t m, uint64_t M,
