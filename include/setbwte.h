@@ -122,6 +122,20 @@ setbwte_status setbwte_rank(setbwte_t h, uint8_t c, uint64_t k, uint64_t* out);
 setbwte_status setbwte_rank_batch(setbwte_t h, const uint8_t* c_dev, const uint64_t* k_dev,
                                   uint64_t q, uint64_t* out_dev);
 
+/* FM-index count ("BWT and FM-index") by backward search with C
+ * and rank (Lemma 1 P:97-100 on a row interval): counts[t] = number of
+ * occurrences of pattern t as a substring of the indexed strings (every
+ * offset counted, matches never span a terminator).  Pattern t is
+ * patterns[offsets[t] .. offsets[t+1]) (HOST; offsets has q+1 non-decreasing
+ * u64).  A pattern with a byte outside the alphabet counts 0; the empty
+ * pattern counts n.  counts: HOST, q u64. */
+setbwte_status setbwte_count(setbwte_t h, const uint8_t* patterns, const uint64_t* offsets,
+                             uint64_t q, uint64_t* counts);
+
+/* Same as setbwte_count with DEVICE arrays (d_patterns, d_offsets, d_counts). */
+setbwte_status setbwte_count_device(setbwte_t h, const uint8_t* d_patterns,
+                                    const uint64_t* d_offsets, uint64_t q, uint64_t* d_counts);
+
 /* ConstructSA + B_int of ONE block, without touching the index (Alg.1
  * P:60-63; Sec.3).  Inputs as setbwte_append (HOST).  The block must
  * hold fewer than 2^31 suffixes.  Outputs (HOST, each n_suf = offsets[m]+m

@@ -15,6 +15,8 @@ Functions and the passage each follows (P:<line> = /root/reference/PAPER.md):
 * ``rank``          -- Eq.(2), literal scan
 * ``insert``        -- Insert, Alg.1 P:72-73 / Sec.5, flat list insertion
 * ``suffix_rank``   -- SA position of one suffix by counting (definition)
+* ``count``         -- substring occurrences by literal comparison (what the
+                       FM-index count answers)
 
 Pins for each are in ``tests/test_oracle_pins.py``; see DESIGN.md "Oracle pins".
 """
@@ -65,6 +67,8 @@ def _load():
         lib.oracle_rank.argtypes = [_u8p, ctypes.c_uint64, ctypes.c_uint8, ctypes.c_uint64]
         lib.oracle_rank.restype = ctypes.c_uint64
         lib.oracle_insert.argtypes = [_u8p, ctypes.c_uint64, _u8p, _u64p, ctypes.c_uint64, _u8p]
+        lib.oracle_count.argtypes = [ctypes.c_char_p, _u8p, _u64p, ctypes.c_uint64, _u8p, _u64p,
+                                     ctypes.c_uint64, _u64p, ctypes.c_int]
         lib.oracle_suffix_rank.argtypes = [ctypes.c_char_p, _u8p, _u64p, ctypes.c_uint64,
                                            ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_int,
                                            _u64p]
@@ -181,3 +185,21 @@ def suffix_rank(alphabet: str, data, offsets, j: int, k: int, threads: int | Non
                                     _threads(threads), ctypes.byref(bad))
     _check(rc, bad)
     return int(out.value)
+
+
+def count(alphabet: str, data, offsets, patterns, threads: int | None = 1) -> np.ndarray:
+    """Occurrences of each pattern (list of str/bytes) in the strings."""
+    bs = [p.encode() if isinstance(p, str) else bytes(p) for p in patterns]
+    poff = np.zeros(len(bs) + 1, dtype=np.uint64)
+    if bs:
+        poff[1:] = np.cumsum([len(b) for b in bs])
+    data, dp = _u8(data)
+    offsets, op = _u64(offsets)
+    pat, pp = _u8(np.frombuffer(b"".join(bs), np.uint8) if sum(map(len, bs)) else np.zeros(1, np.uint8))
+    poff, pop = _u64(poff)
+    out = np.zeros(max(len(bs), 1), dtype=np.uint64)
+    rc = _load().oracle_count(alphabet.encode(), dp, op, len(offsets) - 1, pp, pop, len(bs),
+                              out.ctypes.data_as(_u64p), _threads(threads))
+    if rc:
+        raise OracleError("oracle error %d" % rc)
+    return out[:len(bs)]

@@ -288,4 +288,34 @@ int oracle_suffix_rank(const char* alphabet, const uint8_t* bytes, const uint64_
     return 0;
 }
 
+/* Occurrences of each pattern as a substring of the strings, every offset
+ * counted (the definition the FM-index count answers; SPEC's
+ * naive_count_occurrences).  Literal comparison at every start position; a
+ * match never spans two strings.  Case-insensitive like the rest. */
+int oracle_count(const char* alphabet, const uint8_t* bytes, const uint64_t* off, uint64_t m,
+                 const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out,
+                 int threads) {
+    if (!alphabet || !off || !poff || !out) return -1;
+    if (threads < 1) threads = 1;
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
+    for (int64_t t = 0; t < (int64_t)q; ++t) {
+        const uint64_t pl = poff[t + 1] - poff[t];
+        uint64_t cnt = 0;
+        if (pl == 0) {
+            cnt = off[m] + m;  /* the empty pattern: every suffix (reading of SETBWTE docs) */
+        } else {
+            for (uint64_t j = 0; j < m; ++j) {
+                const uint64_t L = off[j + 1] - off[j];
+                for (uint64_t a = 0; a + pl <= L; ++a) {
+                    uint64_t k = 0;
+                    while (k < pl && toupper(bytes[off[j] + a + k]) == toupper(pat[poff[t] + k])) ++k;
+                    cnt += (k == pl);
+                }
+            }
+        }
+        out[t] = cnt;
+    }
+    return 0;
+}
+
 }  /* extern "C" */

@@ -31,7 +31,8 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _u64p, ctypes.c_i
 EXPORTS = [
     "setbwte_create", "setbwte_destroy", "setbwte_strerror", "setbwte_append",
     "setbwte_append_device", "setbwte_clear", "setbwte_size", "setbwte_bwt", "setbwte_bwt_device",
-    "setbwte_rank", "setbwte_rank_batch", "setbwte_construct_sa", "setbwte_compute_ranks",
+    "setbwte_rank", "setbwte_rank_batch", "setbwte_count", "setbwte_count_device",
+    "setbwte_construct_sa", "setbwte_compute_ranks",
     "setbwte_set_option", "setbwte_set_profile", "setbwte_set_stream", "setbwte_set_partition",
     "setbwte_stats",
     "setbwte_last_error",
@@ -69,6 +70,8 @@ def load_library(path: str = LIB_PATH):
         "setbwte_bwt_device": ([vp, vp, c64, _u64p], ctypes.c_int),
         "setbwte_rank": ([vp, ctypes.c_uint8, c64, _u64p], ctypes.c_int),
         "setbwte_rank_batch": ([vp, vp, vp, c64, vp], ctypes.c_int),
+        "setbwte_count": ([vp, _u8p, _u64p, c64, _u64p], ctypes.c_int),
+        "setbwte_count_device": ([vp, vp, vp, c64, vp], ctypes.c_int),
         "setbwte_construct_sa": ([vp, _u8p, _u64p, c64, _u32p, _u8p], ctypes.c_int),
         "setbwte_compute_ranks": ([vp, _u8p, _u64p, c64, _u64p], ctypes.c_int),
         "setbwte_set_option": ([vp, ctypes.c_char_p, c64], ctypes.c_int),
@@ -240,6 +243,25 @@ class SetBWTE:
         """Device batch: c_t uint8, k_t int64/uint64, out_t int64/uint64 CUDA tensors."""
         self._check(self._lib.setbwte_rank_batch(self._h, c_t.data_ptr(), k_t.data_ptr(),
                                                  c_t.numel(), out_t.data_ptr()), "rank_batch")
+        return out_t
+
+    def count(self, patterns):
+        """FM-index count of each pattern (list of str/bytes) -> numpy u64 array."""
+        bs = [p.encode() if isinstance(p, str) else bytes(p) for p in patterns]
+        off = np.zeros(len(bs) + 1, dtype=np.uint64)
+        if bs:
+            off[1:] = np.cumsum([len(b) for b in bs])
+        d, dp = _host_u8(b"".join(bs))
+        o, op = _host_u64(off)
+        out = np.zeros(max(len(bs), 1), dtype=np.uint64)
+        self._check(self._lib.setbwte_count(self._h, dp, op, len(bs), out.ctypes.data_as(_u64p)),
+                    "count")
+        return out[:len(bs)]
+
+    def count_device(self, pat_t, off_t, out_t):
+        self._check(self._lib.setbwte_count_device(self._h, pat_t.data_ptr(), off_t.data_ptr(),
+                                                   off_t.numel() - 1, out_t.data_ptr()),
+                    "count_device")
         return out_t
 
     def construct_sa(self, data, offsets):

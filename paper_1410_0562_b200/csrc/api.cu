@@ -945,6 +945,51 @@ setbwte_status setbwte_rank_batch(setbwte_t h, const uint8_t* c_dev, const uint6
     return SETBWTE_OK;
 }
 
+static setbwte_status count_impl(setbwte_t h, const uint8_t* d_pat, const uint64_t* d_off,
+                                 uint64_t q, uint64_t* d_out) {
+    if (h->n == 0) {
+        API_CHECK(h, cudaMemsetAsync(d_out, 0, q * sizeof(uint64_t), h->stream));
+        return SETBWTE_OK;
+    }
+    API_CHECK(h, launch_count(h->prof, h->stream, cur_blk(h), cur_sb(h), h->n,
+                              (const uint64_t*)h->d_C.p, (const uint8_t*)h->d_code_of.p, d_pat,
+                              d_off, q, d_out));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_count(setbwte_t h, const uint8_t* patterns, const uint64_t* offsets,
+                             uint64_t q, uint64_t* counts) {
+    API_ENTER(h);
+    if (q == 0) return SETBWTE_OK;
+    if (!offsets || !counts || (offsets[q] > 0 && !patterns)) return SETBWTE_E_INVALID_ARG;
+    const uint64_t nb = offsets[q];
+    for (uint64_t t = 0; t < q; ++t)
+        if (offsets[t] > offsets[t + 1]) return SETBWTE_E_INVALID_ARG;
+    uint8_t* dp;
+    uint64_t* dof;
+    API_CHECK(h, ensure(h->in_bytes, nb + 16, &dp));
+    API_CHECK(h, ensure(h->in_off, 2 * (q + 1), &dof));
+    if (nb) API_CHECK(h, cudaMemcpyAsync(dp, patterns, nb, cudaMemcpyHostToDevice, h->stream));
+    API_CHECK(h, cudaMemcpyAsync(dof, offsets, (q + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    uint64_t* dout = dof + (q + 1);
+    setbwte_status st = count_impl(h, dp, dof, q, dout);
+    if (st != SETBWTE_OK) return st;
+    API_CHECK(h, cudaMemcpyAsync(counts, dout, q * 8, cudaMemcpyDeviceToHost, h->stream));
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_count_device(setbwte_t h, const uint8_t* d_patterns,
+                                    const uint64_t* d_offsets, uint64_t q, uint64_t* d_counts) {
+    API_ENTER(h);
+    if (q == 0) return SETBWTE_OK;
+    if (!d_patterns || !d_offsets || !d_counts) return SETBWTE_E_INVALID_ARG;
+    setbwte_status st = count_impl(h, d_patterns, d_offsets, q, d_counts);
+    if (st != SETBWTE_OK) return st;
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    return SETBWTE_OK;
+}
+
 setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
                                     uint64_t m, uint32_t* sa_out, uint8_t* bint_out) {
     API_ENTER(h);

@@ -293,6 +293,45 @@ cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uin
     return launch_sb_scan(prof, s, sb_tot, nsb, out_sb, m_new, d_C);
 }
 
+// FM-index count by backward search (Lemma 1 P:97-100 applied to
+// the interval [lo, hi) of rows whose suffixes start with the pattern's
+// processed tail): per pattern P, for k = |P|-1..0: c = P[k];
+// lo = C[c] + rank(c, lo), hi = C[c] + rank(c, hi); count = hi - lo.
+// A byte outside the alphabet makes the count 0; the empty pattern counts n.
+__global__ void count_kernel(const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+                             uint64_t n, const uint64_t* __restrict__ Cd,
+                             const uint8_t* __restrict__ code_of, const uint8_t* __restrict__ pat,
+                             const uint64_t* __restrict__ poff, uint64_t q,
+                             uint64_t* __restrict__ out) {
+    const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < q;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = poff[t], b = poff[t + 1];
+        uint64_t lo = 0, hi = n;
+        for (uint64_t k = b; k > a && lo < hi; --k) {
+            const uint8_t c = code_of[pat[k - 1]];
+            if (c > 3) {
+                lo = hi = 0;
+                break;
+            }
+            const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
+            lo = Cc + dict_rank(blk, sb, c, lo);
+            hi = Cc + dict_rank(blk, sb, c, hi);
+        }
+        out[t] = hi > lo ? hi - lo : 0;
+    }
+}
+
+cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+                         uint64_t n, const uint64_t* d_C, const uint8_t* code_of,
+                         const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out) {
+    if (q == 0) return cudaSuccess;
+    SB_LAUNCH(prof, s, "fm_count", 0, q,
+              count_kernel<<<grid_for(q, 128, 148u * 64u), 128, 0, s>>>(blk, sb, n, d_C, code_of,
+                                                                        pat, poff, q, out));
+    return cudaGetLastError();
+}
+
 __global__ void rank_batch_kernel(const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
                                   uint64_t n, const uint8_t* __restrict__ code_of,
                                   const uint8_t* __restrict__ cq, const uint64_t* __restrict__ kq,

@@ -161,6 +161,9 @@ cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_to
 cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
                               uint64_t n, const uint8_t* code_of, const uint8_t* c,
                               const uint64_t* k, uint64_t q, uint64_t* out);
+cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+                         uint64_t n, const uint64_t* d_C, const uint8_t* code_of,
+                         const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out);
 cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Blk* blk, uint64_t n,
                           const uint8_t* sym_ascii, uint8_t* out);
 // Debug/export: SA + B_int ASCII of a sorted block.

@@ -558,11 +558,11 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
     constexpr int NW = kDigNt / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);  // NW*256
-    uint32_t* s_key = wcnt + NW * 256;                        // kDigTile
-    uint32_t* s_slot = s_key + kDigTile;                      // kDigTile
-    uint32_t* dstart = s_slot + kDigTile;                     // 257
+    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + NW * 256);  // kDigTile (key, slot)
+    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_kv + kDigTile);  // 257
     uint32_t* run_base = dstart + 260;                        // 256
-    uint32_t* tmp = run_base + 256;                           // 32
+    uint32_t* off = run_base + 256;                           // 256: run_base - dstart
+    uint32_t* tmp = off + 256;                                // 32
     uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);      // 256
     const uint32_t nch = misc[M_CHUNKS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -595,25 +595,22 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
                 dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
             }
             block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
+            if (tid < 256) off[tid] = run_base[tid] - dstart[tid];  // mod 2^32
 #pragma unroll
-            for (int it = 0; it < kDigIpt; ++it) {
-                if (dig[it] < 256) {
-                    s_key[dest[it]] = key[it];
-                    s_slot[dest[it]] = slot[it];
-                }
-            }
+            for (int it = 0; it < kDigIpt; ++it)
+                if (dig[it] < 256) s_kv[dest[it]] = make_uint2(key[it], slot[it]);
             __syncthreads();
             // coalesced write-out: consecutive tile positions of one digit go to
             // consecutive global positions
             for (uint32_t i = tid; i < tn; i += kDigNt) {
-                const uint32_t k = s_key[i];
-                const uint32_t d = (k >> shift) & 0xFFu;
-                const uint32_t gp = run_base[d] + (i - dstart[d]);
+                const uint2 kv = s_kv[i];
+                const uint32_t d = (kv.x >> shift) & 0xFFu;
+                const uint32_t gp = off[d] + i;
                 if (fin[d]) {
-                    __stcs(B.saf + gp, s_slot[i]);
+                    __stcs(B.saf + gp, kv.y);
                 } else {
-                    __stcs(S2 + gp, s_slot[i]);
-                    __stcs(K2 + gp, k);
+                    __stcs(S2 + gp, kv.y);
+                    __stcs(K2 + gp, kv.x);
                 }
             }
             __syncthreads();
@@ -624,7 +621,7 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
 }
 
 constexpr size_t scatter_smem() {
-    return (size_t)(kDigNt / 32) * 256 * 4 + 2 * (size_t)kDigTile * 4 + 260 * 4 + 256 * 4 +
+    return (size_t)(kDigNt / 32) * 256 * 4 + 2 * (size_t)kDigTile * 4 + 260 * 4 + 2 * 256 * 4 +
            32 * 4 + 256 + 16;
 }
 

@@ -325,3 +325,38 @@ def test_host_tier_multichunk(SetBWTE):
     idx.append(d, o)
     assert idx.stats()["host_tier"] == 1
     assert idx.bwt() == want
+
+
+# --- FM-index count (NEXT-2) ----------------------------------------------------
+
+def test_fm_count_examples(SetBWTE):
+    for case in SPEC["fm_count"]:
+        idx = SetBWTE(A)
+        idx.append_strings(case["strings"])
+        assert list(idx.count([case["pattern"]])) == [case["count"]], case["cite"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fm_count_vs_oracle(SetBWTE, seed):
+    d, o = synth.random_set(8000 + seed, max_m=64, max_len=50, alphabet=["ACGT", "AC", "GT"][seed % 3])
+    rng = np.random.default_rng(seed)
+    pats = ["".join(rng.choice(list("ACGT"), size=int(rng.integers(1, 13)))) for _ in range(300)]
+    pats += ["", "ACGTN", "a"]
+    idx = SetBWTE(A, block_suffixes=int(rng.integers(50, 500)))
+    idx.append(d, o)
+    want = oracle.count(A, d, o, pats)
+    want[-2] = 0  # 'N' is outside the alphabet
+    assert np.array_equal(idx.count(pats), want)
+
+
+def test_fm_count_c1_and_host_tier(SetBWTE, c1):
+    d, o, _ = c1
+    rng = np.random.default_rng(5)
+    starts = rng.integers(0, len(d) - 20, size=200)
+    pats = [bytes(d[a:a + int(rng.integers(1, 16))]).decode() for a in starts]
+    want = oracle.count(A, d, o, pats, threads=None)
+    for budget in (1 << 40, 1):
+        idx = SetBWTE(A, block_suffixes=25250)
+        idx.set_option("hbm_budget_bytes", budget)
+        idx.append(d, o)
+        assert np.array_equal(idx.count(pats), want)

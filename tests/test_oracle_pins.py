@@ -247,3 +247,18 @@ def test_fm_count_examples_via_oracle_bwt():
             lo = C[c] + oracle.rank(B, c, lo)
             hi = C[c] + oracle.rank(B, c, hi)
         assert hi - lo == case["count"] == brute.naive_count(case["pattern"], case["strings"])
+
+
+def test_oracle_count_pins():
+    """oracle.count against SPEC's fm_count examples and a Python
+    brute force (different code: str slicing)."""
+    for case in SPEC["fm_count"]:
+        d, o = _fs(case["strings"])
+        assert list(oracle.count(A, d, o, [case["pattern"]])) == [case["count"]]
+    for seed in range(10):
+        d, o = synth.random_set(7000 + seed, max_m=12, max_len=20, alphabet=["ACGT", "AC"][seed % 2])
+        strings = synth.to_strings(d, o)
+        rng = np.random.default_rng(seed)
+        pats = ["".join(rng.choice(list("ACGT"), size=int(rng.integers(1, 5)))) for _ in range(20)]
+        got = oracle.count(A, d, o, pats)
+        assert list(got) == [brute.naive_count(p, strings) for p in pats]
