@@ -96,6 +96,29 @@ setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_
 setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,
                                      const uint64_t* d_offsets, uint64_t m);
 
+/* Reverse orientation ("the strings are added in a forward loop ...
+ * though reversal is also possible").  Adds m strings (same layout and
+ * all-or-nothing validation as setbwte_append) BEFORE every string already
+ * indexed: afterwards setbwte_bwt() == the one-shot BWT of
+ * (these strings, in order) followed by (the strings indexed before).
+ * Blocks are inserted last block first; a new string's terminator suffix has
+ * rank 0 among the indexed suffixes (every older terminator is larger). */
+setbwte_status setbwte_prepend(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                               uint64_t m);
+
+/* setbwte_prepend with DEVICE-resident inputs (as setbwte_append_device). */
+setbwte_status setbwte_prepend_device(setbwte_t h, const uint8_t* d_strings,
+                                      const uint64_t* d_offsets, uint64_t m);
+
+/* BWT merge (the LF / insert machinery of Alg.1
+ * with B_int given): appends the strings of index `other` after those of h,
+ * using other's BWT only (its strings are recovered by LF walks).  Afterwards
+ * setbwte_bwt(h) == the one-shot BWT of (h's strings) followed by (other's
+ * strings); other is unchanged.  Both handles must be on the same device with
+ * the same alphabet (else SETBWTE_E_UNSUPPORTED); other == h or NULL ->
+ * SETBWTE_E_INVALID_ARG.  Synchronous. */
+setbwte_status setbwte_merge(setbwte_t h, setbwte_t other);
+
 /* Remove every string (n = m = 0) but keep device allocations for reuse. */
 setbwte_status setbwte_clear(setbwte_t h);
 

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsetbwte.so")
+LIB_PATH = os.environ.get("SETBWTE_LIB") or os.path.join(_PKG, "libsetbwte.so")
 
 STATUS = {
     0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_CHAR", 3: "E_OUT_OF_RANGE", 4: "E_NOMEM",
@@ -30,7 +30,8 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _u64p, ctypes.c_i
 #: every symbol include/setbwte.h declares
 EXPORTS = [
     "setbwte_create", "setbwte_destroy", "setbwte_strerror", "setbwte_append",
-    "setbwte_append_device", "setbwte_clear", "setbwte_size", "setbwte_bwt", "setbwte_bwt_device",
+    "setbwte_append_device", "setbwte_prepend", "setbwte_prepend_device", "setbwte_merge",
+    "setbwte_clear", "setbwte_size", "setbwte_bwt", "setbwte_bwt_device",
     "setbwte_rank", "setbwte_rank_batch", "setbwte_count", "setbwte_count_device",
     "setbwte_construct_sa", "setbwte_compute_ranks",
     "setbwte_set_option", "setbwte_set_profile", "setbwte_set_stream", "setbwte_set_partition",
@@ -64,6 +65,9 @@ def load_library(path: str = LIB_PATH):
         "setbwte_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "setbwte_append": ([vp, _u8p, _u64p, c64], ctypes.c_int),
         "setbwte_append_device": ([vp, vp, vp, c64], ctypes.c_int),
+        "setbwte_prepend": ([vp, _u8p, _u64p, c64], ctypes.c_int),
+        "setbwte_prepend_device": ([vp, vp, vp, c64], ctypes.c_int),
+        "setbwte_merge": ([vp, vp], ctypes.c_int),
         "setbwte_clear": ([vp], ctypes.c_int),
         "setbwte_size": ([vp, _u64p, _u64p], ctypes.c_int),
         "setbwte_bwt": ([vp, vp, c64, _u64p], ctypes.c_int),
@@ -204,6 +208,29 @@ class SetBWTE:
             m = offsets_t.numel() - 1
         self._check(self._lib.setbwte_append_device(self._h, data_t.data_ptr(),
                                                     offsets_t.data_ptr(), m), "append_device")
+
+    def prepend(self, data, offsets):
+        """Reverse orientation: add strings BEFORE every indexed string."""
+        d, dp = _host_u8(data)
+        o, op = _host_u64(offsets)
+        self._check(self._lib.setbwte_prepend(self._h, dp, op, len(o) - 1), "prepend")
+
+    def prepend_strings(self, strings):
+        bs = [s.encode() if isinstance(s, str) else bytes(s) for s in strings]
+        off = np.zeros(len(bs) + 1, dtype=np.uint64)
+        if bs:
+            off[1:] = np.cumsum([len(b) for b in bs])
+        self.prepend(b"".join(bs), off)
+
+    def prepend_device(self, data_t, offsets_t, m: int | None = None):
+        if m is None:
+            m = offsets_t.numel() - 1
+        self._check(self._lib.setbwte_prepend_device(self._h, data_t.data_ptr(),
+                                                     offsets_t.data_ptr(), m), "prepend_device")
+
+    def merge(self, other: "SetBWTE"):
+        """BWT merge: append the strings of `other` (from its BWT) after ours."""
+        self._check(self._lib.setbwte_merge(self._h, other._h), "merge")
 
     def clear(self):
         self._check(self._lib.setbwte_clear(self._h), "clear")

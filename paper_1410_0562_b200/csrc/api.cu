@@ -167,6 +167,10 @@ struct setbwte_s {
     DevBuf stage_in, stage_out;
     std::vector<uint64_t> h_sb_start;
 
+    // reverse orientation: the strings of the running call go BEFORE
+    // every string already indexed, so a new terminator is the smallest suffix
+    bool prepending = false;
+
     // data-parallel ComputeRanks
     int rank = 0, world = 1;
     setbwte_allgather_fn allgather = nullptr;
@@ -266,8 +270,8 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     if (h->world <= 1) {
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_blk(h), cur_sb(h),
-                                          (const uint64_t*)h->d_C.p, h->m, n_suf - (j1 - j0), g,
-                                          gw, h->rank_ilp));
+                                          (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
+                                          n_suf - (j1 - j0), g, gw, h->rank_ilp));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
@@ -287,8 +291,8 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     const uint64_t a = sl[h->rank], b = sl[h->rank + 1];
     const uint64_t steps = (slot_of[h->rank + 1] - slot_of[h->rank]) - (b - a);
     API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
-                                      cur_blk(h), cur_sb(h), (const uint64_t*)h->d_C.p, h->m,
-                                      steps, g, gw, h->rank_ilp));
+                                      cur_blk(h), cur_sb(h), (const uint64_t*)h->d_C.p,
+                                      h->prepending ? 0 : h->m, steps, g, gw, h->rank_ilp));
     std::vector<uint64_t> bytes(h->world);
     for (int r = 0; r < h->world; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
     if (!h->allgather) return SETBWTE_E_STATE;
@@ -304,6 +308,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
 // (the paper's stage pipeline P:190-191).
 struct BlockDesc {
     uint64_t j0, j1, S0, S1;
+    uint64_t ev;  // index of the ev_packed event after which its slots are packed
 };
 
 // Pinned mapped host buffer for the dictionary with >= nblk Blks, keeping
@@ -375,6 +380,51 @@ setbwte_status host_insert(setbwte_t h, const void* pos, int gw, const uint8_t* 
     return SETBWTE_OK;
 }
 
+// Output buffers of one Insert of n_ins symbols (HBM or host tier).
+struct InsertBufs {
+    Blk* ob = nullptr;
+    uint64_t *osb = nullptr, *tot = nullptr, *sb_start = nullptr;
+    uint64_t nsb = 0;
+};
+
+setbwte_status insert_prepare(setbwte_t h, uint64_t n_ins, InsertBufs* ib) {
+    const uint64_t n_out = h->n + n_ins;
+    const uint64_t nblk = (n_out >> 6) + 1;
+    ib->nsb = (n_out >> kSbShift) + 1;
+    const int nxt = 1 - h->cur;
+    if (!h->host_tier && nblk * sizeof(Blk) > h->hbm_budget) {
+        // the dictionary outgrows its HBM budget: move B_ext to the host tier
+        // (after this block's ComputeRanks, which still reads the HBM copy)
+        setbwte_status st2 = host_reserve(h, nblk, cur_blk(h), true, h->n ? (h->n >> 6) + 1 : 0);
+        if (st2 != SETBWTE_OK) return st2;
+        h->host_tier = true;
+        free_buf(h->blk[0]);
+        free_buf(h->blk[1]);
+    }
+    if (!h->host_tier) API_CHECK(h, ensure(h->blk[nxt], nblk, &ib->ob));
+    API_CHECK(h, ensure(h->sb[nxt], ib->nsb * 4, &ib->osb));
+    API_CHECK(h, ensure(h->sb_tot, ib->nsb * 5 + 8, &ib->tot));  // totals + sb_start
+    ib->sb_start = ib->tot + 4 * (ib->nsb + 1);
+    return SETBWTE_OK;
+}
+
+// B_ext := Insert(B_int, g_sa, B_ext) with pos / B_int / sb_start ready.
+setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos, int gw,
+                             const uint8_t* bint, uint64_t n_ins, uint64_t m_add) {
+    const uint64_t m_new = h->m + m_add;
+    if (h->host_tier) {
+        setbwte_status st = host_insert(h, pos, gw, bint, n_ins, ib.osb, ib.tot, ib.sb_start, m_new);
+        if (st != SETBWTE_OK) return st;
+    } else {
+        API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_ins, ib.ob,
+                                   ib.osb, ib.tot, ib.sb_start, m_new, (uint64_t*)h->d_C.p));
+    }
+    h->cur = 1 - h->cur;
+    h->n += n_ins;
+    h->m = m_new;
+    return SETBWTE_OK;
+}
+
 // ComputeRanks, B_int + g_sa gather, Insert; on the main stream.
 setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc& b,
                                  const uint32_t* saf) {
@@ -387,41 +437,51 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // g := ComputeRanks(S_jk, B_ext)
     setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw);
     if (st != SETBWTE_OK) return st;
-    // B_ext := Insert(B_int, g_sa, B_ext) -- buffers first
-    const uint64_t n_out = h->n + n_suf;
-    const uint64_t nblk = (n_out >> 6) + 1;
-    const uint64_t nsb = (n_out >> kSbShift) + 1;
-    const int nxt = 1 - h->cur;
-    Blk* ob = nullptr;
-    uint64_t *osb, *tot;
-    if (!h->host_tier && nblk * sizeof(Blk) > h->hbm_budget) {
-        // the dictionary outgrows its HBM budget: move B_ext to the host tier
-        // (after this block's ComputeRanks, which still reads the HBM copy)
-        setbwte_status st2 = host_reserve(h, nblk, cur_blk(h), true, h->n ? (h->n >> 6) + 1 : 0);
-        if (st2 != SETBWTE_OK) return st2;
-        h->host_tier = true;
-        free_buf(h->blk[0]);
-        free_buf(h->blk[1]);
-    }
-    if (!h->host_tier) API_CHECK(h, ensure(h->blk[nxt], nblk, &ob));
-    API_CHECK(h, ensure(h->sb[nxt], nsb * 4, &osb));
-    API_CHECK(h, ensure(h->sb_tot, nsb * 5 + 8, &tot));  // totals + sb_start
-    uint64_t* sb_start = tot + 4 * (nsb + 1);
+    InsertBufs ib;
+    st = insert_prepare(h, n_suf, &ib);
+    if (st != SETBWTE_OK) return st;
     // B_int := B(S_jk, SA_int), g_sa / pos and the superblock
     // slices of pos, fused
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
-                               (uint32_t)n_suf, pos, gw, bint, sb_start, nsb));
-    const uint64_t m_new = h->m + (b.j1 - b.j0);
-    if (h->host_tier) {
-        st = host_insert(h, pos, gw, bint, n_suf, osb, tot, sb_start, m_new);
-        if (st != SETBWTE_OK) return st;
-    } else {
-        API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_suf, ob,
-                                   osb, tot, sb_start, m_new, (uint64_t*)h->d_C.p));
+                               (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb));
+    return insert_finish(h, ib, pos, gw, bint, n_suf, b.j1 - b.j0);
+}
+
+void build_stats(setbwte_t h);
+
+// BWT merge (NEXT-4): h := h followed by the strings of o, from o's BWT alone.
+setbwte_status merge_impl(setbwte_t h, setbwte_t o) {
+    h->prof.reset();
+    h->sstats = SortStats();
+    h->last_blocks = o->n ? 1 : 0;
+    h->last_bases = o->n - o->m;
+    h->last_m = o->m;
+    if (o->n == 0) {
+        build_stats(h);
+        return SETBWTE_OK;
     }
-    h->cur = nxt;
-    h->n = n_out;
-    h->m = m_new;
+    API_CHECK(h, cudaStreamSynchronize(o->stream));
+    const uint64_t n_o = o->n;
+    const int gw = (h->n + n_o) < (1ull << 32) ? 4 : 8;
+    uint64_t *g, *pos;
+    uint8_t* bint;
+    API_CHECK(h, ensure(h->g, n_o, &g));
+    API_CHECK(h, ensure(h->pos, n_o, &pos));
+    API_CHECK(h, ensure(h->bint, n_o, &bint));
+    API_CHECK(h, launch_merge_ranks(h->prof, h->stream, cur_blk(o), cur_sb(o),
+                                    (const uint64_t*)o->d_C.p, o->m, n_o,
+                                    h->n ? cur_blk(h) : nullptr, h->n ? cur_sb(h) : nullptr,
+                                    (const uint64_t*)h->d_C.p, h->m, g, gw));
+    InsertBufs ib;
+    setbwte_status st = insert_prepare(h, n_o, &ib);
+    if (st != SETBWTE_OK) return st;
+    API_CHECK(h, launch_merge_pos(h->prof, h->stream, cur_blk(o), n_o, g, pos, gw, bint,
+                                  ib.sb_start, ib.nsb));
+    st = insert_finish(h, ib, pos, gw, bint, n_o, o->m);
+    if (st != SETBWTE_OK) return st;
+    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    API_CHECK(h, h->prof.resolve());
+    build_stats(h);
     return SETBWTE_OK;
 }
 
@@ -488,7 +548,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         cudaError_t e = cudaSetDevice(h->device);
         for (size_t k = l; k < K && e == cudaSuccess; k += NL) {
             // this block's slots and the group straddling into the next block
-            e = cudaStreamWaitEvent(L.stream, h->ev_packed[std::min(k + 1, K - 1)], 0);
+            e = cudaStreamWaitEvent(L.stream, h->ev_packed[blocks[k].ev], 0);
             if (e != cudaSuccess) break;
             if (k >= (size_t)NL) {
                 // SA_int buffer of this lane is free once block k-NL's gather ran
@@ -617,7 +677,7 @@ void build_stats(setbwte_t h) {
 // (all-or-nothing).  Device input: d_bytes already holds everything.
 setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_t* host_off,
                            const uint8_t* d_bytes, const uint64_t* d_off, uint64_t m,
-                           uint64_t n_bytes) {
+                           uint64_t n_bytes, bool prepend = false) {
     h->prof.reset();
     h->sstats = SortStats();
     h->last_blocks = 0;
@@ -669,7 +729,8 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     h->last_blocks = K;
     std::vector<BlockDesc> blocks(K);
     for (uint64_t b = 0; b < K; ++b)
-        blocks[b] = BlockDesc{bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1], bounds[2 * b + 3]};
+        blocks[b] = BlockDesc{bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1], bounds[2 * b + 3],
+                              std::min(b + 1, K - 1)};
     // bytes in (host input) and packing, block by block on the copy stream
     while (h->ev_packed.size() < K) {
         cudaEvent_t ev;
@@ -709,7 +770,13 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
         h->err_byte = byte;
         return SETBWTE_E_INVALID_CHAR;
     };
-    setbwte_status st = run_blocks(h, pk, blocks, validate);
+    // reverse orientation: the last block first, each one prepended to the
+    // index (its strings precede every string indexed so far)
+    std::vector<BlockDesc> order(blocks);
+    if (prepend) std::reverse(order.begin(), order.end());
+    h->prepending = prepend;
+    setbwte_status st = run_blocks(h, pk, order, validate);
+    h->prepending = false;
     // the main stream joins the copy stream (the bytes buffer is reused later)
     API_CHECK(h, cudaEventRecord(h->ev_start, h->copy_stream));
     API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
@@ -827,17 +894,17 @@ void setbwte_destroy(setbwte_t h) {
     delete h;
 }
 
-setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,
-                                     const uint64_t* d_offsets, uint64_t m) {
+static setbwte_status add_device(setbwte_t h, const uint8_t* d_strings, const uint64_t* d_offsets,
+                                 uint64_t m, bool prepend) {
     API_ENTER(h);
     if (m > 0 && !d_offsets) return SETBWTE_E_INVALID_ARG;
-    return append_impl(h, nullptr, nullptr, d_strings, d_offsets, m, ~0ull);
+    return append_impl(h, nullptr, nullptr, d_strings, d_offsets, m, ~0ull, prepend);
 }
 
-setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
-                              uint64_t m) {
+static setbwte_status add_host(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                               uint64_t m, bool prepend) {
     API_ENTER(h);
-    if (m == 0) return append_impl(h, nullptr, nullptr, nullptr, nullptr, 0, 0);
+    if (m == 0) return append_impl(h, nullptr, nullptr, nullptr, nullptr, 0, 0, prepend);
     if (!offsets) return SETBWTE_E_INVALID_ARG;
     const uint64_t nb = offsets[m];
     if (nb > 0 && !strings) return SETBWTE_E_INVALID_ARG;
@@ -850,7 +917,36 @@ setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_
     API_CHECK(h, ensure(h->in_off, m + 1, &dof));
     API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                  h->stream));
-    return append_impl(h, strings, offsets, db, dof, m, nb);
+    return append_impl(h, strings, offsets, db, dof, m, nb, prepend);
+}
+
+setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,
+                                     const uint64_t* d_offsets, uint64_t m) {
+    return add_device(h, d_strings, d_offsets, m, false);
+}
+
+setbwte_status setbwte_append(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                              uint64_t m) {
+    return add_host(h, strings, offsets, m, false);
+}
+
+setbwte_status setbwte_prepend(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
+                               uint64_t m) {
+    return add_host(h, strings, offsets, m, true);
+}
+
+setbwte_status setbwte_prepend_device(setbwte_t h, const uint8_t* d_strings,
+                                      const uint64_t* d_offsets, uint64_t m) {
+    return add_device(h, d_strings, d_offsets, m, true);
+}
+
+setbwte_status setbwte_merge(setbwte_t h, setbwte_t other) {
+    API_ENTER(h);
+    if (!other || other == h) return SETBWTE_E_INVALID_ARG;
+    if (other->failed) return SETBWTE_E_STATE;
+    if (other->device != h->device || strcmp(other->alpha, h->alpha) != 0)
+        return SETBWTE_E_UNSUPPORTED;
+    return merge_impl(h, other);
 }
 
 setbwte_status setbwte_clear(setbwte_t h) {

@@ -209,39 +209,71 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
 }
 
 // Exclusive scan of the superblock totals -> u64 superblock counters, and C.
+// One CTA: each thread owns a contiguous run of superblocks; the run totals
+// are scanned with warp shuffles (no shared-memory Hillis-Steele rounds).
 __global__ void __launch_bounds__(1024) sb_scan_kernel(const uint64_t* __restrict__ sb_tot,
                                                        uint64_t nsb, uint64_t* __restrict__ sb,
                                                        uint64_t m_new, uint64_t* __restrict__ Cd) {
-    __shared__ uint64_t part[1024][4];
-    const uint32_t tid = threadIdx.x;
+    __shared__ uint64_t wtot[32][4];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t per = (nsb + 1023) / 1024;
     const uint64_t b = tid * per, e = min(b + per, nsb);
     uint64_t acc[4] = {0, 0, 0, 0};
-    for (uint64_t i = b; i < e; ++i)
-        for (int c = 0; c < 4; ++c) acc[c] += sb_tot[i * 4 + c];
-    for (int c = 0; c < 4; ++c) part[tid][c] = acc[c];
-    __syncthreads();
-    for (uint32_t o = 1; o < 1024; o <<= 1) {
-        uint64_t v[4] = {0, 0, 0, 0};
-        if (tid >= o)
-            for (int c = 0; c < 4; ++c) v[c] = part[tid - o][c];
-        __syncthreads();
-        for (int c = 0; c < 4; ++c) part[tid][c] += v[c];
-        __syncthreads();
+    for (uint64_t i = b; i < e; ++i) {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(sb_tot + i * 4);
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(sb_tot + i * 4 + 2);
+        acc[0] += x.x;
+        acc[1] += x.y;
+        acc[2] += y.x;
+        acc[3] += y.y;
     }
-    uint64_t run[4];
-    for (int c = 0; c < 4; ++c) run[c] = tid ? part[tid - 1][c] : 0;
-    for (uint64_t i = b; i < e; ++i)
-        for (int c = 0; c < 4; ++c) {
-            sb[i * 4 + c] = run[c];
-            run[c] += sb_tot[i * 4 + c];
+    uint64_t inc[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        inc[c] = acc[c];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, inc[c], o);
+            if (lane >= (uint32_t)o) inc[c] += v;
         }
-    if (tid == 0) {
-        // C[c] = #symbols < c: all m '$' plus the smaller codes (Lemma 1)
+    }
+    if (lane == 31)
+        for (int c = 0; c < 4; ++c) wtot[warp][c] = inc[c];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint64_t x = wtot[lane][c];
+            uint64_t y = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, y, o);
+                if (lane >= (uint32_t)o) y += v;
+            }
+            wtot[lane][c] = y - x;  // exclusive over warps
+        }
+    }
+    __syncthreads();
+    uint64_t run[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) run[c] = wtot[warp][c] + inc[c] - acc[c];
+    for (uint64_t i = b; i < e; ++i) {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(sb_tot + i * 4);
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(sb_tot + i * 4 + 2);
+        *reinterpret_cast<ulonglong2*>(sb + i * 4) = make_ulonglong2(run[0], run[1]);
+        *reinterpret_cast<ulonglong2*>(sb + i * 4 + 2) = make_ulonglong2(run[2], run[3]);
+        run[0] += x.x;
+        run[1] += x.y;
+        run[2] += y.x;
+        run[3] += y.y;
+    }
+    if (tid == 1023) {
+        // C[c] = #symbols < c: all m '$' plus the smaller codes (Lemma 1);
+        // thread 1023's running counts are the totals over all superblocks
         uint64_t acc2 = m_new;
         for (int c = 0; c < 4; ++c) {
             Cd[c] = acc2;
-            acc2 += part[1023][c];
+            acc2 += run[c];
         }
         Cd[4] = acc2;  // = n (consistency)
     }

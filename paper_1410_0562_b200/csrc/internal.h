@@ -140,6 +140,13 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  int gw, int ilp);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64)
 // With sb_start != NULL also writes sb_start[0..nsb] (superblock slices of pos).
+cudaError_t launch_merge_ranks(Profiler& prof, cudaStream_t s, const Blk* oblk, const uint64_t* osb,
+                               const uint64_t* oC, uint64_t m_o, uint64_t n_o, const Blk* hblk,
+                               const uint64_t* hsb, const uint64_t* hC, uint64_t init, void* gsa,
+                               int gw);
+cudaError_t launch_merge_pos(Profiler& prof, cudaStream_t s, const Blk* oblk, uint64_t n_o,
+                             const void* gsa, void* pos, int gw, uint8_t* bint, uint64_t* sb_start,
+                             uint64_t nsb);
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,

@@ -173,4 +173,120 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// BWT merge ("the same LF/insert machinery with B_int
+// given"): the strings of a second index O are added after those of the
+// index H.  O's own BWT is B_int in O's row order; g_sa[r] (the number of
+// H-suffixes smaller than O's suffix at row r) follows from walking every
+// string of O backwards in both indexes at once (Lemma 1 P:95-100 applied
+// to O for the row and to H for the rank):
+//     r := j (row of $_j in O);  g := m_H;  g_sa[r] := g
+//     while O.B[r] != '$':  c := O.B[r];  r := C_O[c] + rank_O(c, r);
+//                           g := C_H[c] + rank_H(c, g);  g_sa[r] := g
+// Every row of O is visited once; then pos[r] = g_sa[r] + r as in Alg.1.
+template <class G>
+__global__ void __launch_bounds__(256) merge_ranks_kernel(
+    const Blk* __restrict__ oblk, const uint64_t* __restrict__ osb, const uint64_t* __restrict__ oC,
+    uint64_t m_o, const Blk* __restrict__ hblk, const uint64_t* __restrict__ hsb,
+    const uint64_t* __restrict__ hC, uint64_t init, G* __restrict__ gsa) {
+    const uint64_t hC0 = hblk ? hC[0] : 0, hC1 = hblk ? hC[1] : 0, hC2 = hblk ? hC[2] : 0,
+                   hC3 = hblk ? hC[3] : 0;
+    const uint64_t oC0 = oC[0], oC1 = oC[1], oC2 = oC[2], oC3 = oC[3];
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < m_o;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = j, g = init;
+        gsa[r] = (G)g;
+        for (;;) {
+            uint64_t w0, w1, w2, w3;
+            asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
+                : "l"(oblk + (r >> 6)));
+            const uint32_t bit = (uint32_t)(r & 63);
+            if ((w3 >> bit) & 1ull) break;  // '$': row of the string's first suffix
+            const uint32_t c = (uint32_t)((w1 >> bit) & 1ull) | ((uint32_t)((w2 >> bit) & 1ull) << 1);
+            const uint64_t ro = __ldg(osb + ((r >> kSbShift) << 2) + c) +
+                                ((w0 >> (16 * c)) & 0xFFFFull) +
+                                (uint64_t)__popcll(match_plane(c, w1, w2, w3) & ((1ull << bit) - 1ull));
+            r = (c == 0 ? oC0 : c == 1 ? oC1 : c == 2 ? oC2 : oC3) + ro;
+            g = hblk ? (c == 0 ? hC0 : c == 1 ? hC1 : c == 2 ? hC2 : hC3) + dict_rank(hblk, hsb, c, g)
+                     : 0ull;
+            gsa[r] = (G)g;
+        }
+    }
+}
+
+// pos[r] = g_sa[r] + r, B_int[r] = O.B[r] (code | '$' flag) and the superblock
+// slices of pos (as in gather_kernel).
+template <class G>
+__global__ void merge_pos_kernel(const Blk* __restrict__ oblk, uint64_t n_o, const G* __restrict__ gsa,
+                                 G* __restrict__ pos, uint8_t* __restrict__ bint,
+                                 uint64_t* __restrict__ sb_start, uint64_t nsb) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t iters = (n_o + stride - 1) / stride;
+    for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t i = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        const bool v = i < n_o;
+        uint64_t pv = 0;
+        if (v) {
+            pv = (uint64_t)__ldcs(gsa + i) + i;
+            __stcs(pos + i, (G)pv);
+            const Blk* b = oblk + (i >> 6);
+            const uint32_t bit = (uint32_t)(i & 63);
+            const uint64_t lo = __ldg(&b->lo), hi = __ldg(&b->hi), dol = __ldg(&b->dol);
+            const uint8_t sym = ((dol >> bit) & 1ull)
+                                    ? (uint8_t)4
+                                    : (uint8_t)(((lo >> bit) & 1ull) | (((hi >> bit) & 1ull) << 1));
+            bint[i] = sym;
+        }
+        uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
+        if (v) {
+            if (lane == 0 && i > 0) prev = (uint64_t)gsa[i - 1] + (i - 1);
+            const uint64_t cur = pv >> kSbShift;
+            const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
+            for (uint64_t s = first; s <= cur && s <= nsb; ++s) sb_start[s] = i;
+            if (i + 1 == n_o)
+                for (uint64_t s = cur + 1; s <= nsb; ++s) sb_start[s] = n_o;
+        }
+    }
+}
+
+cudaError_t launch_merge_ranks(Profiler& prof, cudaStream_t s, const Blk* oblk, const uint64_t* osb,
+                               const uint64_t* oC, uint64_t m_o, uint64_t n_o, const Blk* hblk,
+                               const uint64_t* hsb, const uint64_t* hC, uint64_t init, void* gsa,
+                               int gw) {
+    if (m_o == 0) return cudaSuccess;
+    // per LF step: two Blk sectors + two superblock counters + the g_sa write
+    const double bytes = (80.0 + gw) * (double)(n_o - m_o) + (double)gw * m_o;
+    const unsigned grid = grid_for(m_o, 256, 1u << 20);
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "merge_ranks", bytes, n_o - m_o,
+                  merge_ranks_kernel<uint32_t><<<grid, 256, 0, s>>>(oblk, osb, oC, m_o, hblk, hsb, hC,
+                                                                    init, (uint32_t*)gsa));
+    } else {
+        SB_LAUNCH(prof, s, "merge_ranks", bytes, n_o - m_o,
+                  merge_ranks_kernel<uint64_t><<<grid, 256, 0, s>>>(oblk, osb, oC, m_o, hblk, hsb, hC,
+                                                                    init, (uint64_t*)gsa));
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_pos(Profiler& prof, cudaStream_t s, const Blk* oblk, uint64_t n_o,
+                             const void* gsa, void* pos, int gw, uint8_t* bint, uint64_t* sb_start,
+                             uint64_t nsb) {
+    if (n_o == 0) return cudaSuccess;
+    const double bytes = (2.0 * gw + 1.0 + 0.5) * (double)n_o;
+    const unsigned grid = grid_for(n_o, 256, 148u * 64u);
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "merge_pos", bytes, n_o,
+                  merge_pos_kernel<uint32_t><<<grid, 256, 0, s>>>(oblk, n_o, (const uint32_t*)gsa,
+                                                                  (uint32_t*)pos, bint, sb_start, nsb));
+    } else {
+        SB_LAUNCH(prof, s, "merge_pos", bytes, n_o,
+                  merge_pos_kernel<uint64_t><<<grid, 256, 0, s>>>(oblk, n_o, (const uint64_t*)gsa,
+                                                                  (uint64_t*)pos, bint, sb_start, nsb));
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace setbwte

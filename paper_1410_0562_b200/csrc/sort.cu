@@ -44,8 +44,14 @@ constexpr uint32_t kChunk = 16384; // largest chunk of a digit pass
 constexpr uint32_t kMinChunk = 2048;
 constexpr uint32_t kMaxChunks = 1024;
 constexpr uint32_t kGroup = 32;    // chunks per prefix group
-constexpr int kDigNt = 512;        // digit-pass CTA
-constexpr int kDigIpt = 8;
+#ifndef SB_DIG_NT
+#define SB_DIG_NT 512
+#endif
+#ifndef SB_DIG_IPT
+#define SB_DIG_IPT 8
+#endif
+constexpr int kDigNt = SB_DIG_NT;  // digit-pass CTA
+constexpr int kDigIpt = SB_DIG_IPT;
 constexpr int kDigTile = kDigNt * kDigIpt;
 
 // BIT2..BIT16: 33..512 members whose unknown key bits fit in 16 (keys valid,
@@ -351,7 +357,10 @@ __global__ void chunkify_kernel(Lists in, SegX* __restrict__ segx, Chunk* __rest
         const uint32_t hi = (s.len + kMinChunk - 1) / kMinChunk;
         uint32_t nch = max(lo, min(hi, want));
         nch = nch > kMaxChunks ? kMaxChunks : nch;
-        const uint32_t clen = (s.len + nch - 1) / nch;
+        uint32_t clen = (s.len + nch - 1) / nch;
+        // whole scatter tiles per chunk: a ragged last tile costs a full
+        // tile's ranking and barriers (1 element per tile at 2^24/1024)
+        if (clen > (uint32_t)kDigTile) clen = (clen + kDigTile - 1) / kDigTile * kDigTile;
         nch = (s.len + clen - 1) / clen;
         const uint32_t ngr = (nch + kGroup - 1) / kGroup;
         uint32_t base = 0, gbase = 0;
@@ -551,7 +560,25 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
     }
 }
 
-__global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// A scatter tile: tile-local source pointers of one chunk.
+struct Tile {
+    uint32_t c, t0, end;  // chunk, first element, chunk end
+};
+
+__global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     Lists in, const SegX* __restrict__ segx, const Chunk* __restrict__ chunks, const uint32_t* misc,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gtot,
     const uint32_t* __restrict__ dbase, Bufs B) {
@@ -559,69 +586,116 @@ __global__ void __launch_bounds__(kDigNt) digit_scatter_kernel(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);  // NW*256
     uint2* s_kv = reinterpret_cast<uint2*>(wcnt + NW * 256);  // kDigTile (key, slot)
-    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_kv + kDigTile);  // 257
+    uint32_t* s_ink = reinterpret_cast<uint32_t*>(s_kv + kDigTile);  // kDigTile: next tile's keys
+    uint32_t* s_ins = s_ink + kDigTile;                               // kDigTile: next tile's slots
+    uint32_t* dstart = s_ins + kDigTile;                      // 257
     uint32_t* run_base = dstart + 260;                        // 256
     uint32_t* off = run_base + 256;                           // 256: run_base - dstart
     uint32_t* tmp = off + 256;                                // 32
     uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);      // 256
     const uint32_t nch = misc[M_CHUNKS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-        const Chunk ch = chunks[c];
-        if (segx[ch.seg].skip) continue;  // uniform across the CTA
-        const Seg s = in.seg[LARGE][ch.seg];
-        const uint32_t shift = meta_shift(s.meta);
+
+    // Tiles of this CTA's chunks in order; the next tile's keys (and slots)
+    // are prefetched into shared memory with cp.async while the current one
+    // is ranked.  Each thread copies exactly the elements it later reads, so
+    // the prefetch needs no barrier.
+    auto first_tile = [&](uint32_t c) -> Tile {
+        for (; c < nch; c += gridDim.x) {
+            const Chunk ch = chunks[c];
+            if (!segx[ch.seg].skip) return Tile{c, ch.begin, ch.end};
+        }
+        return Tile{nch, 0u, 0u};
+    };
+    auto next_tile = [&](const Tile& t) -> Tile {
+        if (t.t0 + kDigTile < t.end) return Tile{t.c, t.t0 + kDigTile, t.end};
+        return first_tile(t.c + gridDim.x);
+    };
+    auto prefetch = [&](const Tile& t) {
+        if (t.c >= nch) return;
+        const Seg s = in.seg[LARGE][chunks[t.c].seg];
         const uint32_t buf = meta_buf(s.meta);
-        const uint32_t* S = B.sa[buf];
-        const uint32_t* K = B.key[buf];
+        const uint32_t tn = min((uint32_t)kDigTile, t.end - t.t0);
+        const uint32_t* K = B.key[buf] + t.t0;
+        const uint32_t* S = B.sa[buf] + t.t0;
         const bool iota = meta_iota(s.meta);
+#pragma unroll
+        for (int it = 0; it < kDigIpt; ++it) {
+            const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
+            if (e < tn) {
+                cp_async4(s_ink + e, K + e);
+                if (!iota) cp_async4(s_ins + e, S + e);
+            }
+        }
+        cp_async_commit();
+    };
+
+    Tile cur = first_tile(blockIdx.x);
+    prefetch(cur);
+    uint32_t chunk_of_setup = ~0u;
+    uint32_t shift = 0, buf = 0;
+    bool iota = false;
+    while (cur.c < nch) {
+        if (cur.c != chunk_of_setup) {
+            // new chunk: the previous chunk's write-out must be done with fin/run_base
+            __syncthreads();
+            const Chunk ch = chunks[cur.c];
+            const Seg s = in.seg[LARGE][ch.seg];
+            shift = meta_shift(s.meta);
+            buf = meta_buf(s.meta);
+            iota = meta_iota(s.meta);
+            if (tid < 256) {
+                const uint32_t db = dbase[(size_t)ch.seg * 256 + tid];
+                run_base[tid] = (db & 0x7FFFFFFFu) + gtot[(size_t)ch.group * 256 + tid] +
+                                hist[(size_t)cur.c * 256 + tid];
+                fin[tid] = (uint8_t)(db >> 31);
+            }
+            chunk_of_setup = cur.c;
+        }
         uint32_t* S2 = B.sa[1 - buf];
         uint32_t* K2 = B.key[1 - buf];
-        if (tid < 256) {
-            const uint32_t db = dbase[(size_t)ch.seg * 256 + tid];
-            run_base[tid] = (db & 0x7FFFFFFFu) + gtot[(size_t)ch.group * 256 + tid] +
-                            hist[(size_t)c * 256 + tid];
-            fin[tid] = (uint8_t)(db >> 31);
+        const uint32_t t0 = cur.t0;
+        const uint32_t tn = min((uint32_t)kDigTile, cur.end - t0);
+        uint32_t key[kDigIpt], slot[kDigIpt], dig[kDigIpt], dest[kDigIpt];
+        cp_async_wait_all();
+#pragma unroll
+        for (int it = 0; it < kDigIpt; ++it) {
+            const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
+            const bool valid = e < tn;
+            key[it] = valid ? s_ink[e] : 0u;
+            slot[it] = valid ? (iota ? t0 + e : s_ins[e]) : 0u;
+            dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
         }
-        for (uint32_t t0 = ch.begin; t0 < ch.end; t0 += kDigTile) {
-            const uint32_t tn = min((uint32_t)kDigTile, ch.end - t0);
-            uint32_t key[kDigIpt], slot[kDigIpt], dig[kDigIpt], dest[kDigIpt];
+        cur = next_tile(cur);
+        prefetch(cur);
+        block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
+        if (tid < 256) {
+            off[tid] = run_base[tid] - dstart[tid];  // mod 2^32
+            run_base[tid] += dstart[tid + 1] - dstart[tid];
+        }
 #pragma unroll
-            for (int it = 0; it < kDigIpt; ++it) {
-                const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
-                const bool valid = e < tn;
-                key[it] = valid ? __ldcs(K + t0 + e) : 0u;
-                slot[it] = valid ? (iota ? t0 + e : __ldcs(S + t0 + e)) : 0u;
-                dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
+        for (int it = 0; it < kDigIpt; ++it)
+            if (dig[it] < 256) s_kv[dest[it]] = make_uint2(key[it], slot[it]);
+        __syncthreads();
+        // coalesced write-out: consecutive tile positions of one digit go to
+        // consecutive global positions.  The next tile's block_rank barriers
+        // order this loop's shared reads before their overwrite.
+        for (uint32_t i = tid; i < tn; i += kDigNt) {
+            const uint2 kv = s_kv[i];
+            const uint32_t d = (kv.x >> shift) & 0xFFu;
+            const uint32_t gp = off[d] + i;
+            if (fin[d]) {
+                __stcs(B.saf + gp, kv.y);
+            } else {
+                __stcs(S2 + gp, kv.y);
+                __stcs(K2 + gp, kv.x);
             }
-            block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
-            if (tid < 256) off[tid] = run_base[tid] - dstart[tid];  // mod 2^32
-#pragma unroll
-            for (int it = 0; it < kDigIpt; ++it)
-                if (dig[it] < 256) s_kv[dest[it]] = make_uint2(key[it], slot[it]);
-            __syncthreads();
-            // coalesced write-out: consecutive tile positions of one digit go to
-            // consecutive global positions
-            for (uint32_t i = tid; i < tn; i += kDigNt) {
-                const uint2 kv = s_kv[i];
-                const uint32_t d = (kv.x >> shift) & 0xFFu;
-                const uint32_t gp = off[d] + i;
-                if (fin[d]) {
-                    __stcs(B.saf + gp, kv.y);
-                } else {
-                    __stcs(S2 + gp, kv.y);
-                    __stcs(K2 + gp, kv.x);
-                }
-            }
-            __syncthreads();
-            if (tid < 256) run_base[tid] += dstart[tid + 1] - dstart[tid];
-            __syncthreads();
         }
     }
 }
 
 constexpr size_t scatter_smem() {
-    return (size_t)(kDigNt / 32) * 256 * 4 + 2 * (size_t)kDigTile * 4 + 260 * 4 + 2 * 256 * 4 +
+    return (size_t)(kDigNt / 32) * 256 * 4 + 4 * (size_t)kDigTile * 4 + 260 * 4 + 2 * 256 * 4 +
            32 * 4 + 256 + 16;
 }
 
@@ -1281,8 +1355,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                                                                                   slot_base, n_suf,
                                                                                   k0));
     SB_CHECK(cudaGetLastError());
-    SB_LAUNCH(prof, s, "sort_init", 4.0 * n, n,
-              init_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc));
+    SB_LAUNCH(prof, s, "sort_init", n <= kCapM ? 4.0 * n : 0.0, n,
+              init_kernel<<<n <= kCapM ? grid_for(n, 256) : 1u, 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc));
     SB_CHECK(cudaGetLastError());
     uint32_t h_cnt[NCLASS] = {0};
     if (n > 1) h_cnt[class_of(Seg{0u, (uint32_t)n, 0u, 24u | (1u << 9)})] = 1;

@@ -360,3 +360,108 @@ def test_fm_count_c1_and_host_tier(SetBWTE, c1):
         idx.set_option("hbm_budget_bytes", budget)
         idx.append(d, o)
         assert np.array_equal(idx.count(pats), want)
+
+
+# --- reverse orientation and BWT merge (NEXT-4) ------------------------
+
+def _split(d, o, cut):
+    o = np.asarray(o, dtype=np.uint64)
+    a_d, a_o = d[: int(o[cut])], o[: cut + 1]
+    b_d, b_o = d[int(o[cut]):], o[cut:] - o[cut]
+    return (a_d, a_o), (b_d, b_o)
+
+
+def test_prepend_golden(SetBWTE):
+    idx = SetBWTE(A)
+    idx.append_strings(["GG", "", "AC"])
+    idx.prepend_strings(["ACGT", "CA"])
+    assert idx.bwt().decode() == TWO["one_shot_bwt"]
+    idx = SetBWTE(A)
+    idx.prepend_strings(["G"])
+    idx.prepend_strings(["AC"])
+    assert idx.bwt().decode() == "CG$A$"
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_prepend_random_vs_oracle(SetBWTE, seed):
+    d, o = synth.random_set(9000 + seed, max_m=48, max_len=40, alphabet=["ACGT", "AC"][seed % 2])
+    m = len(o) - 1
+    rng = np.random.default_rng(seed)
+    c1, c2 = sorted(rng.integers(0, m + 1, size=2).tolist())
+    (x_d, x_o), (yz_d, yz_o) = _split(d, o, c1)
+    (y_d, y_o), (z_d, z_o) = _split(yz_d, yz_o, c2 - c1)
+    idx = SetBWTE(A, block_suffixes=int(rng.integers(20, 300)))
+    idx.append(y_d, y_o)      # Y
+    idx.prepend(x_d, x_o)     # X Y
+    idx.append(z_d, z_o)      # X Y Z
+    assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+def test_prepend_device_c1(SetBWTE, c1):
+    import torch
+    d, o, want = c1
+    (a_d, a_o), (b_d, b_o) = _split(d, o, 400)
+    idx = SetBWTE(A, block_suffixes=25250)
+    idx.append(b_d, b_o)
+    idx.prepend_device(torch.from_numpy(np.ascontiguousarray(a_d)).cuda(),
+                       torch.from_numpy(np.ascontiguousarray(a_o).view(np.int64)).cuda())
+    assert idx.bwt() == want
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_merge_random_vs_oracle(SetBWTE, seed):
+    d, o = synth.random_set(9500 + seed, max_m=48, max_len=40, alphabet=["ACGT", "GT"][seed % 2])
+    m = len(o) - 1
+    rng = np.random.default_rng(seed)
+    cut = int(rng.integers(0, m + 1))
+    (a_d, a_o), (b_d, b_o) = _split(d, o, cut)
+    h = SetBWTE(A, block_suffixes=int(rng.integers(20, 300)))
+    h.append(a_d, a_o)
+    other = SetBWTE(A, block_suffixes=int(rng.integers(20, 300)))
+    other.append(b_d, b_o)
+    before = other.bwt()
+    h.merge(other)
+    assert h.bwt() == oracle.bwt(A, d, o)
+    assert other.bwt() == before == oracle.bwt(A, b_d, b_o)
+    assert h.size() == (int(o[-1]) + m, m)
+
+
+@pytest.mark.parametrize("budget", [1 << 40, 1])
+def test_merge_c1_and_host_tier(SetBWTE, c1, budget):
+    d, o, want = c1
+    (a_d, a_o), (b_d, b_o) = _split(d, o, 600)
+    h = SetBWTE(A, block_suffixes=25250)
+    h.set_option("hbm_budget_bytes", budget)
+    h.append(a_d, a_o)
+    other = SetBWTE(A, block_suffixes=10000)
+    other.set_option("hbm_budget_bytes", budget)
+    other.append(b_d, b_o)
+    h.merge(other)
+    assert h.bwt() == want
+    # queries on the merged index
+    rng = np.random.default_rng(1)
+    starts = rng.integers(0, len(d) - 12, size=50)
+    pats = [bytes(d[a:a + 6]).decode() for a in starts]
+    assert np.array_equal(h.count(pats), oracle.count(A, d, o, pats))
+
+
+def test_merge_edge_cases(SetBWTE):
+    empty = SetBWTE(A)
+    h = SetBWTE(A)
+    h.append_strings(["AC", "G"])
+    h.merge(empty)
+    assert h.bwt().decode() == "CG$A$"
+    e2 = SetBWTE(A)
+    e2.merge(h)
+    assert e2.bwt().decode() == "CG$A$"
+    e3 = SetBWTE(A)
+    e3.append_strings(["", ""])
+    e3.merge(h)   # {"","","AC","G"}
+    d, o = synth.from_strings(["", "", "AC", "G"])
+    assert e3.bwt() == oracle.bwt(A, d, o)
+    with pytest.raises(Exception):
+        h.merge(h)
+    other = SetBWTE("AC")
+    other.append_strings(["AC"])
+    with pytest.raises(Exception):
+        h.merge(other)
