@@ -1116,6 +1116,7 @@ setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const u
                                (uint32_t)n_suf, pos, 8, bint));
     API_CHECK(h, launch_bint_ascii(h->prof, h->stream, bint, (uint32_t)n_suf,
                                    (const uint8_t*)h->d_sym.p, asc));
+    API_CHECK(h, launch_strip_payload(h->stream, saf, (uint32_t)n_suf));
     if (sa_out)
         API_CHECK(h, cudaMemcpyAsync(sa_out, saf, n_suf * 4, cudaMemcpyDeviceToHost, h->stream));
     if (bint_out)

@@ -127,6 +127,18 @@ struct SortStats {
     std::vector<uint64_t> active_per_pass;  // elements entering each digit pass
 };
 cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf);
+// SA payload: while a block has fewer than 2^29 suffixes, every SA entry the
+// sort moves is (slot | b << 29) with b = the block's B_int symbol of that
+// suffix (2-bit code, or 4 for '$', Alg.1), attached when the slot is
+// generated.  The gather then reads B_int with the SA entry instead of two
+// random text lookups.
+constexpr uint32_t kPayloadShift = 29;
+__host__ __device__ inline bool sa_payload(uint64_t n_suf) { return n_suf < (1ull << kPayloadShift); }
+__host__ __device__ inline uint32_t sa_slot_mask(uint64_t n_suf) {
+    return sa_payload(n_suf) ? (1u << kPayloadShift) - 1u : 0xFFFFFFFFu;
+}
+cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n);
+
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
                        uint32_t* d_sa_final, SortStats* st, bool reserve_only = false);

@@ -117,6 +117,7 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
                               const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
                               uint8_t* __restrict__ bint, uint64_t* __restrict__ sb_start,
                               uint64_t nsb) {
+    const uint32_t smask = sa_slot_mask(n_suf);
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t iters = (n_suf + stride - 1) / stride;  // warp-uniform trip count
@@ -126,20 +127,25 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
         uint64_t pv = 0;
         if (v) {
             // streaming (evict-first) SA / pos / B_int accesses leave L2 to g
-            const uint32_t sl = __ldcs(sa + i);
-            const uint64_t p = slot_base + sl;
+            const uint32_t e = __ldcs(sa + i);
+            const uint32_t sl = e & smask;
             pv = (g ? (uint64_t)__ldg(g + sl) : 0ull) + i;
             __stcs(pos + i, (G)pv);
             uint8_t b;
-            if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
-            else b = (uint8_t)text_sym(text, p - 1);
+            if (smask != 0xFFFFFFFFu) {
+                b = (uint8_t)(e >> kPayloadShift);  // B_int carried by the SA entry
+            } else {
+                const uint64_t p = slot_base + sl;
+                if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
+                else b = (uint8_t)text_sym(text, p - 1);
+            }
             __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
         }
         if (sb_start) {
             uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
             if (v) {
                 if (lane == 0 && i > 0) {
-                    const uint32_t sl1 = sa[i - 1];
+                    const uint32_t sl1 = sa[i - 1] & smask;
                     prev = (g ? (uint64_t)__ldg(g + sl1) : 0ull) + (i - 1);
                 }
                 const uint64_t cur = pv >> kSbShift;

@@ -84,7 +84,17 @@ struct Bufs {
     const uint32_t* text;
     const uint32_t* term;
     uint64_t base;
+    uint32_t smask;  // slot bits of an SA entry (sa_slot_mask); ~0 without payload
 };
+
+// SA entry of block-local slot sl: the slot plus, with payload, its B_int
+// symbol (the symbol before the suffix, or 4 = '$' at a string start).
+__device__ __forceinline__ uint32_t sa_entry(const Bufs& B, uint32_t sl) {
+    if (B.smask == 0xFFFFFFFFu) return sl;
+    const uint64_t p = B.base + sl;
+    const uint32_t b = (sl == 0 || term_bit(B.term, p - 1)) ? 4u : text_sym(B.text, p - 1);
+    return sl | (b << kPayloadShift);
+}
 
 __device__ __forceinline__ uint32_t meta_shift(uint32_t m) { return m & 0xFF; }
 __device__ __forceinline__ uint32_t meta_buf(uint32_t m) { return (m >> 8) & 1; }
@@ -149,7 +159,7 @@ __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint3
     uint32_t group = group0;
     for (;;) {
         uint32_t key = 0;
-        if (active) key = have_key ? key0 : suffix_key(B.text, B.term, B.base + slot, word);
+        if (active) key = have_key ? key0 : suffix_key(B.text, B.term, B.base + (slot & B.smask), word);
         have_key = false;
         unsigned long long comp;
         if (!valid) comp = ~0ull;
@@ -312,13 +322,13 @@ __global__ void keygen_kernel(const uint32_t* __restrict__ text, const uint32_t*
 // init / control
 // ---------------------------------------------------------------------------
 __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ saf, uint32_t n,
-                            Lists in, Lists out, uint32_t* misc) {
+                            Lists in, Lists out, uint32_t* misc, Bufs B) {
     // a LARGE first segment reads its slots as "iota" (meta bit) and never
     // needs them materialised; smaller blocks go straight to the segment sorts
     if (n <= kCapM) {
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
              i += (uint64_t)gridDim.x * blockDim.x)
-            sa0[i] = (uint32_t)i;
+            sa0[i] = sa_entry(B, (uint32_t)i);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         for (int c = 0; c < NCLASS; ++c) {
@@ -326,7 +336,7 @@ __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ s
             out.cnt[c] = 0;
         }
         for (int c = 0; c < M_N; ++c) misc[c] = 0;
-        if (n == 1) saf[0] = 0;
+        if (n == 1) saf[0] = sa_entry(B, 0u);
         else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 1, n > kCapM ? 1u : 0u)});
     }
 }
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
                     key[u] = 0;
                     if (p < ch.end) {
                         const uint32_t sl = meta_iota(s.meta) ? p : __ldg(S + p);
-                        key[u] = suffix_key(B.text, B.term, B.base + sl, s.word);
+                        key[u] = suffix_key(B.text, B.term, B.base + (sl & B.smask), s.word);
                         K[p] = key[u];
                     }
                 }
@@ -633,7 +643,7 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     Tile cur = first_tile(blockIdx.x);
     prefetch(cur);
     uint32_t chunk_of_setup = ~0u;
-    uint32_t shift = 0, buf = 0;
+    uint32_t shift = 0, buf = 0, word_of_setup = 0;
     bool iota = false;
     while (cur.c < nch) {
         if (cur.c != chunk_of_setup) {
@@ -644,6 +654,7 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             shift = meta_shift(s.meta);
             buf = meta_buf(s.meta);
             iota = meta_iota(s.meta);
+            word_of_setup = s.word;
             if (tid < 256) {
                 const uint32_t db = dbase[(size_t)ch.seg * 256 + tid];
                 run_base[tid] = (db & 0x7FFFFFFFu) + gtot[(size_t)ch.group * 256 + tid] +
@@ -665,6 +676,31 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             key[it] = valid ? s_ink[e] : 0u;
             slot[it] = valid ? (iota ? t0 + e : s_ins[e]) : 0u;
             dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
+        }
+        if (iota && B.smask != 0xFFFFFFFFu) {
+            // generated slots get their B_int payload.  On key word 0 the
+            // symbol before slot s is the top symbol of slot s-1's key and a
+            // clamp of 0 marks s-1 as a terminator: the previous element's key
+            // comes from the neighbouring lane (or the warp's previous tile
+            // element), no text lookups.
+            if (word_of_setup == 0) {
+                const uint32_t e0 = warp * (32 * kDigIpt);
+                uint32_t carry = 0;
+                if (lane == 0 && e0 < tn && t0 + e0 > 0) carry = B.key[buf][t0 + e0 - 1];
+#pragma unroll
+                for (int it = 0; it < kDigIpt; ++it) {
+                    const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, key[it], 1);
+                    const uint32_t last = __shfl_sync(0xFFFFFFFFu, key[it], 31);
+                    const uint32_t pk = lane == 0 ? carry : up;
+                    carry = last;
+                    const uint32_t sl = slot[it];
+                    const uint32_t b = (sl == 0 || (pk & 15u) == 0) ? 4u : (pk >> 30);
+                    slot[it] = sl | (b << kPayloadShift);
+                }
+            } else {
+#pragma unroll
+                for (int it = 0; it < kDigIpt; ++it) slot[it] = sa_entry(B, slot[it]);
+            }
         }
         cur = next_tile(cur);
         prefetch(cur);
@@ -985,7 +1021,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
             if ((uint32_t)it < nit && e < L) {
                 slot[it] = S[s.start + e];
                 key[it] = kv ? B.key[bid][s.start + e]
-                             : suffix_key(B.text, B.term, B.base + slot[it], s.word);
+                             : suffix_key(B.text, B.term, B.base + (slot[it] & B.smask), s.word);
             }
         }
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1181,7 +1217,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
         for (uint32_t i = tid; i < len; i += NT) {
             const uint32_t sl = S[s.start + i];
             slotA[i] = sl;
-            keyA[i] = kv ? B.key[buf][s.start + i] : suffix_key(B.text, B.term, B.base + sl, s.word);
+            keyA[i] = kv ? B.key[buf][s.start + i] : suffix_key(B.text, B.term, B.base + (sl & B.smask), s.word);
         }
         __syncthreads();
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1270,6 +1306,11 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
     }
 }
 
+__global__ void strip_payload_kernel(uint32_t* sa, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        sa[i] &= (1u << kPayloadShift) - 1u;
+}
+
 }  // namespace sortk
 
 using namespace sortk;
@@ -1335,6 +1376,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.text = text;
     B.term = term;
     B.base = slot_base;
+    B.smask = sa_slot_mask(n_suf);
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
@@ -1356,7 +1398,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                                                                                   k0));
     SB_CHECK(cudaGetLastError());
     SB_LAUNCH(prof, s, "sort_init", n <= kCapM ? 4.0 * n : 0.0, n,
-              init_kernel<<<n <= kCapM ? grid_for(n, 256) : 1u, 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc));
+              init_kernel<<<n <= kCapM ? grid_for(n, 256) : 1u, 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc, B));
     SB_CHECK(cudaGetLastError());
     uint32_t h_cnt[NCLASS] = {0};
     if (n > 1) h_cnt[class_of(Seg{0u, (uint32_t)n, 0u, 24u | (1u << 9)})] = 1;
@@ -1465,6 +1507,12 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     prof.add_bytes("sort_medium", 12.0 * h_misc[M_ELEMS_M], h_misc[M_ELEMS_M]);
     prof.add_bytes("sort_bitonic", 12.0 * h_misc[M_ELEMS_B], h_misc[M_ELEMS_B]);
     return cudaSuccess;
+}
+
+cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n) {
+    if (n == 0 || !sa_payload(n)) return cudaSuccess;
+    sortk::strip_payload_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa, n);
+    return cudaGetLastError();
 }
 
 }  // namespace setbwte

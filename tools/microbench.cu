@@ -156,6 +156,18 @@ int main() {
         });
         printf("  \"gather32_l2_48MiB_gsectors_s\": %.2f, \"gather32_l2_48MiB_gbs\": %.1f,\n",
                q / gl / 1e6, 32.0 * q / gl / 1e6);
+        // random 4-byte loads over growing footprints: where random reads stop
+        // hitting L2 (the gather's g array is 4 B x block suffixes)
+        printf("  \"gather4_by_footprint_gloads_s\": {");
+        const int mbs[] = {16, 32, 48, 64, 80, 96, 112, 128, 256};
+        for (int k = 0; k < 9; ++k) {
+            const uint64_t n4 = ((uint64_t)mbs[k] << 20) / 4;
+            const float t = best_of(10, [&] {
+                gather4_kernel<<<grid * 4, nt>>>(reinterpret_cast<const uint32_t*>(a), n4, q, 17 + k, sink);
+            });
+            printf("%s\"%d\": %.1f", k ? ", " : "", mbs[k], q / t / 1e6);
+        }
+        printf("},\n");
         CK(cudaFree(a));
     }
     {  // atomics into 2^24 counters (64 MiB, L2-resident)
