@@ -104,7 +104,9 @@ __device__ __forceinline__ void merge_word(uint32_t (&oo)[2][3], uint64_t xl, ui
     }
 }
 
-constexpr uint32_t kStage = 16384;  // inserted entries staged in shared memory per superblock
+// inserted entries staged in shared memory per superblock (dynamic shared
+// memory): enough for a block that adds up to ~60 % new symbols
+constexpr uint32_t kStage = 40960;
 
 template <class G>
 __global__ void __launch_bounds__(kInsNt) insert_kernel(
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
     // in_blk / out_blk are indexed by absolute Blk number; the host-tier path
     // passes pointers biased by its staging window (only the window is touched)
     __shared__ uint32_t wcnt[kBlkPerSb];
-    __shared__ uint16_t ent[kStage];  // (offset in word) | (B_int code+$ << 6)
+    extern __shared__ uint16_t ent[];  // kStage: (offset in word) | (B_int code+$ << 6)
     __shared__ uint32_t wsum[4][kInsWarps];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint64_t sbi = sb_begin + blockIdx.x; sbi < sb_end; sbi += gridDim.x) {
@@ -124,11 +126,24 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
         __syncthreads();
         const uint64_t i_lo = sb_start[sbi], i_hi = sb_start[sbi + 1];
         const bool staged = i_hi - i_lo <= kStage;
-        // pass 1 (coalesced): inserted symbols per output word, staged entries
-        for (uint64_t i = i_lo + tid; i < i_hi; i += kInsNt) {
-            const uint32_t rel = (uint32_t)((uint64_t)__ldg(pos + i) - o0);
-            atomicAdd(&wcnt[rel >> 6], 1u);
-            if (staged) ent[i - i_lo] = (uint16_t)((rel & 63u) | ((uint32_t)__ldg(bint + i) << 6));
+        // pass 1 (coalesced): inserted symbols per output word, staged entries;
+        // four independent loads in flight per thread
+        for (uint64_t i0 = i_lo + tid; i0 < i_hi; i0 += 4 * kInsNt) {
+            uint32_t rel[4], bb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t i = i0 + (uint64_t)u * kInsNt;
+                rel[u] = i < i_hi ? (uint32_t)((uint64_t)__ldg(pos + i) - o0) : 0u;
+                bb[u] = (i < i_hi && staged) ? (uint32_t)__ldg(bint + i) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t i = i0 + (uint64_t)u * kInsNt;
+                if (i < i_hi) {
+                    atomicAdd(&wcnt[rel[u] >> 6], 1u);
+                    if (staged) ent[i - i_lo] = (uint16_t)((rel[u] & 63u) | (bb[u] << 6));
+                }
+            }
         }
         __syncthreads();
         // exclusive scan over the 1024 words (two-level)
@@ -168,14 +183,34 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
             // merge one 32-symbol half at a time: all shifts stay 32-bit
             const uint64_t span = n_out - ow0;
             const uint32_t lim = span >= 64 ? 64u : (uint32_t)span;
-            uint32_t oo[2][3];
-            if (staged)
-                merge_word<true, G>(oo, xl, xh, xd, lim, cnt, ent + arel, pos, bint, a, ow0);
-            else
-                merge_word<false, G>(oo, xl, xh, xd, lim, cnt, ent, pos, bint, a, ow0);
-            ol = (uint64_t)oo[0][0] | ((uint64_t)oo[1][0] << 32);
-            oh = (uint64_t)oo[0][1] | ((uint64_t)oo[1][1] << 32);
-            od = (uint64_t)oo[0][2] | ((uint64_t)oo[1][2] << 32);
+            if (cnt == 64 && (a & 15) == 0) {
+                // every symbol of the word is inserted (e.g. the first block):
+                // its planes are B_int[a .. a+64) bit-sliced, 8 bytes at a time
+                const uint4* src = reinterpret_cast<const uint4*>(bint + a);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 v = __ldg(src + q);
+                    const uint64_t w2[2] = {((uint64_t)v.y << 32) | v.x, ((uint64_t)v.w << 32) | v.z};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t sh8 = 16 * q + 8 * h;
+                        // bit k of byte j -> bit j (the "multiply gather" of 8 flag bits)
+                        const uint64_t m = 0x0101010101010101ull, mul = 0x0102040810204080ull;
+                        ol |= (((w2[h] & m) * mul) >> 56) << sh8;
+                        oh |= ((((w2[h] >> 1) & m) * mul) >> 56) << sh8;
+                        od |= ((((w2[h] >> 2) & m) * mul) >> 56) << sh8;
+                    }
+                }
+            } else {
+                uint32_t oo[2][3];
+                if (staged)
+                    merge_word<true, G>(oo, xl, xh, xd, lim, cnt, ent + arel, pos, bint, a, ow0);
+                else
+                    merge_word<false, G>(oo, xl, xh, xd, lim, cnt, ent, pos, bint, a, ow0);
+                ol = (uint64_t)oo[0][0] | ((uint64_t)oo[1][0] << 32);
+                oh = (uint64_t)oo[0][1] | ((uint64_t)oo[1][1] << 32);
+                od = (uint64_t)oo[0][2] | ((uint64_t)oo[1][2] << 32);
+            }
             const uint64_t V = lim == 64 ? ~0ull : ((1ull << lim) - 1ull);  // real positions
 #pragma unroll
             for (int c = 0; c < 4; ++c) c4[c] = __popcll(match_plane(c, ol, oh, od) & V);
@@ -291,15 +326,19 @@ cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Blk* in_bl
     const double frac = (double)nsb_r / (double)((n_out >> kSbShift) + 1);
     const double bytes = frac * (0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins);
     const unsigned grid = (unsigned)(nsb_r < 148u * 64u ? nsb_r : 148u * 64u);
+    SB_CHECK(cudaFuncSetAttribute(insert_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kStage * 2)));
+    SB_CHECK(cudaFuncSetAttribute(insert_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kStage * 2)));
     if (gw == 4) {
         SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
-                  insert_kernel<uint32_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint32_t*)pos,
+                  insert_kernel<uint32_t><<<grid, kInsNt, kStage * 2, s>>>(in_blk, n_in, (const uint32_t*)pos,
                                                                    bint, n_ins, out_blk, n_out,
                                                                    sb_tot, sb_start, sb_begin,
                                                                    sb_end));
     } else {
         SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
-                  insert_kernel<uint64_t><<<grid, kInsNt, 0, s>>>(in_blk, n_in, (const uint64_t*)pos,
+                  insert_kernel<uint64_t><<<grid, kInsNt, kStage * 2, s>>>(in_blk, n_in, (const uint64_t*)pos,
                                                                    bint, n_ins, out_blk, n_out,
                                                                    sb_tot, sb_start, sb_begin,
                                                                    sb_end));
