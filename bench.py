@@ -370,9 +370,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if os.path.exists(tr_path):
         ent = json.load(open(tr_path)).get(dname)
         if ent:
-            traffic = ent.get("dram_bytes_per_launch")
-            traffic_note = {"algorithmic_bytes": ent.get("algorithmic_bytes_per_launch"),
-                            "launch": ent.get("launch")}
+            # the captured launch's DRAM bytes, scaled to this run's average
+            # launch by the ratio of algorithmic bytes (the capture is one
+            # full-size launch; the average mixes full and partial passes)
+            dram = ent.get("dram_bytes_per_launch")
+            alg = ent.get("algorithmic_bytes_per_launch")
+            traffic = round(dram * per_launch_bytes / alg, 1) if dram and alg else dram
+            traffic_note = {"captured_dram_bytes": dram, "captured_algorithmic_bytes": alg,
+                            "launch": ent.get("launch"),
+                            "scaled": bool(dram and alg)}
     roof = {"kernel": dname, "bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
             "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,

@@ -195,7 +195,13 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     <= 3 n log(sigma) bits of system
  *                     memory) and Insert rewrites it in place through HBM
  *                     staging.  Default: unlimited.
- *   "host_tier"       1: move B_ext to the host tier now (and keep it there). */
+ *   "host_tier"       1: move B_ext to the host tier now (and keep it there).
+ *   "insert_split"    1: with setbwte_set_partition world > 1 and B_ext in HBM,
+ *                     Insert is split by output range (rank r merges output
+ *                     superblocks [nsb*r/P, nsb*(r+1)/P)) and the new
+ *                     dictionary's Blk slices and superblock totals are
+ *                     all-gathered through the same callback;
+ *                     0 (default): every rank runs the whole Insert. */
 setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value);
 
 /* Kernel timing for setbwte_stats: mode 0 = off, 1 = every launch, 2 = only
@@ -214,7 +220,10 @@ setbwte_status setbwte_set_stream(setbwte_t h, void* cuda_stream);
  * stream, ctx): buf is a DEVICE buffer holding the concatenation of all
  * ranks' slices; this rank's slice is already filled; on return (work queued
  * on `stream` is allowed) every slice must be filled.  bytes_per_rank has
- * `world` entries.  world == 1 (the default) disables the exchange. */
+ * `world` entries.  world == 1 (the default) disables the exchange.  With
+ * option "insert_split" the callback is also used, twice per block, for the
+ * new B_ext dictionary (32-byte Blks) and its superblock totals (32 bytes per
+ * 2^16 symbols).  A non-zero return makes the append fail (SETBWTE_E_STATE). */
 typedef int (*setbwte_allgather_fn)(void* buf, const uint64_t* bytes_per_rank, int world,
                                     void* stream, void* ctx);
 setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,

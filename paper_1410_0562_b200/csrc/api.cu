@@ -171,8 +171,9 @@ struct setbwte_s {
     // every string already indexed, so a new terminator is the smallest suffix
     bool prepending = false;
 
-    // data-parallel ComputeRanks
+    // data-parallel ComputeRanks (and, with insert_split, Insert by output range)
     int rank = 0, world = 1;
+    bool insert_split = false;
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
 
@@ -415,6 +416,29 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
     if (h->host_tier) {
         setbwte_status st = host_insert(h, pos, gw, bint, n_ins, ib.osb, ib.tot, ib.sb_start, m_new);
         if (st != SETBWTE_OK) return st;
+    } else if (h->world > 1 && h->insert_split && h->allgather) {
+        // Insert split by output range: rank r merges output
+        // superblocks [nsb*r/P, nsb*(r+1)/P) only; the new dictionary's Blks and
+        // the superblock totals are then all-gathered (slices in rank order),
+        // and every rank scans the totals itself.
+        const uint64_t n_out = h->n + n_ins;
+        const uint64_t nblk = (n_out >> 6) + 1;
+        const uint64_t P = (uint64_t)h->world;
+        std::vector<uint64_t> blk_bytes(P), tot_bytes(P);
+        for (uint64_t r = 0; r < P; ++r) {
+            const uint64_t a = ib.nsb * r / P, b = ib.nsb * (r + 1) / P;
+            const uint64_t ba = std::min(a * kBlkPerSb, nblk), bb = std::min(b * kBlkPerSb, nblk);
+            blk_bytes[r] = (bb - ba) * sizeof(Blk);
+            tot_bytes[r] = (b - a) * 4 * sizeof(uint64_t);
+        }
+        const uint64_t a = ib.nsb * h->rank / P, b = ib.nsb * (h->rank + 1) / P;
+        API_CHECK(h, launch_insert_range(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_ins,
+                                         ib.ob, ib.tot, ib.sb_start, a, b));
+        if (h->allgather(ib.ob, blk_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx) ||
+            h->allgather(ib.tot, tot_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
+            return SETBWTE_E_STATE;
+        API_CHECK(h, launch_sb_scan(h->prof, h->stream, ib.tot, ib.nsb, ib.osb, m_new,
+                                    (uint64_t*)h->d_C.p));
     } else {
         API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_ins, ib.ob,
                                    ib.osb, ib.tot, ib.sb_start, m_new, (uint64_t*)h->d_C.p));
@@ -533,6 +557,26 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         lanes[l].ev_sorted = h->ev_sorted[l];
         lanes[l].prof.on = h->prof.on;
         lanes[l].prof.only = h->prof.only;
+    }
+    if (h->sort_lanes == 0) {
+        // no pipelining: every stage of every block in order on the calling
+        // thread and the main stream (what per-launch profiling needs: no
+        // other thread can enqueue between a launch and its events)
+        for (size_t k = 0; k < K; ++k) {
+            API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_packed[blocks[k].ev], 0));
+            if (k == 0) {
+                setbwte_status st0 = validate();
+                if (st0 != SETBWTE_OK) return st0;
+            }
+            API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, blocks[k].S0,
+                                    (uint32_t)(blocks[k].S1 - blocks[k].S0), saf2, &h->sstats));
+            setbwte_status st1 = rank_insert_stage(h, pk, blocks[k], saf2);
+            if (st1 != SETBWTE_OK) {
+                if (k > 0) h->failed = true;
+                return st1;
+            }
+        }
+        return SETBWTE_OK;
     }
     // the sort lanes start after everything queued on the main stream so far
     API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
@@ -1177,6 +1221,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "hbm_budget_bytes")) {
         if (value < 1) return SETBWTE_E_INVALID_ARG;
         h->hbm_budget = value;
+    } else if (!strcmp(key, "insert_split")) {
+        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        h->insert_split = value != 0;
     } else if (!strcmp(key, "sort_lanes")) {
         if (value > 2) return SETBWTE_E_INVALID_ARG;
         h->sort_lanes = (int)value;

@@ -981,13 +981,80 @@ __global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists 
             v[r] = e < L ? (((__ldg(K + s.start + e) & rmask) << IDXB) | e) : 0xFFFFFFFFu;
         }
         warp_bitonic<NIT>(v);
+        // sorted order is lane-major (element e = lane*NIT + r); ties on this
+        // word (equal keys with 14 real symbols) are found in registers
+        uint32_t* sl32 = reinterpret_cast<uint32_t*>(buf);  // N slots in sorted order
+        uint32_t* tl = sl32 + N;                            // compacted tie list
+        uint32_t k16[NIT];
 #pragma unroll
         for (int r = 0; r < NIT; ++r) {
             const uint32_t e = lane * NIT + r;
-            if (e < L) buf[e] = make_uint2(top | (v[r] >> IDXB), __ldg(S + s.start + (v[r] & (N - 1))));
+            k16[r] = v[r] >> IDXB;
+            if (e < L) sl32[e] = __ldg(S + s.start + (v[r] & (N - 1)));
         }
+        const uint32_t nxt0 = __shfl_down_sync(0xFFFFFFFFu, k16[0], 1);
+        uint32_t eqn = 0;  // bit r: element e ties with e+1
+#pragma unroll
+        for (int r = 0; r < NIT; ++r) {
+            const uint32_t e = lane * NIT + r;
+            const uint32_t nk = r + 1 < NIT ? k16[r + 1] : nxt0;
+            if (e + 1 < L && nk == k16[r] && (k16[r] & 15u) == (uint32_t)kKeySyms) eqn |= 1u << r;
+        }
+        const uint32_t lastn = __shfl_up_sync(0xFFFFFFFFu, eqn >> (NIT - 1), 1) & (lane > 0 ? 1u : 0u);
+        const uint32_t eqp = ((eqn << 1) | lastn) & ((1u << NIT) - 1u);  // bit r: ties with e-1
+        const uint32_t tb = eqn | eqp;
         __syncwarp();
-        warp_tail(buf, s, out, B);
+        for (uint32_t e = lane; e < L; e += 32) __stcs(B.saf + s.start + e, sl32[e]);
+        if (__any_sync(0xFFFFFFFFu, tb != 0)) {
+            // compact the tied elements (sorted order kept; bit 31 = run start)
+            const uint32_t c = __popc(tb);
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t T = __shfl_sync(0xFFFFFFFFu, x, 31);
+            uint32_t w = x - c;
+#pragma unroll
+            for (int r = 0; r < NIT; ++r)
+                if ((tb >> r) & 1u) tl[w++] = (lane * NIT + r) | (((eqp >> r) & 1u) ? 0u : 0x80000000u);
+            __syncwarp();
+            // batches of whole runs through warp_finish on the next word
+            for (uint32_t b = 0; b < T;) {
+                const uint32_t j = b + lane;
+                const uint32_t te = j < T ? tl[j] : 0u;
+                const uint32_t starts = __ballot_sync(0xFFFFFFFFu, j < T && (te >> 31));
+                const bool full_fit = b + 32 >= T || (tl[b + 32] >> 31);
+                uint32_t nb = full_fit ? min(32u, T - b) : (starts & ~1u) ? 31u - __clz(starts & ~1u) : 0u;
+                if (nb == 0) {
+                    // one run longer than 32: a segment of the next round
+                    uint32_t Lr = 32;
+                    for (;;) {
+                        const uint32_t q = b + Lr + lane;
+                        const bool st = q >= T || (tl[q] >> 31);
+                        const uint32_t bl = __ballot_sync(0xFFFFFFFFu, st);
+                        if (bl) {
+                            Lr += __ffs(bl) - 1;
+                            break;
+                        }
+                        Lr += 32;
+                    }
+                    const uint32_t rs = tl[b] & 0xFFFFu;
+                    for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = sl32[rs + q];
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
+                    b += Lr;
+                    continue;
+                }
+                const uint32_t e = te & 0xFFFFu;
+                const uint32_t grp = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
+                uint32_t sl = lane < nb ? sl32[e] : 0u;
+                sl = warp_finish(sl, nb, s.word + 1, 0u, false, B, grp);
+                __syncwarp();
+                if (lane < nb) B.saf[s.start + e] = sl;
+                b += nb;
+            }
+        }
         __syncwarp();
     }
 }
