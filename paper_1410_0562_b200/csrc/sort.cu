@@ -279,30 +279,37 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t 
 // consecutive slots per thread share 3 text words and 2 terminator words;
 // 64-byte vector stores.  Same encoding as suffix_key (common.cuh).
 // ---------------------------------------------------------------------------
+// Key word 0 of the 16 slots p0 .. p0+15 (p0 a multiple of 16 inside the
+// packed text): 3 text words and 2 terminator words for all 16.
+__device__ __forceinline__ void keys16(const uint32_t* __restrict__ text,
+                                       const uint32_t* __restrict__ term, uint64_t p0,
+                                       uint32_t (&k)[16]) {
+    const uint64_t w = p0 >> 4;
+    const uint32_t off = (uint32_t)(p0 & 15);
+    const uint32_t t0 = __ldg(text + w), t1 = __ldg(text + w + 1), t2 = __ldg(text + w + 2);
+    const uint64_t v01 = ((uint64_t)t0 << 32) | t1, v12 = ((uint64_t)t1 << 32) | t2;
+    const uint64_t tb = p0 >> 5;
+    const uint32_t toff = (uint32_t)(p0 & 31);
+    const uint64_t T = ((uint64_t)__ldg(term + tb) << 32) | __ldg(term + tb + 1);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t o = off + j;
+        const uint64_t v = o < 16 ? (v01 << (2 * o)) : (v12 << (2 * (o - 16)));
+        uint32_t syms = (uint32_t)(v >> 36);
+        uint32_t ended = (uint32_t)__clzll((long long)(T << (toff + j)));
+        ended = ended > (uint32_t)kKeySyms ? (uint32_t)kKeySyms : ended;
+        const uint32_t keep = 2 * ended;
+        const uint32_t mask = keep == 0 ? 0u : (0x0FFFFFFFu & ~((1u << (28 - keep)) - 1u));
+        k[j] = ((syms & mask) << 4) | ended;
+    }
+}
+
 __global__ void keygen_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
                               uint64_t base, uint32_t n, uint32_t* __restrict__ key) {
     const uint32_t ng = (n + 15) >> 4;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
-        const uint64_t p0 = base + 16ull * g;
-        const uint64_t w = p0 >> 4;
-        const uint32_t off = (uint32_t)(p0 & 15);
-        const uint32_t t0 = __ldg(text + w), t1 = __ldg(text + w + 1), t2 = __ldg(text + w + 2);
-        const uint64_t v01 = ((uint64_t)t0 << 32) | t1, v12 = ((uint64_t)t1 << 32) | t2;
-        const uint64_t tb = p0 >> 5;
-        const uint32_t toff = (uint32_t)(p0 & 31);
-        const uint64_t T = ((uint64_t)__ldg(term + tb) << 32) | __ldg(term + tb + 1);
         uint32_t k[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t o = off + j;
-            const uint64_t v = o < 16 ? (v01 << (2 * o)) : (v12 << (2 * (o - 16)));
-            uint32_t syms = (uint32_t)(v >> 36);
-            uint32_t ended = (uint32_t)__clzll((long long)(T << (toff + j)));
-            ended = ended > (uint32_t)kKeySyms ? (uint32_t)kKeySyms : ended;
-            const uint32_t keep = 2 * ended;
-            const uint32_t mask = keep == 0 ? 0u : (0x0FFFFFFFu & ~((1u << (28 - keep)) - 1u));
-            k[j] = ((syms & mask) << 4) | ended;
-        }
+        keys16(text, term, base + 16ull * g, k);
         const uint32_t i0 = 16 * g;
         if (i0 + 16 <= n) {
             uint4* dst = reinterpret_cast<uint4*>(key + i0);
@@ -337,7 +344,8 @@ __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ s
         }
         for (int c = 0; c < M_N; ++c) misc[c] = 0;
         if (n == 1) saf[0] = sa_entry(B, 0u);
-        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, 1, n > kCapM ? 1u : 0u)});
+        // a LARGE first segment gets its keys from the first histogram pass
+        else if (n > 1) emit(in, Seg{0u, n, 0u, make_meta(24, 0, n > kCapM ? 0u : 1u, n > kCapM ? 1u : 0u)});
     }
 }
 
@@ -409,7 +417,34 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
         const bool kv = meta_kv(s.meta);
         const uint32_t* S = B.sa[buf];
         uint32_t* K = B.key[buf];
-        if (kv) {
+        if (!kv && meta_iota(s.meta) && s.word == 0) {
+            // the block's first pass: key word 0 generated here from the packed
+            // text (16 consecutive slots per thread, keys16) and written for the
+            // scatter -- no separate key-generation pass
+            for (uint32_t g = (ch.begin >> 4) + tid; g <= (ch.end - 1) >> 4; g += kDigNt) {
+                uint32_t k[16];
+                keys16(B.text, B.term, B.base + 16ull * g, k);
+                const uint32_t i0 = 16 * g;
+                if (i0 >= ch.begin && i0 + 16 <= ch.end) {
+                    uint4* dst = reinterpret_cast<uint4*>(K + i0);
+                    dst[0] = make_uint4(k[0], k[1], k[2], k[3]);
+                    dst[1] = make_uint4(k[4], k[5], k[6], k[7]);
+                    dst[2] = make_uint4(k[8], k[9], k[10], k[11]);
+                    dst[3] = make_uint4(k[12], k[13], k[14], k[15]);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) atomicAdd(&h[warp][(k[j] >> shift) & 0xFFu], 1u);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t p = i0 + j;
+                        if (p >= ch.begin && p < ch.end) {
+                            K[p] = k[j];
+                            atomicAdd(&h[warp][(k[j] >> shift) & 0xFFu], 1u);
+                        }
+                    }
+                }
+            }
+        } else if (kv) {
             // keys valid: 4 consecutive keys per thread per 16-byte load
             const uint32_t a0 = ch.begin & ~3u;
             for (uint32_t p0 = a0; p0 < ch.end; p0 += kDigNt * 4 * 2) {
@@ -1459,11 +1494,12 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
 
-    SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
-              keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(text, term,
-                                                                                  slot_base, n_suf,
-                                                                                  k0));
-    SB_CHECK(cudaGetLastError());
+    if (n <= kCapM) {
+        SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
+                  keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(
+                      text, term, slot_base, n_suf, k0));
+        SB_CHECK(cudaGetLastError());
+    }
     SB_LAUNCH(prof, s, "sort_init", n <= kCapM ? 4.0 * n : 0.0, n,
               init_kernel<<<n <= kCapM ? grid_for(n, 256) : 1u, 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc, B));
     SB_CHECK(cudaGetLastError());

@@ -9,4 +9,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file gpurun_out/${r}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     > gpurun_out/${r}_ncu_launches.log 2>&1; echo launches_rc=$?
 bash tools/prof.sh ${r}_full "digit_scatter:0" "bitonic_kernel:0" "compute_ranks:4" "gather_kernel:5" \
-    "insert_kernel:5" "digit_hist:0" "sort_keygen|keygen_kernel:0"
+    "insert_kernel:5" "digit_hist:0" "tiny_kernel:0"
