@@ -126,14 +126,25 @@ __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
 // loops -- ncu, profiles/).
 template <int NB>
 __device__ __forceinline__ uint32_t peers_of(uint32_t d) {
-    uint32_t peers = 0xFFFFFFFFu;
+    // per bit: test into a predicate, ballot it, replicate the lane's bit
+    // (selp), and fold  diff |= bal ^ rep  in one 3-input LOP3 (LUT 0xF6 =
+    // a | (b ^ c)); peers = lanes whose digit has no differing bit = ~diff
+    uint32_t diff = 0u;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-        const uint32_t bit = (d >> b) & 1u;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-        peers &= bal ^ (bit - 1u);  // bit ? bal : ~bal, branch-free
+        asm("{\n\t"
+            ".reg .pred p;\n\t"
+            ".reg .b32 t, bal, rep;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
+            "selp.b32 rep, 0xffffffff, 0, p;\n\t"
+            "lop3.b32 %0, %0, bal, rep, 0xF6;\n\t"
+            "}"
+            : "+r"(diff)
+            : "r"(d), "r"(1u << b));
     }
-    return peers;
+    return ~diff;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
