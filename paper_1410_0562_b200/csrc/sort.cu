@@ -616,10 +616,12 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
     }
 }
 
-__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+// 4-byte async copy global -> shared, L2 evict-first (the scatter reads each
+// key / slot once; the rank dictionary and g should keep L2)
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src)
+                 "l"(src), "l"(pol)
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
@@ -651,6 +653,8 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);      // 256
     const uint32_t nch = misc[M_CHUNKS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t pol_ef;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
 
     // Tiles of this CTA's chunks in order; the next tile's keys (and slots)
     // are prefetched into shared memory with cp.async while the current one
@@ -679,8 +683,8 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
         for (int it = 0; it < kDigIpt; ++it) {
             const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
             if (e < tn) {
-                cp_async4(s_ink + e, K + e);
-                if (!iota) cp_async4(s_ins + e, S + e);
+                cp_async4(s_ink + e, K + e, pol_ef);
+                if (!iota) cp_async4(s_ins + e, S + e, pol_ef);
             }
         }
         cp_async_commit();
@@ -1024,7 +1028,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists 
 #pragma unroll
         for (int r = 0; r < NIT; ++r) {
             const uint32_t e = lane * NIT + r;
-            v[r] = e < L ? (((__ldg(K + s.start + e) & rmask) << IDXB) | e) : 0xFFFFFFFFu;
+            v[r] = e < L ? (((__ldcs(K + s.start + e) & rmask) << IDXB) | e) : 0xFFFFFFFFu;
         }
         warp_bitonic<NIT>(v);
         // sorted order is lane-major (element e = lane*NIT + r); ties on this
@@ -1036,7 +1040,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists 
         for (int r = 0; r < NIT; ++r) {
             const uint32_t e = lane * NIT + r;
             k16[r] = v[r] >> IDXB;
-            if (e < L) sl32[e] = __ldg(S + s.start + (v[r] & (N - 1)));
+            if (e < L) sl32[e] = __ldcs(S + s.start + (v[r] & (N - 1)));
         }
         const uint32_t nxt0 = __shfl_down_sync(0xFFFFFFFFu, k16[0], 1);
         uint32_t eqn = 0;  // bit r: element e ties with e+1
