@@ -162,42 +162,74 @@ __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint3
                                                 uint32_t key0, bool have_key, const Bufs& B,
                                                 uint32_t group0 = 0, bool active0 = true) {
     // Several independent runs may be packed into one call: lanes [g, g+len)
-    // of each run carry group0 = g (its first lane); runs never mix because
-    // the composite sorts by group first.
+    // of each run carry group0 = g (its first lane); runs never mix.  A lane
+    // that is not active (or not valid) is a group of its own.
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = lane < L;
     bool active = valid && active0;
-    uint32_t group = group0;
+    uint32_t group = active ? group0 : lane;
     for (;;) {
         uint32_t key = 0;
         if (active) key = have_key ? key0 : suffix_key(B.text, B.term, B.base + (slot & B.smask), word);
         have_key = false;
-        unsigned long long comp;
-        if (!valid) comp = ~0ull;
-        else if (active) comp = ((unsigned long long)group << 37) | ((unsigned long long)key << 5) | lane;
-        else comp = ((unsigned long long)lane << 37) | lane;
-#pragma unroll
-        for (uint32_t k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, comp, j);
-                const bool up = (lane & k) == 0;
-                const bool lower = (lane & j) == 0;
-                const unsigned long long mn = comp < other ? comp : other;
-                const unsigned long long mx = comp < other ? other : comp;
-                comp = (lower == up) ? mn : mx;
+        // group extents: [group, gend)
+        const uint32_t starts = __ballot_sync(0xFFFFFFFFu, group == lane);
+        const uint32_t above = lane == 31 ? 0u : (starts & (0xFFFFFFFEu << group) & ~((2u << lane) - 1u));
+        const uint32_t gend = above ? (uint32_t)(__ffs(above) - 1) : 32u;
+        const uint32_t W = __reduce_max_sync(0xFFFFFFFFu, gend - group);
+        if (W <= 8) {
+            // short runs (the usual case: pairs): stable rank inside the group
+            // by comparing with the at most W-1 neighbours on each side, then
+            // move slot and key to lane group+rank
+            uint32_t rank = 0;
+            for (uint32_t d = 1; d < W; ++d) {
+                const uint32_t ku = __shfl_up_sync(0xFFFFFFFFu, key, d);
+                const uint32_t kd = __shfl_down_sync(0xFFFFFFFFu, key, d);
+                if (lane >= group + d && ku <= key) ++rank;
+                if (lane + d < gend && kd < key) ++rank;
             }
+            const uint32_t dest = group + rank;
+            uint32_t ns = slot, nk = key;
+            for (int d = -(int)W + 1; d < (int)W; ++d) {
+                const uint32_t srcl = (uint32_t)((int)lane + d) & 31u;
+                const uint32_t dd = __shfl_sync(0xFFFFFFFFu, dest, srcl);
+                const uint32_t ss = __shfl_sync(0xFFFFFFFFu, slot, srcl);
+                const uint32_t kk = __shfl_sync(0xFFFFFFFFu, key, srcl);
+                if ((int)lane + d >= 0 && (int)lane + d < 32 && dd == lane) {
+                    ns = ss;
+                    nk = kk;
+                }
+            }
+            slot = ns;
+            key = nk;
+        } else {
+            unsigned long long comp;
+            if (!valid) comp = ~0ull;
+            else comp = ((unsigned long long)group << 37) | ((unsigned long long)key << 5) | lane;
+#pragma unroll
+            for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                    const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, comp, j);
+                    const bool up = (lane & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    const unsigned long long mn = comp < other ? comp : other;
+                    const unsigned long long mx = comp < other ? other : comp;
+                    comp = (lower == up) ? mn : mx;
+                }
+            }
+            slot = __shfl_sync(0xFFFFFFFFu, slot, (uint32_t)(comp & 31));
+            key = (uint32_t)(comp >> 5);
         }
-        slot = __shfl_sync(0xFFFFFFFFu, slot, (uint32_t)(comp & 31));
-        const unsigned long long hi = comp >> 5;
-        const unsigned long long prv = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
-        const unsigned long long nxt = __shfl_down_sync(0xFFFFFFFFu, hi, 1);
-        const bool eqp = valid && lane > 0 && prv == hi;
-        const bool eqn = valid && lane + 1 < L && nxt == hi;
-        const uint32_t k32 = (uint32_t)(hi & 0xFFFFFFFFull);
-        active = (eqp || eqn) && ((k32 & 15u) == (uint32_t)kKeySyms);
-        const uint32_t starts = __ballot_sync(0xFFFFFFFFu, valid && !eqp);
-        group = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
+        // ties on this word with 14 real symbols continue on the next word
+        const uint32_t kp = __shfl_up_sync(0xFFFFFFFFu, key, 1);
+        const uint32_t kn = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+        const bool g_active = active;  // whole groups are active or not
+        const bool eqp = g_active && lane > group && kp == key;
+        const bool eqn = g_active && lane + 1 < gend && kn == key;
+        active = (eqp || eqn) && ((key & 15u) == (uint32_t)kKeySyms);
+        const uint32_t st2 = __ballot_sync(0xFFFFFFFFu, !active || !eqp);
+        group = active ? 31u - __clz(st2 & (0xFFFFFFFFu >> (31 - lane))) : lane;
         if (!__any_sync(0xFFFFFFFFu, active)) break;
         ++word;
     }
@@ -788,7 +820,7 @@ constexpr size_t scatter_smem() {
 // ---------------------------------------------------------------------------
 // TINY: one warp per segment
 // ---------------------------------------------------------------------------
-constexpr uint32_t kTinyPerWarp = 16;  // list entries per warp, packed into shared calls
+constexpr uint32_t kTinyPerWarp = 32;  // list entries per warp, packed into shared calls
 
 // Fast path for packed tiny segments whose unknown key bits fit in 16 (keys
 // valid, shift <= 8): one u32 bitonic over the warp on (group, key bits, lane).
@@ -841,9 +873,20 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
         // lanes through the sort: the composite sorts by group first)
         uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0, rb = 0;
         bool mine = false, kv = false, fast = true;
+        // all of the warp's list entries in one coalesced load (lane l holds
+        // entry i0+l); the packing loop below broadcasts them with shuffles, so
+        // it never waits on memory
+        Seg mys = Seg{0u, 0u, 0u, 0u};
+        if (lane < i1 - i0) mys = in.seg[TINY][i0 + lane];
         for (uint32_t i = i0; i <= i1; ++i) {
             Seg sg;
-            if (i < i1) sg = in.seg[TINY][i];
+            if (i < i1) {
+                const uint32_t src = i - i0;
+                sg.start = __shfl_sync(0xFFFFFFFFu, mys.start, src);
+                sg.len = __shfl_sync(0xFFFFFFFFu, mys.len, src);
+                sg.word = __shfl_sync(0xFFFFFFFFu, mys.word, src);
+                sg.meta = __shfl_sync(0xFFFFFFFFu, mys.meta, src);
+            }
             if (i == i1 || lb + sg.len > 32) {
                 if (lb) {
                     uint32_t r;
