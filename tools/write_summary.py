@@ -88,7 +88,8 @@ def main():
         m = raw(rep, metrics)
         if not m:
             continue
-        shutil.copy(rep, os.path.join(PROF, os.path.basename(rep)))
+        if i == 0:  # the dominant kernel's full report is kept (the others stay in gpurun_out/)
+            shutil.copy(rep, os.path.join(PROF, os.path.basename(rep)))
         t = num(*m["gpu__time_duration.sum"])
         d = num(*m["dram__bytes_read.sum"]) + num(*m["dram__bytes_write.sum"])
         full_lines.append("%-22s %8.1f %9.1f %8.0f %6.1f %6.1f %6.1f %5s %9.2f %6.1f" % (
@@ -119,8 +120,11 @@ def main():
           "its share of the serialised launch list below: %s." % (
               dom, roof.get("share_of_step") or 0.0, "%.3f" % share_ncu if share_ncu else "n/a"),
           "Raw list: `profiles/%s_launches.csv`." % r, "", table, "",
-          "## ncu --set full, one launch each (`profiles/%s_full_*.ncu-rep`)" % r, "", "```"] + \
+          "## ncu --set full, one launch each (`profiles/%s_full_0.ncu-rep` = digit_scatter)" % r, "", "```"] + \
         full_lines + ["```", ""]
+    rd = os.path.join(PROF, r + "_reading.md")
+    if os.path.exists(rd):
+        md += ["", open(rd).read()]
     open(os.path.join(PROF, r + "_summary.md"), "w").write("\n".join(md))
     print("wrote", os.path.join(PROF, r + "_summary.md"))
 
