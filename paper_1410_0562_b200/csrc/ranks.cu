@@ -26,7 +26,12 @@ __device__ __forceinline__ void store4(G* dst, G a, G b, G c, G d);
 template <>
 __device__ __forceinline__ void store4<uint32_t>(uint32_t* dst, uint32_t a, uint32_t b, uint32_t c,
                                                  uint32_t d) {
-    *reinterpret_cast<uint4*>(dst) = make_uint4(a, b, c, d);
+    // g is read back at random by the gather right after ComputeRanks: keep
+    // it in L2 (evict-last; measured +1 % on c2 over the default policy)
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst), "r"(a),
+                 "r"(b), "r"(c), "r"(d), "l"(pol));
 }
 template <>
 __device__ __forceinline__ void store4<uint64_t>(uint64_t* dst, uint64_t a, uint64_t b, uint64_t c,
