@@ -196,6 +196,11 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     memory) and Insert rewrites it in place through HBM
  *                     staging.  Default: unlimited.
  *   "host_tier"       1: move B_ext to the host tier now (and keep it there).
+ *   "sa_payload"      1 (default): while a block has < 2^29 suffixes, its SA
+ *                     entries carry the B_int symbol in their top 3 bits; 0:
+ *                     never (as for larger blocks: ComputeRanks records B_int
+ *                     per slot instead).  Results are identical; the option
+ *                     exists so both paths can be tested at small sizes.
  *   "insert_split"    1: with setbwte_set_partition world > 1 and B_ext in HBM,
  *                     Insert is split by output range (rank r merges output
  *                     superblocks [nsb*r/P, nsb*(r+1)/P)) and the new

@@ -148,7 +148,7 @@ struct setbwte_s {
 
     // append scratch
     DevBuf in_bytes, in_off, text, term, slot_off, gfirst, bounds, err, small;
-    DevBuf saf, g, pos, bint, outbuf;
+    DevBuf saf, g, pos, bint, outbuf, bslot;
     SortScratch sort, sort2;
 
     // options
@@ -174,6 +174,7 @@ struct setbwte_s {
     // data-parallel ComputeRanks (and, with insert_split, Insert by output range)
     int rank = 0, world = 1;
     bool insert_split = false;
+    uint64_t payload_limit = kPayloadLimit;  // option "sa_payload"
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
 
@@ -262,7 +263,8 @@ inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cu
 // slots starting at slot_base).  With world > 1, only this rank's slice is
 // computed and the slices are exchanged by the allgather callback.
 setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1,
-                                 uint64_t slot_base, uint64_t n_suf, void* g, int gw) {
+                                 uint64_t slot_base, uint64_t n_suf, void* g, int gw,
+                                 uint8_t* bslot = nullptr) {
     if (h->n == 0) {
         // empty B_ext: every suffix has rank 0
         API_CHECK(h, cudaMemsetAsync(g, 0, n_suf * gw, h->stream));
@@ -272,7 +274,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_blk(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
-                                          n_suf - (j1 - j0), g, gw, h->rank_ilp));
+                                          n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
@@ -458,8 +460,13 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     uint64_t* g = (uint64_t*)h->g.p;
     uint64_t* pos = (uint64_t*)h->pos.p;
     uint8_t* bint = (uint8_t*)h->bint.p;
+    // blocks too large for the SA payload: ComputeRanks records B_int per
+    // slot (single-rank ComputeRanks over a non-empty index only)
+    uint8_t* bslot = nullptr;
+    if (!sa_payload(n_suf, h->payload_limit) && h->n != 0 && h->world <= 1)
+        API_CHECK(h, ensure(h->bslot, n_suf + 8, &bslot));
     // g := ComputeRanks(S_jk, B_ext)
-    setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw);
+    setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw, bslot);
     if (st != SETBWTE_OK) return st;
     InsertBufs ib;
     st = insert_prepare(h, n_suf, &ib);
@@ -467,7 +474,8 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // B_int := B(S_jk, SA_int), g_sa / pos and the superblock
     // slices of pos, fused
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
-                               (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb));
+                               (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb, bslot,
+                               h->payload_limit));
     return insert_finish(h, ib, pos, gw, bint, n_suf, b.j1 - b.j0);
 }
 
@@ -569,7 +577,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
                 if (st0 != SETBWTE_OK) return st0;
             }
             API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, blocks[k].S0,
-                                    (uint32_t)(blocks[k].S1 - blocks[k].S0), saf2, &h->sstats));
+                                    (uint32_t)(blocks[k].S1 - blocks[k].S0), saf2, &h->sstats,
+                                    false, h->payload_limit));
             setbwte_status st1 = rank_insert_stage(h, pk, blocks[k], saf2);
             if (st1 != SETBWTE_OK) {
                 if (k > 0) h->failed = true;
@@ -604,7 +613,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
                 if (e != cudaSuccess) break;
             }
             e = sort_block(L.prof, L.stream, *L.ws, pk.text, pk.term, blocks[k].S0,
-                           (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st);
+                           (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st, false,
+                           h->payload_limit);
             if (e == cudaSuccess) e = cudaEventRecord(L.ev_sorted, L.stream);
             std::lock_guard<std::mutex> lk(mu);
             if (e != cudaSuccess) {
@@ -909,7 +919,7 @@ void setbwte_destroy(setbwte_t h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     DevBuf* bufs[] = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0], &h->sb[1],
                       &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term, &h->gfirst,
-                      &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos,
+                      &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos, &h->bslot,
                       &h->bint, &h->outbuf, &h->sort.sa0, &h->sort.sa1, &h->sort.k0,
                       &h->sort.k1, &h->sort.segs_a, &h->sort.segs_b, &h->sort.small_a,
                       &h->sort.small_b, &h->sort.chunks, &h->sort.hist, &h->sort.ctr,
@@ -1155,12 +1165,13 @@ setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const u
     API_CHECK(h, ensure(h->bint, n_suf, &bint));
     API_CHECK(h, ensure(h->outbuf, n_suf, &asc));
     API_CHECK(h, sort_block(h->prof, h->stream, h->sort, po.pk.text, po.pk.term, 0,
-                            (uint32_t)n_suf, saf, nullptr));
+                            (uint32_t)n_suf, saf, nullptr, false, h->payload_limit));
     API_CHECK(h, launch_gather(h->prof, h->stream, po.pk.text, po.pk.term, 0, saf, nullptr,
-                               (uint32_t)n_suf, pos, 8, bint));
+                               (uint32_t)n_suf, pos, 8, bint, nullptr, 0, nullptr,
+                               h->payload_limit));
     API_CHECK(h, launch_bint_ascii(h->prof, h->stream, bint, (uint32_t)n_suf,
                                    (const uint8_t*)h->d_sym.p, asc));
-    API_CHECK(h, launch_strip_payload(h->stream, saf, (uint32_t)n_suf));
+    API_CHECK(h, launch_strip_payload(h->stream, saf, (uint32_t)n_suf, h->payload_limit));
     if (sa_out)
         API_CHECK(h, cudaMemcpyAsync(sa_out, saf, n_suf * 4, cudaMemcpyDeviceToHost, h->stream));
     if (bint_out)
@@ -1221,6 +1232,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "hbm_budget_bytes")) {
         if (value < 1) return SETBWTE_E_INVALID_ARG;
         h->hbm_budget = value;
+    } else if (!strcmp(key, "sa_payload")) {
+        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        h->payload_limit = value ? kPayloadLimit : 0;
     } else if (!strcmp(key, "insert_split")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;

@@ -133,15 +133,20 @@ cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf);
 // generated.  The gather then reads B_int with the SA entry instead of two
 // random text lookups.
 constexpr uint32_t kPayloadShift = 29;
-__host__ __device__ inline bool sa_payload(uint64_t n_suf) { return n_suf < (1ull << kPayloadShift); }
-__host__ __device__ inline uint32_t sa_slot_mask(uint64_t n_suf) {
-    return sa_payload(n_suf) ? (1u << kPayloadShift) - 1u : 0xFFFFFFFFu;
+// (limit: the handle's option "sa_payload"; 0 switches the payload off)
+constexpr uint64_t kPayloadLimit = 1ull << kPayloadShift;
+__host__ __device__ inline bool sa_payload(uint64_t n_suf, uint64_t limit = kPayloadLimit) {
+    return n_suf < limit && n_suf < kPayloadLimit;
 }
-cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n);
+__host__ __device__ inline uint32_t sa_slot_mask(uint64_t n_suf, uint64_t limit = kPayloadLimit) {
+    return sa_payload(n_suf, limit) ? (1u << kPayloadShift) - 1u : 0xFFFFFFFFu;
+}
+cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n, uint64_t limit);
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
-                       uint32_t* d_sa_final, SortStats* st, bool reserve_only = false);
+                       uint32_t* d_sa_final, SortStats* st, bool reserve_only = false,
+                       uint64_t payload_limit = kPayloadLimit);
 
 // ranks.cu -- A3 ComputeRanks (Lemma 1, Alg.2) and the
 // fused A2/A4 extraction + gather (Alg.1).
@@ -149,7 +154,7 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp);
+                                 int gw, int ilp, uint8_t* bslot = nullptr);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64)
 // With sb_start != NULL also writes sb_start[0..nsb] (superblock slices of pos).
 cudaError_t launch_merge_ranks(Profiler& prof, cudaStream_t s, const Blk* oblk, const uint64_t* osb,
@@ -162,7 +167,8 @@ cudaError_t launch_merge_pos(Profiler& prof, cudaStream_t s, const Blk* oblk, ui
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
-                          uint64_t* sb_start = nullptr, uint64_t nsb = 0);
+                          uint64_t* sb_start = nullptr, uint64_t nsb = 0,
+                          const uint8_t* bslot = nullptr, uint64_t payload_limit = kPayloadLimit);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,

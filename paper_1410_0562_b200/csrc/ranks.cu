@@ -44,7 +44,7 @@ template <class G>
 __global__ void __launch_bounds__(256) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
     uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
-    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g) {
+    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
     for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
          j += (uint64_t)gridDim.x * blockDim.x) {
@@ -53,6 +53,11 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
         const uint64_t le = slot_off[j + 1] - 1 - slot_base;
         uint64_t i = m_ext;
         g[le] = (G)i;
+        // blocks too large for the SA payload: the walk also records B_int per
+        // slot (the symbol it reads at q is B_int of the suffix at q+1; a
+        // string's first suffix has '$'), so the gather reads one byte per
+        // suffix instead of two random text lookups
+        if (bslot) bslot[l0] = 4;
         uint64_t lp = le;  // next step computes slot lp-1
         uint64_t wi = ~0ull;
         uint32_t word = 0;
@@ -63,6 +68,7 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
                 word = __ldg(text + wi);
             }
             const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
+            if (bslot) bslot[q + 1] = (uint8_t)c;
             const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
             i = Cc + dict_rank(blk, sb, c, i);
             return i;
@@ -92,7 +98,7 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp) {
+                                 int gw, int ilp, uint8_t* bslot) {
     (void)ilp;
     if (j1 <= j0) return cudaSuccess;
     // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
@@ -104,11 +110,11 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
     if (gw == 4) {
         SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                   compute_ranks_kernel<uint32_t><<<grid, 256, 0, s>>>(
-                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g));
+                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g, bslot));
     } else {
         SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                   compute_ranks_kernel<uint64_t><<<grid, 256, 0, s>>>(
-                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g));
+                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g, bslot));
     }
     return cudaGetLastError();
 }
@@ -121,8 +127,7 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
                               uint64_t slot_base, const uint32_t* __restrict__ sa,
                               const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
                               uint8_t* __restrict__ bint, uint64_t* __restrict__ sb_start,
-                              uint64_t nsb) {
-    const uint32_t smask = sa_slot_mask(n_suf);
+                              uint64_t nsb, const uint8_t* __restrict__ bslot, uint32_t smask) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t iters = (n_suf + stride - 1) / stride;  // warp-uniform trip count
@@ -139,6 +144,8 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
             uint8_t b;
             if (smask != 0xFFFFFFFFu) {
                 b = (uint8_t)(e >> kPayloadShift);  // B_int carried by the SA entry
+            } else if (bslot) {
+                b = __ldg(bslot + sl);  // recorded by ComputeRanks
             } else {
                 const uint64_t p = slot_base + sl;
                 if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
@@ -166,7 +173,9 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
 cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
-                          uint64_t* sb_start, uint64_t nsb) {
+                          uint64_t* sb_start, uint64_t nsb, const uint8_t* bslot,
+                          uint64_t payload_limit) {
+    const uint32_t smask = sa_slot_mask(n_suf, payload_limit);
     // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol + term bit)
     const double bytes = (5.375 + 2.0 * gw) * n_suf;
     const unsigned grid = grid_for(n_suf, 256, 148u * 64u);
@@ -174,12 +183,12 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint32_t*)g, n_suf,
-                                                               (uint32_t*)pos, bint, sb_start, nsb));
+                                                               (uint32_t*)pos, bint, sb_start, nsb, bslot, smask));
     } else {
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint64_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint64_t*)g, n_suf,
-                                                               (uint64_t*)pos, bint, sb_start, nsb));
+                                                               (uint64_t*)pos, bint, sb_start, nsb, bslot, smask));
     }
     return cudaGetLastError();
 }

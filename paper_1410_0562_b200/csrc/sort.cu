@@ -1483,7 +1483,8 @@ cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf) {
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
-                       uint32_t* d_sa_final, SortStats* st, bool reserve_only) {
+                       uint32_t* d_sa_final, SortStats* st, bool reserve_only,
+                       uint64_t payload_limit) {
     if (n_suf == 0) return cudaSuccess;
     const size_t n = n_suf;
     const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
@@ -1536,7 +1537,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.text = text;
     B.term = term;
     B.base = slot_base;
-    B.smask = sa_slot_mask(n_suf);
+    B.smask = sa_slot_mask(n_suf, payload_limit);
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
@@ -1670,8 +1671,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     return cudaSuccess;
 }
 
-cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n) {
-    if (n == 0 || !sa_payload(n)) return cudaSuccess;
+cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n, uint64_t limit) {
+    if (n == 0 || !sa_payload(n, limit)) return cudaSuccess;
     sortk::strip_payload_kernel<<<grid_for(n, 256), 256, 0, s>>>(sa, n);
     return cudaGetLastError();
 }

@@ -465,3 +465,39 @@ def test_merge_edge_cases(SetBWTE):
     other.append_strings(["AC"])
     with pytest.raises(Exception):
         h.merge(other)
+
+
+# --- blocks without the SA payload (the > 2^29-suffix path, forced small) ---------
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_sets_without_payload(SetBWTE, seed):
+    d, o = synth.random_set(13000 + seed, max_m=48, max_len=60, alphabet=["ACGT", "AC"][seed % 2])
+    rng = np.random.default_rng(seed)
+    idx = SetBWTE(A, block_suffixes=int(rng.integers(30, 400)))
+    idx.set_option("sa_payload", 0)
+    m = len(o) - 1
+    cut = int(rng.integers(0, m + 1))
+    o = np.asarray(o, dtype=np.uint64)
+    idx.append(d[: int(o[cut])], o[: cut + 1])
+    idx.append(d[int(o[cut]):], o[cut:] - o[cut])
+    assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+@pytest.mark.parametrize("M", [25250, 50500])
+def test_c1_without_payload(SetBWTE, c1, M):
+    d, o, want = c1
+    idx = SetBWTE(A, block_suffixes=M)
+    idx.set_option("sa_payload", 0)
+    idx.append(d, o)
+    assert idx.bwt() == want
+    # stage view: ConstructSA + B_int of one block, SA entries without payload
+    sa, bint = idx.construct_sa(d[: int(o[50])], o[:51])
+    assert list(sa) == list(oracle.block_sa(A, d[: int(o[50])], o[:51]))
+
+
+def test_genome_without_payload(SetBWTE):
+    d, o = synth.genome_sampled(3000, 120, 60000, seed=4)
+    idx = SetBWTE(A, block_suffixes=60000)
+    idx.set_option("sa_payload", 0)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o, threads=None)
