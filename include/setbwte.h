@@ -196,6 +196,8 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     memory) and Insert rewrites it in place through HBM
  *                     staging.  Default: unlimited.
  *   "host_tier"       1: move B_ext to the host tier now (and keep it there).
+ *   "g_width"         width of g / pos: 0 or 4 (default) = u32 while the new
+ *                     index has < 2^32 symbols, else u64; 8 = always u64.
  *   "sa_payload"      1 (default): while a block has < 2^29 suffixes, its SA
  *                     entries carry the B_int symbol in their top 3 bits; 0:
  *                     never (as for larger blocks: ComputeRanks records B_int

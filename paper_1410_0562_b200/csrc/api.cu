@@ -175,6 +175,7 @@ struct setbwte_s {
     int rank = 0, world = 1;
     bool insert_split = false;
     uint64_t payload_limit = kPayloadLimit;  // option "sa_payload"
+    int g_width = 0;                         // option "g_width": 0 auto, 8 = always u64
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
 
@@ -264,7 +265,7 @@ inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cu
 // computed and the slices are exchanged by the allgather callback.
 setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, uint64_t n_suf, void* g, int gw,
-                                 uint8_t* bslot = nullptr) {
+                                 uint8_t* bslot = nullptr, bool bing = false) {
     if (h->n == 0) {
         // empty B_ext: every suffix has rank 0
         API_CHECK(h, cudaMemsetAsync(g, 0, n_suf * gw, h->stream));
@@ -274,7 +275,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_blk(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
-                                          n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot));
+                                          n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot, bing));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
@@ -456,17 +457,21 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
                                  const uint32_t* saf) {
     const uint64_t n_suf = b.S1 - b.S0;
     // g / pos width: u32 while every position of the new B_ext fits
-    const int gw = (h->n + n_suf) < (1ull << 32) ? 4 : 8;
+    const int gw = (h->n + n_suf) < (1ull << 32) && h->g_width != 8 ? 4 : 8;
     uint64_t* g = (uint64_t*)h->g.p;
     uint64_t* pos = (uint64_t*)h->pos.p;
     uint8_t* bint = (uint8_t*)h->bint.p;
     // blocks too large for the SA payload: ComputeRanks records B_int per
     // slot (single-rank ComputeRanks over a non-empty index only)
+    // (with u64 g, B_int goes into g's top byte instead: bing)
     uint8_t* bslot = nullptr;
-    if (!sa_payload(n_suf, h->payload_limit) && h->n != 0 && h->world <= 1)
-        API_CHECK(h, ensure(h->bslot, n_suf + 8, &bslot));
+    bool bing = false;
+    if (!sa_payload(n_suf, h->payload_limit) && h->n != 0 && h->world <= 1) {
+        if (gw == 8) bing = true;
+        else API_CHECK(h, ensure(h->bslot, n_suf + 8, &bslot));
+    }
     // g := ComputeRanks(S_jk, B_ext)
-    setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw, bslot);
+    setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw, bslot, bing);
     if (st != SETBWTE_OK) return st;
     InsertBufs ib;
     st = insert_prepare(h, n_suf, &ib);
@@ -475,7 +480,7 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // slices of pos, fused
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
                                (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb, bslot,
-                               h->payload_limit));
+                               h->payload_limit, bing));
     return insert_finish(h, ib, pos, gw, bint, n_suf, b.j1 - b.j0);
 }
 
@@ -494,7 +499,7 @@ setbwte_status merge_impl(setbwte_t h, setbwte_t o) {
     }
     API_CHECK(h, cudaStreamSynchronize(o->stream));
     const uint64_t n_o = o->n;
-    const int gw = (h->n + n_o) < (1ull << 32) ? 4 : 8;
+    const int gw = (h->n + n_o) < (1ull << 32) && h->g_width != 8 ? 4 : 8;
     uint64_t *g, *pos;
     uint8_t* bint;
     API_CHECK(h, ensure(h->g, n_o, &g));
@@ -1232,6 +1237,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "hbm_budget_bytes")) {
         if (value < 1) return SETBWTE_E_INVALID_ARG;
         h->hbm_budget = value;
+    } else if (!strcmp(key, "g_width")) {
+        if (value != 0 && value != 4 && value != 8) return SETBWTE_E_INVALID_ARG;
+        h->g_width = (int)value;
     } else if (!strcmp(key, "sa_payload")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->payload_limit = value ? kPayloadLimit : 0;

@@ -154,8 +154,10 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp, uint8_t* bslot = nullptr);
-// g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64)
+                                 int gw, int ilp, uint8_t* bslot = nullptr, bool bing = false);
+// g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64).
+// Blocks without the SA payload get B_int from ComputeRanks: bslot (one byte
+// per slot) with u32 g, or bing = the top byte of each u64 g.
 // With sb_start != NULL also writes sb_start[0..nsb] (superblock slices of pos).
 cudaError_t launch_merge_ranks(Profiler& prof, cudaStream_t s, const Blk* oblk, const uint64_t* osb,
                                const uint64_t* oC, uint64_t m_o, uint64_t n_o, const Blk* hblk,
@@ -168,7 +170,8 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
                           uint64_t* sb_start = nullptr, uint64_t nsb = 0,
-                          const uint8_t* bslot = nullptr, uint64_t payload_limit = kPayloadLimit);
+                          const uint8_t* bslot = nullptr, uint64_t payload_limit = kPayloadLimit,
+                          bool bing = false);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,

@@ -44,7 +44,8 @@ template <class G>
 __global__ void __launch_bounds__(256) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
     uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
-    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot) {
+    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot,
+    bool bing) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
     for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
          j += (uint64_t)gridDim.x * blockDim.x) {
@@ -73,6 +74,22 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
             i = Cc + dict_rank(blk, sb, c, i);
             return i;
         };
+        if (sizeof(G) == 8 && bing) {
+            // u64 g without SA payload: B_int rides in g's top byte (g < 2^56).
+            // B_int of the suffix at q+1 is the symbol read at q, so each g
+            // is stored one step late, with that symbol
+            uint64_t pq = le, pv = i;
+            for (uint64_t q = le; q-- > l0;) {
+                const uint64_t v = step(q);
+                const uint64_t p = q + slot_base;
+                const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
+                g[pq] = (G)(pv | ((uint64_t)c << 56));
+                pq = q;
+                pv = v;
+            }
+            g[pq] = (G)(pv | (4ull << 56));  // a string's first suffix: '$'
+            continue;
+        }
         // single steps down to a 4-aligned local slot, then 4 steps per
         // vector store (one store instruction instead of four)
         while (lp > l0 && (lp & 3) != 0) {
@@ -98,7 +115,7 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp, uint8_t* bslot) {
+                                 int gw, int ilp, uint8_t* bslot, bool bing) {
     (void)ilp;
     if (j1 <= j0) return cudaSuccess;
     // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
@@ -110,11 +127,11 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
     if (gw == 4) {
         SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                   compute_ranks_kernel<uint32_t><<<grid, 256, 0, s>>>(
-                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g, bslot));
+                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g, bslot, false));
     } else {
         SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                   compute_ranks_kernel<uint64_t><<<grid, 256, 0, s>>>(
-                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g, bslot));
+                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g, bslot, bing));
     }
     return cudaGetLastError();
 }
@@ -127,7 +144,8 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
                               uint64_t slot_base, const uint32_t* __restrict__ sa,
                               const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
                               uint8_t* __restrict__ bint, uint64_t* __restrict__ sb_start,
-                              uint64_t nsb, const uint8_t* __restrict__ bslot, uint32_t smask) {
+                              uint64_t nsb, const uint8_t* __restrict__ bslot, bool bing,
+                              uint32_t smask) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t iters = (n_suf + stride - 1) / stride;  // warp-uniform trip count
@@ -139,10 +157,15 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
             // streaming (evict-first) SA / pos / B_int accesses leave L2 to g
             const uint32_t e = __ldcs(sa + i);
             const uint32_t sl = e & smask;
-            pv = (g ? (uint64_t)__ldg(g + sl) : 0ull) + i;
+            uint64_t gv = g ? (uint64_t)__ldg(g + sl) : 0ull;
+            const uint8_t bg = (uint8_t)(gv >> 56);
+            if (bing) gv &= (1ull << 56) - 1ull;
+            pv = gv + i;
             __stcs(pos + i, (G)pv);
             uint8_t b;
-            if (smask != 0xFFFFFFFFu) {
+            if (bing) {
+                b = bg;  // B_int stored in g's top byte by ComputeRanks
+            } else if (smask != 0xFFFFFFFFu) {
                 b = (uint8_t)(e >> kPayloadShift);  // B_int carried by the SA entry
             } else if (bslot) {
                 b = __ldg(bslot + sl);  // recorded by ComputeRanks
@@ -158,7 +181,9 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
             if (v) {
                 if (lane == 0 && i > 0) {
                     const uint32_t sl1 = sa[i - 1] & smask;
-                    prev = (g ? (uint64_t)__ldg(g + sl1) : 0ull) + (i - 1);
+                    uint64_t g1 = g ? (uint64_t)__ldg(g + sl1) : 0ull;
+                    if (bing) g1 &= (1ull << 56) - 1ull;
+                    prev = g1 + (i - 1);
                 }
                 const uint64_t cur = pv >> kSbShift;
                 const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
@@ -174,7 +199,7 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
                           uint64_t* sb_start, uint64_t nsb, const uint8_t* bslot,
-                          uint64_t payload_limit) {
+                          uint64_t payload_limit, bool bing) {
     const uint32_t smask = sa_slot_mask(n_suf, payload_limit);
     // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol + term bit)
     const double bytes = (5.375 + 2.0 * gw) * n_suf;
@@ -183,12 +208,12 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint32_t*)g, n_suf,
-                                                               (uint32_t*)pos, bint, sb_start, nsb, bslot, smask));
+                                                               (uint32_t*)pos, bint, sb_start, nsb, bslot, false, smask));
     } else {
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint64_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint64_t*)g, n_suf,
-                                                               (uint64_t*)pos, bint, sb_start, nsb, bslot, smask));
+                                                               (uint64_t*)pos, bint, sb_start, nsb, bslot, bing, smask));
     }
     return cudaGetLastError();
 }

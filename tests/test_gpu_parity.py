@@ -501,3 +501,26 @@ def test_genome_without_payload(SetBWTE):
     idx.set_option("sa_payload", 0)
     idx.append(d, o)
     assert idx.bwt() == oracle.bwt(A, d, o, threads=None)
+
+
+@pytest.mark.parametrize("payload", [0, 1])
+@pytest.mark.parametrize("seed", range(6))
+def test_random_sets_u64_g(SetBWTE, seed, payload):
+    """u64 g / pos (forced), with and without the SA payload (without it,
+    ComputeRanks stores B_int in g's top byte)."""
+    d, o = synth.random_set(14000 + seed, max_m=48, max_len=60)
+    rng = np.random.default_rng(seed)
+    idx = SetBWTE(A, block_suffixes=int(rng.integers(30, 400)))
+    idx.set_option("g_width", 8)
+    idx.set_option("sa_payload", payload)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+def test_c1_u64_g_without_payload(SetBWTE, c1):
+    d, o, want = c1
+    idx = SetBWTE(A, block_suffixes=25250)
+    idx.set_option("g_width", 8)
+    idx.set_option("sa_payload", 0)
+    idx.append(d, o)
+    assert idx.bwt() == want
