@@ -203,6 +203,10 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     never (as for larger blocks: ComputeRanks records B_int
  *                     per slot instead).  Results are identical; the option
  *                     exists so both paths can be tested at small sizes.
+ *   "kw1_min"         blocks of at least this many suffixes (default: none)
+ *                     precompute key word 1 of every slot in one sequential
+ *                     pass, so resolving word-0 ties reads one 4-byte key
+ *                     instead of two random text lookups.  Results identical.
  *   "insert_split"    1: with setbwte_set_partition world > 1 and B_ext in HBM,
  *                     Insert is split by output range (rank r merges output
  *                     superblocks [nsb*r/P, nsb*(r+1)/P)) and the new

@@ -174,7 +174,7 @@ struct setbwte_s {
     // data-parallel ComputeRanks (and, with insert_split, Insert by output range)
     int rank = 0, world = 1;
     bool insert_split = false;
-    uint64_t payload_limit = kPayloadLimit;  // option "sa_payload"
+    SortOpts sopt;                           // options "sa_payload", "kw1_min"
     int g_width = 0;                         // option "g_width": 0 auto, 8 = always u64
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
@@ -466,7 +466,7 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // (with u64 g, B_int goes into g's top byte instead: bing)
     uint8_t* bslot = nullptr;
     bool bing = false;
-    if (!sa_payload(n_suf, h->payload_limit) && h->n != 0 && h->world <= 1) {
+    if (!sa_payload(n_suf, h->sopt.payload_limit) && h->n != 0 && h->world <= 1) {
         if (gw == 8) bing = true;
         else API_CHECK(h, ensure(h->bslot, n_suf + 8, &bslot));
     }
@@ -480,7 +480,7 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // slices of pos, fused
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
                                (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb, bslot,
-                               h->payload_limit, bing));
+                               h->sopt.payload_limit, bing));
     return insert_finish(h, ib, pos, gw, bint, n_suf, b.j1 - b.j0);
 }
 
@@ -558,8 +558,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
     API_CHECK(h, ensure(h->g, max_suf, &tmp));
     API_CHECK(h, ensure(h->pos, max_suf, &tmp));
     API_CHECK(h, ensure(h->bint, max_suf, &tb));
-    API_CHECK(h, sort_reserve(h->sort, (uint32_t)max_suf));
-    if (NL > 1) API_CHECK(h, sort_reserve(h->sort2, (uint32_t)max_suf));
+    API_CHECK(h, sort_reserve(h->sort, (uint32_t)max_suf, h->sopt));
+    if (NL > 1) API_CHECK(h, sort_reserve(h->sort2, (uint32_t)max_suf, h->sopt));
     const uint64_t n_final = h->n + total;
     API_CHECK(h, ensure(h->sb_tot, ((n_final >> kSbShift) + 1) * 5 + 8, &tmp));
     SortLane lanes[2];
@@ -583,7 +583,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
             }
             API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, blocks[k].S0,
                                     (uint32_t)(blocks[k].S1 - blocks[k].S0), saf2, &h->sstats,
-                                    false, h->payload_limit));
+                                    false, h->sopt));
             setbwte_status st1 = rank_insert_stage(h, pk, blocks[k], saf2);
             if (st1 != SETBWTE_OK) {
                 if (k > 0) h->failed = true;
@@ -619,7 +619,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
             }
             e = sort_block(L.prof, L.stream, *L.ws, pk.text, pk.term, blocks[k].S0,
                            (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st, false,
-                           h->payload_limit);
+                           h->sopt);
             if (e == cudaSuccess) e = cudaEventRecord(L.ev_sorted, L.stream);
             std::lock_guard<std::mutex> lk(mu);
             if (e != cudaSuccess) {
@@ -1170,13 +1170,13 @@ setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const u
     API_CHECK(h, ensure(h->bint, n_suf, &bint));
     API_CHECK(h, ensure(h->outbuf, n_suf, &asc));
     API_CHECK(h, sort_block(h->prof, h->stream, h->sort, po.pk.text, po.pk.term, 0,
-                            (uint32_t)n_suf, saf, nullptr, false, h->payload_limit));
+                            (uint32_t)n_suf, saf, nullptr, false, h->sopt));
     API_CHECK(h, launch_gather(h->prof, h->stream, po.pk.text, po.pk.term, 0, saf, nullptr,
                                (uint32_t)n_suf, pos, 8, bint, nullptr, 0, nullptr,
-                               h->payload_limit));
+                               h->sopt.payload_limit));
     API_CHECK(h, launch_bint_ascii(h->prof, h->stream, bint, (uint32_t)n_suf,
                                    (const uint8_t*)h->d_sym.p, asc));
-    API_CHECK(h, launch_strip_payload(h->stream, saf, (uint32_t)n_suf, h->payload_limit));
+    API_CHECK(h, launch_strip_payload(h->stream, saf, (uint32_t)n_suf, h->sopt.payload_limit));
     if (sa_out)
         API_CHECK(h, cudaMemcpyAsync(sa_out, saf, n_suf * 4, cudaMemcpyDeviceToHost, h->stream));
     if (bint_out)
@@ -1242,7 +1242,10 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
         h->g_width = (int)value;
     } else if (!strcmp(key, "sa_payload")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
-        h->payload_limit = value ? kPayloadLimit : 0;
+        h->sopt.payload_limit = value ? kPayloadLimit : 0;
+    } else if (!strcmp(key, "kw1_min")) {
+        if (value == 0) return SETBWTE_E_INVALID_ARG;
+        h->sopt.kw1_min = value;
     } else if (!strcmp(key, "insert_split")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;

@@ -120,13 +120,15 @@ cudaError_t launch_slices(Profiler& prof, cudaStream_t s, const uint64_t* d_slot
 // sort.cu -- A1 ConstructSA (Sec.3).
 struct SortScratch {
     DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr, gtot, groups;
+    DevBuf kw1;  // key word 1 of every slot (large blocks only)
 };
 struct SortStats {
     uint64_t digit_passes = 0;
     uint64_t rounds = 0;
     std::vector<uint64_t> active_per_pass;  // elements entering each digit pass
 };
-cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf);
+struct SortOpts;
+cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf, const SortOpts& opts);
 // SA payload: while a block has fewer than 2^29 suffixes, every SA entry the
 // sort moves is (slot | b << 29) with b = the block's B_int symbol of that
 // suffix (2-bit code, or 4 for '$', Alg.1), attached when the slot is
@@ -142,11 +144,16 @@ __host__ __device__ inline uint32_t sa_slot_mask(uint64_t n_suf, uint64_t limit 
     return sa_payload(n_suf, limit) ? (1u << kPayloadShift) - 1u : 0xFFFFFFFFu;
 }
 cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n, uint64_t limit);
+// per-handle sort options (setbwte_set_option "sa_payload", "kw1_min")
+struct SortOpts {
+    uint64_t payload_limit = kPayloadLimit;
+    uint64_t kw1_min = 1ull << 40;  // blocks from this size precompute key word 1 (off by default)
+};
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
                        uint32_t* d_sa_final, SortStats* st, bool reserve_only = false,
-                       uint64_t payload_limit = kPayloadLimit);
+                       const SortOpts& opts = SortOpts());
 
 // ranks.cu -- A3 ComputeRanks (Lemma 1, Alg.2) and the
 // fused A2/A4 extraction + gather (Alg.1).

@@ -85,7 +85,18 @@ struct Bufs {
     const uint32_t* term;
     uint64_t base;
     uint32_t smask;  // slot bits of an SA entry (sa_slot_mask); ~0 without payload
+    const uint32_t* kw1;  // key word 1 per block-local slot, or null
 };
+
+// Key word `word` of the suffix of an SA entry.  Large blocks precompute word
+// 1 for every slot in one sequential pass (kw1): their word-0 ties are common
+// (134 M suffixes against 4^14 windows in c3; nearly all in c4), and one 4-byte
+// read replaces two random text/terminator lookups.
+__device__ __forceinline__ uint32_t key_of(const Bufs& B, uint32_t entry, uint32_t word) {
+    const uint32_t sl = entry & B.smask;
+    if (word == 1 && B.kw1) return __ldg(B.kw1 + sl);
+    return suffix_key(B.text, B.term, B.base + sl, word);
+}
 
 // SA entry of block-local slot sl: the slot plus, with payload, its B_int
 // symbol (the symbol before the suffix, or 4 = '$' at a string start).
@@ -170,7 +181,7 @@ __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint3
     uint32_t group = active ? group0 : lane;
     for (;;) {
         uint32_t key = 0;
-        if (active) key = have_key ? key0 : suffix_key(B.text, B.term, B.base + (slot & B.smask), word);
+        if (active) key = have_key ? key0 : key_of(B, slot, word);
         have_key = false;
         // group extents: [group, gend)
         const uint32_t starts = __ballot_sync(0xFFFFFFFFu, group == lane);
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
                     key[u] = 0;
                     if (p < ch.end) {
                         const uint32_t sl = meta_iota(s.meta) ? p : __ldg(S + p);
-                        key[u] = suffix_key(B.text, B.term, B.base + (sl & B.smask), s.word);
+                        key[u] = key_of(B, sl, s.word);
                         K[p] = key[u];
                     }
                 }
@@ -1181,7 +1192,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
             if ((uint32_t)it < nit && e < L) {
                 slot[it] = S[s.start + e];
                 key[it] = kv ? B.key[bid][s.start + e]
-                             : suffix_key(B.text, B.term, B.base + (slot[it] & B.smask), s.word);
+                             : key_of(B, slot[it], s.word);
             }
         }
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1377,7 +1388,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
         for (uint32_t i = tid; i < len; i += NT) {
             const uint32_t sl = S[s.start + i];
             slotA[i] = sl;
-            keyA[i] = kv ? B.key[buf][s.start + i] : suffix_key(B.text, B.term, B.base + (sl & B.smask), s.word);
+            keyA[i] = kv ? B.key[buf][s.start + i] : key_of(B, sl, s.word);
         }
         __syncthreads();
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1475,16 +1486,16 @@ __global__ void strip_payload_kernel(uint32_t* sa, uint32_t n) {
 
 using namespace sortk;
 
-cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf) {
+cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf, const SortOpts& opts) {
     Profiler dummy;
     (void)dummy;
-    return sort_block(dummy, nullptr, ws, nullptr, nullptr, 0, n_suf, nullptr, nullptr, true);
+    return sort_block(dummy, nullptr, ws, nullptr, nullptr, 0, n_suf, nullptr, nullptr, true, opts);
 }
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
                        uint32_t* d_sa_final, SortStats* st, bool reserve_only,
-                       uint64_t payload_limit) {
+                       const SortOpts& opts) {
     if (n_suf == 0) return cudaSuccess;
     const size_t n = n_suf;
     const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
@@ -1527,6 +1538,10 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         A.cnt = ctr;
         Bl.cnt = ctr + NCLASS;
     }
+    if (n >= opts.kw1_min) {
+        uint32_t* kw1;
+        SB_CHECK(ensure(ws.kw1, n + 16, &kw1));
+    }
     if (reserve_only) return cudaSuccess;
     Bufs B;
     B.sa[0] = sa0;
@@ -1537,7 +1552,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.text = text;
     B.term = term;
     B.base = slot_base;
-    B.smask = sa_slot_mask(n_suf, payload_limit);
+    B.smask = sa_slot_mask(n_suf, opts.payload_limit);
+    B.kw1 = nullptr;
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
@@ -1553,6 +1569,15 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
 
+    if (n >= opts.kw1_min) {
+        uint32_t* kw1;
+        SB_CHECK(ensure(ws.kw1, n + 16, &kw1));  // reserved by sort_reserve
+        SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
+                  keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(
+                      text, term, slot_base + kKeySyms, n_suf, kw1));
+        SB_CHECK(cudaGetLastError());
+        B.kw1 = kw1;
+    }
     if (n <= kCapM) {
         SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
                   keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(

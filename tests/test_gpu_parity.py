@@ -524,3 +524,27 @@ def test_c1_u64_g_without_payload(SetBWTE, c1):
     idx.set_option("sa_payload", 0)
     idx.append(d, o)
     assert idx.bwt() == want
+
+
+@pytest.mark.parametrize("payload", [0, 1])
+@pytest.mark.parametrize("kind", ["all_A", "AC_repeat", "staircase", "uniform"])
+def test_precomputed_word1_keys(SetBWTE, kind, payload):
+    """Blocks that precompute key word 1 (forced with kw1_min = 1) on
+    tie-heavy inputs; results must not change."""
+    if kind == "uniform":
+        d, o = synth.random_set(15000, max_m=64, max_len=80)
+    else:
+        d, o = synth.adversarial(kind, 40, 70)
+    idx = SetBWTE(A, block_suffixes=500)
+    idx.set_option("kw1_min", 1)
+    idx.set_option("sa_payload", payload)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+def test_genome_precomputed_word1_keys(SetBWTE):
+    d, o = synth.genome_sampled(3000, 120, 60000, seed=5)
+    idx = SetBWTE(A, block_suffixes=90000)
+    idx.set_option("kw1_min", 1)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o, threads=None)

@@ -16,8 +16,11 @@ ap.add_argument("--len", type=int, default=100)
 ap.add_argument("--M", type=int, default=1 << 24)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--genome", type=int, default=0)
+ap.add_argument("--var", action="store_true", help="c4-style read lengths U[1000, 10000]")
 a = ap.parse_args()
-if a.genome:
+if a.var:
+    d, o = synth.uniform_var(a.reads, 1000, 10000, seed=1)
+elif a.genome:
     d, o = synth.genome_sampled(a.reads, a.len, a.genome, seed=1)
 else:
     d, o = synth.uniform(a.reads, a.len, seed=1)
