@@ -204,9 +204,12 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     per slot instead).  Results are identical; the option
  *                     exists so both paths can be tested at small sizes.
  *   "kw1_min"         blocks of at least this many suffixes (default: none)
- *                     precompute key word 1 of every slot in one sequential
- *                     pass, so resolving word-0 ties reads one 4-byte key
- *                     instead of two random text lookups.  Results identical.
+ *                     carry key word 1 with every element through the digit
+ *                     passes (generated in one sequential pass), so resolving
+ *                     a word-0 tie reads the element's own word-1 key instead
+ *                     of two random text lookups.  Results identical; measured
+ *                     slower on c3 (the wider scatter costs more than the
+ *                     lookups it saves), hence off by default.
  *   "insert_split"    1: with setbwte_set_partition world > 1 and B_ext in HBM,
  *                     Insert is split by output range (rank r merges output
  *                     superblocks [nsb*r/P, nsb*(r+1)/P)) and the new

@@ -120,7 +120,7 @@ cudaError_t launch_slices(Profiler& prof, cudaStream_t s, const uint64_t* d_slot
 // sort.cu -- A1 ConstructSA (Sec.3).
 struct SortScratch {
     DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr, gtot, groups;
-    DevBuf kw1;  // key word 1 of every slot (large blocks only)
+    DevBuf kw1, kw1b;  // key word 1 in position order, ping-pong (large blocks only)
 };
 struct SortStats {
     uint64_t digit_passes = 0;

@@ -85,17 +85,12 @@ struct Bufs {
     const uint32_t* term;
     uint64_t base;
     uint32_t smask;  // slot bits of an SA entry (sa_slot_mask); ~0 without payload
-    const uint32_t* kw1;  // key word 1 per block-local slot, or null
+    uint32_t* key1[2];  // key word 1 in position order (large blocks), or null
 };
 
-// Key word `word` of the suffix of an SA entry.  Large blocks precompute word
-// 1 for every slot in one sequential pass (kw1): their word-0 ties are common
-// (134 M suffixes against 4^14 windows in c3; nearly all in c4), and one 4-byte
-// read replaces two random text/terminator lookups.
+// Key word `word` of the suffix of an SA entry (text lookups).
 __device__ __forceinline__ uint32_t key_of(const Bufs& B, uint32_t entry, uint32_t word) {
-    const uint32_t sl = entry & B.smask;
-    if (word == 1 && B.kw1) return __ldg(B.kw1 + sl);
-    return suffix_key(B.text, B.term, B.base + sl, word);
+    return suffix_key(B.text, B.term, B.base + (entry & B.smask), word);
 }
 
 // SA entry of block-local slot sl: the slot plus, with payload, its B_int
@@ -111,9 +106,15 @@ __device__ __forceinline__ uint32_t meta_shift(uint32_t m) { return m & 0xFF; }
 __device__ __forceinline__ uint32_t meta_buf(uint32_t m) { return (m >> 8) & 1; }
 __device__ __forceinline__ uint32_t meta_kv(uint32_t m) { return (m >> 9) & 1; }
 __device__ __forceinline__ uint32_t meta_iota(uint32_t m) { return (m >> 10) & 1; }
+// k1bad: the segment's elements were reordered without their key-1 words
+__device__ __forceinline__ uint32_t meta_k1bad(uint32_t m) { return (m >> 11) & 1; }
 __device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint32_t kv,
-                                              uint32_t iota = 0) {
-    return shift | (buf << 8) | (kv << 9) | (iota << 10);
+                                              uint32_t iota = 0, uint32_t k1bad = 0) {
+    return shift | (buf << 8) | (kv << 9) | (iota << 10) | (k1bad << 11);
+}
+// key word 1 of the element at position pos of buffer buf, when carried
+__device__ __forceinline__ bool k1_ok(const Bufs& B, uint32_t meta) {
+    return B.key1[0] != nullptr && !meta_k1bad(meta);
 }
 __host__ __device__ __forceinline__ int class_of(const Seg& c) {
     if (c.len <= kTiny) return TINY;
@@ -536,7 +537,8 @@ __global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chun
                     key[u] = 0;
                     if (p < ch.end) {
                         const uint32_t sl = meta_iota(s.meta) ? p : __ldg(S + p);
-                        key[u] = key_of(B, sl, s.word);
+                        key[u] = (s.word == 1 && k1_ok(B, s.meta)) ? B.key1[buf][p]
+                                                                    : key_of(B, sl, s.word);
                         K[p] = key[u];
                     }
                 }
@@ -640,10 +642,10 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
                 c.len = total;
                 if (shift == 0) {
                     c.word = s.word + 1;
-                    c.meta = make_meta(24, cbuf, 0, ciota);
+                    c.meta = make_meta(24, cbuf, 0, ciota, meta_k1bad(s.meta));
                 } else {
                     c.word = s.word;
-                    c.meta = make_meta(shift - 8, cbuf, 1, ciota);
+                    c.meta = make_meta(shift - 8, cbuf, 1, ciota, meta_k1bad(s.meta));
                 }
                 cls = class_of(c);
                 local = atomicAdd(&ccount[cls], 1u);
@@ -679,17 +681,23 @@ struct Tile {
     uint32_t c, t0, end;  // chunk, first element, chunk end
 };
 
+// IPT items per thread (tile = kDigNt * IPT); K1: the segment data also
+// carries key word 1 (B.key1), moved with the key and the slot
+template <int IPT, bool K1>
 __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     Lists in, const SegX* __restrict__ segx, const Chunk* __restrict__ chunks, const uint32_t* misc,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gtot,
     const uint32_t* __restrict__ dbase, Bufs B) {
     constexpr int NW = kDigNt / 32;
+    constexpr int TILE = kDigNt * IPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);  // NW*256
-    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + NW * 256);  // kDigTile (key, slot)
-    uint32_t* s_ink = reinterpret_cast<uint32_t*>(s_kv + kDigTile);  // kDigTile: next tile's keys
-    uint32_t* s_ins = s_ink + kDigTile;                               // kDigTile: next tile's slots
-    uint32_t* dstart = s_ins + kDigTile;                      // 257
+    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + NW * 256);  // TILE (key, slot)
+    uint32_t* s_ink = reinterpret_cast<uint32_t*>(s_kv + TILE);  // TILE: next tile's keys
+    uint32_t* s_ins = s_ink + TILE;                              // TILE: next tile's slots
+    uint32_t* s_in1 = s_ins + TILE;                              // TILE (K1): next tile's word-1 keys
+    uint32_t* s_k1 = s_in1 + (K1 ? TILE : 0);                    // TILE (K1): staged word-1 keys
+    uint32_t* dstart = s_k1 + (K1 ? TILE : 0);                   // 257
     uint32_t* run_base = dstart + 260;                        // 256
     uint32_t* off = run_base + 256;                           // 256: run_base - dstart
     uint32_t* tmp = off + 256;                                // 32
@@ -711,23 +719,25 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
         return Tile{nch, 0u, 0u};
     };
     auto next_tile = [&](const Tile& t) -> Tile {
-        if (t.t0 + kDigTile < t.end) return Tile{t.c, t.t0 + kDigTile, t.end};
+        if (t.t0 + TILE < t.end) return Tile{t.c, t.t0 + TILE, t.end};
         return first_tile(t.c + gridDim.x);
     };
     auto prefetch = [&](const Tile& t) {
         if (t.c >= nch) return;
         const Seg s = in.seg[LARGE][chunks[t.c].seg];
         const uint32_t buf = meta_buf(s.meta);
-        const uint32_t tn = min((uint32_t)kDigTile, t.end - t.t0);
+        const uint32_t tn = min((uint32_t)TILE, t.end - t.t0);
         const uint32_t* K = B.key[buf] + t.t0;
         const uint32_t* S = B.sa[buf] + t.t0;
+        const uint32_t* K1s = K1 ? B.key1[buf] + t.t0 : nullptr;
         const bool iota = meta_iota(s.meta);
 #pragma unroll
-        for (int it = 0; it < kDigIpt; ++it) {
-            const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
+        for (int it = 0; it < IPT; ++it) {
+            const uint32_t e = warp * (32 * IPT) + it * 32 + lane;
             if (e < tn) {
                 cp_async4(s_ink + e, K + e, pol_ef);
                 if (!iota) cp_async4(s_ins + e, S + e, pol_ef);
+                if (K1) cp_async4(s_in1 + e, K1s + e, pol_ef);
             }
         }
         cp_async_commit();
@@ -758,16 +768,18 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
         }
         uint32_t* S2 = B.sa[1 - buf];
         uint32_t* K2 = B.key[1 - buf];
+        uint32_t* K12 = K1 ? B.key1[1 - buf] : nullptr;
         const uint32_t t0 = cur.t0;
-        const uint32_t tn = min((uint32_t)kDigTile, cur.end - t0);
-        uint32_t key[kDigIpt], slot[kDigIpt], dig[kDigIpt], dest[kDigIpt];
+        const uint32_t tn = min((uint32_t)TILE, cur.end - t0);
+        uint32_t key[IPT], slot[IPT], dig[IPT], dest[IPT], k1v[K1 ? IPT : 1];
         cp_async_wait_all();
 #pragma unroll
-        for (int it = 0; it < kDigIpt; ++it) {
-            const uint32_t e = warp * (32 * kDigIpt) + it * 32 + lane;
+        for (int it = 0; it < IPT; ++it) {
+            const uint32_t e = warp * (32 * IPT) + it * 32 + lane;
             const bool valid = e < tn;
             key[it] = valid ? s_ink[e] : 0u;
             slot[it] = valid ? (iota ? t0 + e : s_ins[e]) : 0u;
+            if (K1) k1v[K1 ? it : 0] = valid ? s_in1[e] : 0u;
             dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
         }
         if (iota && B.smask != 0xFFFFFFFFu) {
@@ -777,11 +789,11 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             // comes from the neighbouring lane (or the warp's previous tile
             // element), no text lookups.
             if (word_of_setup == 0) {
-                const uint32_t e0 = warp * (32 * kDigIpt);
+                const uint32_t e0 = warp * (32 * IPT);
                 uint32_t carry = 0;
                 if (lane == 0 && e0 < tn && t0 + e0 > 0) carry = B.key[buf][t0 + e0 - 1];
 #pragma unroll
-                for (int it = 0; it < kDigIpt; ++it) {
+                for (int it = 0; it < IPT; ++it) {
                     const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, key[it], 1);
                     const uint32_t last = __shfl_sync(0xFFFFFFFFu, key[it], 31);
                     const uint32_t pk = lane == 0 ? carry : up;
@@ -792,19 +804,22 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
                 }
             } else {
 #pragma unroll
-                for (int it = 0; it < kDigIpt; ++it) slot[it] = sa_entry(B, slot[it]);
+                for (int it = 0; it < IPT; ++it) slot[it] = sa_entry(B, slot[it]);
             }
         }
         cur = next_tile(cur);
         prefetch(cur);
-        block_rank<kDigNt, kDigIpt>(dig, dest, wcnt, dstart, tmp);
+        block_rank<kDigNt, IPT>(dig, dest, wcnt, dstart, tmp);
         if (tid < 256) {
             off[tid] = run_base[tid] - dstart[tid];  // mod 2^32
             run_base[tid] += dstart[tid + 1] - dstart[tid];
         }
 #pragma unroll
-        for (int it = 0; it < kDigIpt; ++it)
-            if (dig[it] < 256) s_kv[dest[it]] = make_uint2(key[it], slot[it]);
+        for (int it = 0; it < IPT; ++it)
+            if (dig[it] < 256) {
+                s_kv[dest[it]] = make_uint2(key[it], slot[it]);
+                if (K1) s_k1[dest[it]] = k1v[K1 ? it : 0];
+            }
         __syncthreads();
         // coalesced write-out: consecutive tile positions of one digit go to
         // consecutive global positions.  The next tile's block_rank barriers
@@ -818,14 +833,16 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             } else {
                 __stcs(S2 + gp, kv.y);
                 __stcs(K2 + gp, kv.x);
+                if (K1) __stcs(K12 + gp, s_k1[i]);
             }
         }
     }
 }
 
+template <int IPT, bool K1>
 constexpr size_t scatter_smem() {
-    return (size_t)(kDigNt / 32) * 256 * 4 + 4 * (size_t)kDigTile * 4 + 260 * 4 + 2 * 256 * 4 +
-           32 * 4 + 256 + 16;
+    return (size_t)(kDigNt / 32) * 256 * 4 + (K1 ? 6 : 4) * (size_t)(kDigNt * IPT) * 4 + 260 * 4 +
+           2 * 256 * 4 + 32 * 4 + 256 + 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -839,7 +856,8 @@ constexpr uint32_t kTinyPerWarp = 32;  // list entries per warp, packed into sha
 // this word with 14 real symbols and `run` the first lane of their tie run.
 __device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint32_t grp,
                                                 uint32_t key, uint32_t rb, bool& tie,
-                                                uint32_t& run) {
+                                                uint32_t& run, uint32_t& x) {
+    // x: a per-element value permuted along with the slot
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = lane < L;
     const uint32_t rmask = (1u << rb) - 1u;
@@ -861,6 +879,7 @@ __device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint3
     const uint32_t src = v & 31u;
     const uint32_t s2 = __shfl_sync(0xFFFFFFFFu, slot, src);
     const uint32_t k2 = __shfl_sync(0xFFFFFFFFu, key, src);
+    x = __shfl_sync(0xFFFFFFFFu, x, src);
     const uint32_t hi = v >> 5;
     const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
     const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, hi, 1);
@@ -882,8 +901,8 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
         // pack consecutive segments into the 32 lanes; each lane remembers its
         // segment's output position, start word and key (a segment keeps its
         // lanes through the sort: the composite sorts by group first)
-        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0, rb = 0;
-        bool mine = false, kv = false, fast = true;
+        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0, rb = 0, k1 = 0;
+        bool mine = false, kv = false, fast = true, k1v = false;
         // all of the warp's list entries in one coalesced load (lane l holds
         // entry i0+l); the packing loop below broadcasts them with shuffles, so
         // it never waits on memory
@@ -904,9 +923,13 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
                     if (__all_sync(0xFFFFFFFFu, fast || lane >= lb)) {
                         bool tie;
                         uint32_t run;
-                        r = warp_sort16(slot, lb, grp, key, rb, tie, run);
+                        uint32_t k1p = k1;
+                        r = warp_sort16(slot, lb, grp, key, rb, tie, run, k1p);
+                        // ties continue on word+1; word 1 comes from the carried
+                        // key-1 words (permuted with the slots; the flag is the
+                        // same for every lane of a segment)
                         if (__any_sync(0xFFFFFFFFu, tie))
-                            r = warp_finish(r, lb, word + 1, 0u, false, B, run, tie);
+                            r = warp_finish(r, lb, word + 1, k1p, k1v && word == 0, B, run, tie);
                     } else {
                         r = warp_finish(slot, lb, word, key, kv, B, grp);
                     }
@@ -926,6 +949,12 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
                 kv = meta_kv(sg.meta);
                 slot = B.sa[bf][dst];
                 key = kv ? B.key[bf][dst] : 0u;
+                k1v = k1_ok(B, sg.meta) && (sg.word == 0 || (sg.word == 1 && !kv));
+                k1 = k1v ? B.key1[bf][dst] : 0u;
+                if (sg.word == 1 && !kv && k1v) {
+                    key = k1;  // the word-1 key of a segment at word 1
+                    kv = true;
+                }
                 grp = lb;
                 rb = meta_shift(sg.meta) + 8;
                 fast = kv && meta_shift(sg.meta) <= 8;
@@ -989,7 +1018,7 @@ __device__ __forceinline__ void warp_tail(const uint2* buf, const Seg& s, const 
                     lb += Lr;
                 } else {
                     for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = buf[rs + q].y;
-                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0, 0, 1)});
                 }
             }
         }
@@ -1122,7 +1151,9 @@ __global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists 
             uint32_t w = x - c;
 #pragma unroll
             for (int r = 0; r < NIT; ++r)
-                if ((tb >> r) & 1u) tl[w++] = (lane * NIT + r) | (((eqp >> r) & 1u) ? 0u : 0x80000000u);
+                if ((tb >> r) & 1u)
+                    tl[w++] = (lane * NIT + r) | ((v[r] & (N - 1)) << 16) |
+                              (((eqp >> r) & 1u) ? 0u : 0x80000000u);
             __syncwarp();
             // batches of whole runs through warp_finish on the next word
             for (uint32_t b = 0; b < T;) {
@@ -1146,14 +1177,19 @@ __global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists 
                     }
                     const uint32_t rs = tl[b] & 0xFFFFu;
                     for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = sl32[rs + q];
-                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0)});
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0, 0, 1)});
                     b += Lr;
                     continue;
                 }
                 const uint32_t e = te & 0xFFFFu;
                 const uint32_t grp = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
                 uint32_t sl = lane < nb ? sl32[e] : 0u;
-                sl = warp_finish(sl, nb, s.word + 1, 0u, false, B, grp);
+                // word 1 from the carried key-1 words (the element's position
+                // before this sort: bits 16.. of its tie entry)
+                const bool k1 = s.word == 0 && k1_ok(B, s.meta);
+                const uint32_t kk =
+                    (k1 && lane < nb) ? B.key1[bid][s.start + ((te >> 16) & 0x7FFFu)] : 0u;
+                sl = warp_finish(sl, nb, s.word + 1, kk, k1, B, grp);
                 __syncwarp();
                 if (lane < nb) B.saf[s.start + e] = sl;
                 b += nb;
@@ -1192,7 +1228,8 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
             if ((uint32_t)it < nit && e < L) {
                 slot[it] = S[s.start + e];
                 key[it] = kv ? B.key[bid][s.start + e]
-                             : key_of(B, slot[it], s.word);
+                             : (s.word == 1 && k1_ok(B, s.meta)) ? B.key1[bid][s.start + e]
+                                                                 : key_of(B, slot[it], s.word);
             }
         }
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1388,7 +1425,9 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
         for (uint32_t i = tid; i < len; i += NT) {
             const uint32_t sl = S[s.start + i];
             slotA[i] = sl;
-            keyA[i] = kv ? B.key[buf][s.start + i] : key_of(B, sl, s.word);
+            keyA[i] = kv ? B.key[buf][s.start + i]
+                         : (s.word == 1 && k1_ok(B, s.meta)) ? B.key1[buf][s.start + i]
+                                                             : key_of(B, sl, s.word);
         }
         __syncthreads();
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1470,7 +1509,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
                 if (lane < rr.y) B.saf[s.start + rr.x + lane] = sl;
             } else {
                 for (uint32_t q = lane; q < rr.y; q += 32) S[s.start + rr.x + q] = slotA[rr.x + q];
-                if (lane == 0) emit(out, Seg{s.start + rr.x, rr.y, s.word + 1, make_meta(24, buf, 0)});
+                if (lane == 0) emit(out, Seg{s.start + rr.x, rr.y, s.word + 1, make_meta(24, buf, 0, 0, 1)});
             }
         }
         __syncthreads();
@@ -1541,6 +1580,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     if (n >= opts.kw1_min) {
         uint32_t* kw1;
         SB_CHECK(ensure(ws.kw1, n + 16, &kw1));
+        SB_CHECK(ensure(ws.kw1b, n + 16, &kw1));
     }
     if (reserve_only) return cudaSuccess;
     Bufs B;
@@ -1553,7 +1593,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.term = term;
     B.base = slot_base;
     B.smask = sa_slot_mask(n_suf, opts.payload_limit);
-    B.kw1 = nullptr;
+    B.key1[0] = B.key1[1] = nullptr;
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
@@ -1563,20 +1603,29 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m1));
     SB_CHECK(cudaFuncSetAttribute(local_kernel<2048, 256>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m2));
-    constexpr size_t sm_d = scatter_smem();
+    constexpr size_t sm_d = scatter_smem<kDigIpt, false>();
+    constexpr size_t sm_d1 = scatter_smem<4, true>();
     SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
-    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel,
+    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<kDigIpt, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
+    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<4, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d1));
 
     if (n >= opts.kw1_min) {
-        uint32_t* kw1;
-        SB_CHECK(ensure(ws.kw1, n + 16, &kw1));  // reserved by sort_reserve
+        // large blocks carry key word 1 with every element through the digit
+        // passes (B.key1, position order): resolving a word-0 tie then reads
+        // the element's own word-1 key, not two random text lookups.  Key
+        // word 1 of slot i is key word 0 of slot i + 14.
+        uint32_t *k1a, *k1b;
+        SB_CHECK(ensure(ws.kw1, n + 16, &k1a));  // reserved by sort_reserve
+        SB_CHECK(ensure(ws.kw1b, n + 16, &k1b));
         SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
                   keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(
-                      text, term, slot_base + kKeySyms, n_suf, kw1));
+                      text, term, slot_base + kKeySyms, n_suf, k1a));
         SB_CHECK(cudaGetLastError());
-        B.kw1 = kw1;
+        B.key1[0] = k1a;
+        B.key1[1] = k1b;
     }
     if (n <= kCapM) {
         SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
@@ -1662,9 +1711,15 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                       digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 8u), 256, 0, s>>>(
                           in, out, segx, gtot, dbase));
             SB_CHECK(cudaGetLastError());
-            SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
-                      digit_scatter_kernel<<<g_dig, kDigNt, sm_d, s>>>(in, segx, chunks, misc, hist,
-                                                                      gtot, dbase, B));
+            if (B.key1[0]) {
+                SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
+                          (digit_scatter_kernel<4, true><<<g_dig, kDigNt, sm_d1, s>>>(
+                              in, segx, chunks, misc, hist, gtot, dbase, B)));
+            } else {
+                SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
+                          (digit_scatter_kernel<kDigIpt, false><<<g_dig, kDigNt, sm_d, s>>>(
+                              in, segx, chunks, misc, hist, gtot, dbase, B)));
+            }
             SB_CHECK(cudaGetLastError());
         }
         SB_LAUNCH(prof, s, "sort_ctl", 0, 0, reset_counts_kernel<<<1, 32, 0, s>>>(in.cnt, misc));

@@ -548,3 +548,27 @@ def test_genome_precomputed_word1_keys(SetBWTE):
     idx.set_option("kw1_min", 1)
     idx.append(d, o)
     assert idx.bwt() == oracle.bwt(A, d, o, threads=None)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_sets_carried_word1(SetBWTE, seed):
+    """Key word 1 carried through the digit passes (kw1_min = 1) on random
+    sets with small blocks, both SA layouts and g widths."""
+    d, o = synth.random_set(16000 + seed, max_m=64, max_len=90, alphabet=["ACGT", "AC", "A"][seed % 3])
+    rng = np.random.default_rng(seed)
+    idx = SetBWTE(A, block_suffixes=int(rng.integers(40, 3000)))
+    idx.set_option("kw1_min", 1)
+    idx.set_option("sa_payload", seed % 2)
+    if seed % 4 == 3:
+        idx.set_option("g_width", 8)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+def test_c1_carried_word1(SetBWTE, c1):
+    d, o, want = c1
+    for M in (25250, 101000):
+        idx = SetBWTE(A, block_suffixes=M)
+        idx.set_option("kw1_min", 1)
+        idx.append(d, o)
+        assert idx.bwt() == want
