@@ -185,7 +185,8 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     Default 2^24.
  *   "profile"         1: time every kernel launch with CUDA events on the
  *                     handle's stream (reported by setbwte_stats); 0: off.
- *   "rank_ilp"        strings per thread in the ComputeRanks kernel (1..4).
+ *   "rank_ilp"        1 (default): one string per ComputeRanks thread; 2..4:
+ *                     four strings per thread, their LF steps interleaved.
  *   "sort_lanes"      host threads (each with its own CUDA stream) running
  *                     ConstructSA of upcoming blocks ahead of the in-order
  *                     rank/insert stage (the stage pipeline of P:190-191):

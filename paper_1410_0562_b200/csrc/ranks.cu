@@ -111,18 +111,82 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
     }
 }
 
+// ComputeRanks with K independent strings per thread, their LF steps
+// interleaved so K dictionary loads are in flight per thread.  For the host
+// tier: the dictionary is read zero-copy over PCIe, whose latency needs more
+// requests in flight than there are resident threads (one string each).
+template <class G, int K>
+__global__ void __launch_bounds__(256) compute_ranks_ilp_kernel(
+    const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
+    uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g) {
+    const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t jb = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jb < j1;
+         jb += nthr * K) {
+        uint64_t i[K], lp[K], l0[K], wi[K];
+        uint32_t word[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint64_t j = jb + (uint64_t)k * nthr;
+            wi[k] = ~0ull;
+            word[k] = 0;
+            i[k] = m_ext;
+            if (j < j1) {
+                l0[k] = slot_off[j] - slot_base;
+                lp[k] = slot_off[j + 1] - 1 - slot_base;  // the terminator
+                g[lp[k]] = (G)m_ext;
+            } else {
+                l0[k] = lp[k] = 0;
+            }
+        }
+        for (;;) {
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (lp[k] > l0[k]) {
+                    any = true;
+                    const uint64_t q = --lp[k];
+                    const uint64_t p = q + slot_base;
+                    if ((p >> 4) != wi[k]) {
+                        wi[k] = p >> 4;
+                        word[k] = __ldg(text + wi[k]);
+                    }
+                    const uint32_t c = (word[k] >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
+                    const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
+                    i[k] = Cc + dict_rank(blk, sb, c, i[k]);
+                    g[q] = (G)i[k];
+                }
+            }
+            if (!any) break;
+        }
+    }
+}
+
 cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Blk* blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
                                  int gw, int ilp, uint8_t* bslot, bool bing) {
-    (void)ilp;
     if (j1 <= j0) return cudaSuccess;
     // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
     // superblock counter + g write + 0.25 B packed symbol; per string: 16 B
     // slot offsets + the terminator g.  Units = LF steps.
     const uint64_t nstr = j1 - j0;
     const double bytes = (40.25 + gw) * (double)n_steps + (16.0 + gw) * (double)nstr;
+    if (ilp > 1 && !bslot && !bing) {
+        const unsigned gi = grid_for((nstr + 3) / 4, 256, 1u << 20);
+        if (gw == 4) {
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_ilp_kernel<uint32_t, 4><<<gi, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g)));
+        } else {
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_ilp_kernel<uint64_t, 4><<<gi, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g)));
+        }
+        return cudaGetLastError();
+    }
     const unsigned grid = grid_for(nstr, 256, 1u << 20);
     if (gw == 4) {
         SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,

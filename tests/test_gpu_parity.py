@@ -572,3 +572,19 @@ def test_c1_carried_word1(SetBWTE, c1):
         idx.set_option("kw1_min", 1)
         idx.append(d, o)
         assert idx.bwt() == want
+
+
+@pytest.mark.parametrize("budget", [1 << 40, 1])
+@pytest.mark.parametrize("seed", range(4))
+def test_rank_ilp(SetBWTE, seed, budget):
+    """ComputeRanks with 4 interleaved strings per thread (rank_ilp), HBM and
+    host-tier dictionaries."""
+    d, o = synth.random_set(17000 + seed, max_m=64, max_len=70)
+    rng = np.random.default_rng(seed)
+    idx = SetBWTE(A, block_suffixes=int(rng.integers(30, 600)))
+    idx.set_option("rank_ilp", 4)
+    idx.set_option("hbm_budget_bytes", budget)
+    if seed % 2:
+        idx.set_option("g_width", 8)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
