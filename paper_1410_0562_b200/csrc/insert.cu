@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
         }
         __syncthreads();
         if (wvalid) {
+            SB_ASSERT(((sbi << (kSbShift - 6)) + tid) <= (n_out >> 6));
             uint64_t w0 = 0;
 #pragma unroll
             for (int c = 0; c < 4; ++c)

@@ -69,6 +69,22 @@ struct Profiler {
         (prof).end(name, stream, _ev);                                      \
     } while (0)
 
+// Device-side bounds checks of the debug build (tools/variant.sh dbg ...
+// "-DSB_DEBUG"): a failed check prints and traps, so the launch fails loudly.
+#ifdef SB_DEBUG
+#define SB_ASSERT(cond)                                                               \
+    do {                                                                              \
+        if (!(cond)) {                                                                \
+            printf("SB_ASSERT failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);      \
+            __trap();                                                                 \
+        }                                                                             \
+    } while (0)
+#else
+#define SB_ASSERT(cond) \
+    do {                \
+    } while (0)
+#endif
+
 #define SB_CHECK(expr)                             \
     do {                                           \
         cudaError_t _e = (expr);                   \

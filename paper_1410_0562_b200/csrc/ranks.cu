@@ -221,6 +221,7 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
             // streaming (evict-first) SA / pos / B_int accesses leave L2 to g
             const uint32_t e = __ldcs(sa + i);
             const uint32_t sl = e & smask;
+            SB_ASSERT(sl < n_suf);
             uint64_t gv = g ? (uint64_t)__ldg(g + sl) : 0ull;
             const uint8_t bg = (uint8_t)(gv >> 56);
             if (bing) gv &= (1ull << 56) - 1ull;

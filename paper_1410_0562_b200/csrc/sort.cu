@@ -86,6 +86,7 @@ struct Bufs {
     uint64_t base;
     uint32_t smask;  // slot bits of an SA entry (sa_slot_mask); ~0 without payload
     uint32_t* key1[2];  // key word 1 in position order (large blocks), or null
+    uint32_t n;         // suffixes of the block (debug bounds checks)
 };
 
 // Key word `word` of the suffix of an SA entry (text lookups).
@@ -829,6 +830,7 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             const uint32_t d = (kv.x >> shift) & 0xFFu;
             const uint32_t gp = off[d] + i;
             if (fin[d]) {
+                SB_ASSERT(gp < B.n);
                 __stcs(B.saf + gp, kv.y);
             } else {
                 __stcs(S2 + gp, kv.y);
@@ -933,6 +935,7 @@ __global__ void __launch_bounds__(256) tiny_kernel(Lists in, Bufs B, uint32_t* m
                     } else {
                         r = warp_finish(slot, lb, word, key, kv, B, grp);
                     }
+                    SB_ASSERT(!mine || dst < B.n);
                     if (mine) B.saf[dst] = r;
                 }
                 lb = 0;
@@ -1191,6 +1194,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) bitonic_kernel(Lists in, Lists 
                     (k1 && lane < nb) ? B.key1[bid][s.start + ((te >> 16) & 0x7FFFu)] : 0u;
                 sl = warp_finish(sl, nb, s.word + 1, kk, k1, B, grp);
                 __syncwarp();
+                SB_ASSERT(lane >= nb || (e < L && s.start + e < B.n));
                 if (lane < nb) B.saf[s.start + e] = sl;
                 b += nb;
             }
@@ -1489,6 +1493,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
         }
         // write the order; collect tied runs (equal word, 14 real symbols)
         for (uint32_t i = tid; i < len; i += NT) {
+            SB_ASSERT(s.start + i < B.n);
             B.saf[s.start + i] = slotA[i];
             const uint32_t k = keyA[i];
             const bool starts = (i == 0 || keyA[i - 1] != k) && i + 1 < len && keyA[i + 1] == k &&
@@ -1594,6 +1599,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.base = slot_base;
     B.smask = sa_slot_mask(n_suf, opts.payload_limit);
     B.key1[0] = B.key1[1] = nullptr;
+    B.n = n_suf;
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
