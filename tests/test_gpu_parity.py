@@ -588,3 +588,24 @@ def test_rank_ilp(SetBWTE, seed, budget):
         idx.set_option("g_width", 8)
     idx.append(d, o)
     assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+@pytest.mark.parametrize("lanes", [0, 1, 2])
+def test_pipeline_depth_does_not_change_the_result(SetBWTE, c1, lanes):
+    """SPEC acceptance 8 (determinism across pipeline depth): the sort lanes
+    only reorder work, never the result."""
+    d, o, want = c1
+    idx = SetBWTE(A, block_suffixes=7000)
+    idx.set_option("sort_lanes", lanes)
+    idx.append(d, o)
+    assert idx.bwt() == want
+
+
+def test_option_validation(SetBWTE):
+    idx = SetBWTE(A)
+    for key, bad in [("block_suffixes", 0), ("rank_ilp", 9), ("g_width", 5), ("sa_payload", 2),
+                     ("insert_split", 3), ("kw1_min", 0), ("no_such_option", 1)]:
+        with pytest.raises(Exception):
+            idx.set_option(key, bad)
+    idx.append_strings(["ACGT"])
+    assert idx.bwt().decode() == "T$ACG"
