@@ -417,7 +417,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000.0 * t / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            # integer path: 2-bit symbols, u32 ranks / positions while the index
+            # has < 2^32 symbols (u64 beyond)
+            "dtype": "u32" if n_total < (1 << 32) else "u64", "data": "synthetic",
             "config": {"workload": desc, "reads": m, "bases": bases, "block_suffixes": M,
                        "host_tier": bool(idx.stats().get("host_tier")),
                        "blocks": blocks, "parallelism": "dp%d (ComputeRanks split by string)" % world,
