@@ -47,6 +47,12 @@ static void free_buf(DevBuf& b) {
     b.cap = 0;
 }
 
+void SortScratch::free_all() {
+    for (DevBuf* b : {&sa0, &sa1, &k0, &k1, &segs_a, &segs_b, &small_a, &small_b, &chunks, &hist,
+                      &ctr, &gtot, &groups, &kw1, &kw1b})
+        free_buf(*b);
+}
+
 cudaEvent_t Profiler::get_event() {
     if (!pool.empty()) {
         cudaEvent_t e = pool.back();
@@ -125,12 +131,12 @@ struct setbwte_s {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;       // main stream (user's, or own_stream)
-    cudaStream_t sort_stream = nullptr;   // ConstructSA of upcoming blocks (lane 0)
-    cudaStream_t sort_stream2 = nullptr;  // lane 1
+    static constexpr int kMaxLanes = 4;
+    cudaStream_t lane_stream[kMaxLanes] = {};  // ConstructSA of upcoming blocks, one per sort lane
     cudaStream_t copy_stream = nullptr;   // H2D of an append's bytes + packing, block by block
     std::vector<cudaEvent_t> ev_packed;   // per block: its slots (and the next block's first group) packed
     DevErr* derr_host = nullptr;          // pinned landing spot for the validation result
-    cudaEvent_t ev_start = nullptr, ev_sorted[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_sorted[kMaxLanes] = {}, ev_used[kMaxLanes] = {};
     Profiler prof;
     bool failed = false;
 
@@ -149,12 +155,12 @@ struct setbwte_s {
     // append scratch
     DevBuf in_bytes, in_off, text, term, slot_off, gfirst, bounds, err, small;
     DevBuf saf, g, pos, bint, outbuf, bslot;
-    SortScratch sort, sort2;
+    SortScratch sort[kMaxLanes];  // sort[0] also serves the inline (sort_lanes = 0) path
 
     // options
     uint64_t M = 1ull << 24;
     int rank_ilp = 1;
-    int sort_lanes = 2;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
+    int sort_lanes = 3;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
     uint64_t hbm_budget = ~0ull;  // max bytes of B_ext dictionary kept in HBM
 
     // host tier: B_ext's dictionary in pinned, mapped
@@ -548,24 +554,32 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         max_suf = std::max(max_suf, b.S1 - b.S0);
         total += b.S1 - b.S0;
     }
-    const int NL = (K >= 2 && h->sort_lanes >= 2) ? 2 : 1;  // sort lanes
+    int NL = std::max(1, std::min<int>({h->sort_lanes, (int)K, setbwte_s::kMaxLanes}));
+    {
+        // each lane owns a sort scratch (~30 B per suffix of the largest
+        // block): keep the lanes within half of the free device memory
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const double per_lane = 30.0 * (double)max_suf;
+            while (NL > 1 && per_lane * NL > 0.5 * (double)free_b) --NL;
+        }
+    }
     // reserve everything up front: a cudaFree/cudaMalloc mid-loop would
     // serialise the streams
     uint32_t* saf2;
     uint64_t* tmp;
     uint8_t* tb;
-    API_CHECK(h, ensure(h->saf, 2 * max_suf + 64, &saf2));
+    API_CHECK(h, ensure(h->saf, (size_t)NL * (max_suf + 32) + 64, &saf2));  // one SA_int per lane
     API_CHECK(h, ensure(h->g, max_suf, &tmp));
     API_CHECK(h, ensure(h->pos, max_suf, &tmp));
     API_CHECK(h, ensure(h->bint, max_suf, &tb));
-    API_CHECK(h, sort_reserve(h->sort, (uint32_t)max_suf, h->sopt));
-    if (NL > 1) API_CHECK(h, sort_reserve(h->sort2, (uint32_t)max_suf, h->sopt));
+    for (int l = 0; l < NL; ++l) API_CHECK(h, sort_reserve(h->sort[l], (uint32_t)max_suf, h->sopt));
     const uint64_t n_final = h->n + total;
     API_CHECK(h, ensure(h->sb_tot, ((n_final >> kSbShift) + 1) * 5 + 8, &tmp));
-    SortLane lanes[2];
+    SortLane lanes[setbwte_s::kMaxLanes];
     for (int l = 0; l < NL; ++l) {
-        lanes[l].stream = h->sort_lanes == 0 ? h->stream : l == 0 ? h->sort_stream : h->sort_stream2;
-        lanes[l].ws = l == 0 ? &h->sort : &h->sort2;
+        lanes[l].stream = h->sort_lanes == 0 ? h->stream : h->lane_stream[l];
+        lanes[l].ws = &h->sort[l];
         lanes[l].saf = saf2 + l * (max_suf + 32);
         lanes[l].ev_sorted = h->ev_sorted[l];
         lanes[l].prof.on = h->prof.on;
@@ -581,7 +595,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
                 setbwte_status st0 = validate();
                 if (st0 != SETBWTE_OK) return st0;
             }
-            API_CHECK(h, sort_block(h->prof, h->stream, h->sort, pk.text, pk.term, blocks[k].S0,
+            API_CHECK(h, sort_block(h->prof, h->stream, h->sort[0], pk.text, pk.term, blocks[k].S0,
                                     (uint32_t)(blocks[k].S1 - blocks[k].S0), saf2, &h->sstats,
                                     false, h->sopt));
             setbwte_status st1 = rank_insert_stage(h, pk, blocks[k], saf2);
@@ -889,13 +903,15 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     h->sigma = (int)sigma;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->sort_stream2, cudaStreamNonBlocking);
+    for (int l = 0; l < setbwte_s::kMaxLanes; ++l)
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->lane_stream[l], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->derr_host, sizeof(DevErr), cudaHostAllocDefault);
-    for (cudaEvent_t* ev : {&h->ev_start, &h->ev_sorted[0], &h->ev_sorted[1], &h->ev_used[0],
-                            &h->ev_used[1]})
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
+    for (int l = 0; l < setbwte_s::kMaxLanes; ++l) {
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_sorted[l], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_used[l], cudaEventDisableTiming);
+    }
     h->stream = h->own_stream;
     uint8_t* dc = nullptr;
     uint8_t* ds = nullptr;
@@ -925,24 +941,20 @@ void setbwte_destroy(setbwte_t h) {
     DevBuf* bufs[] = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0], &h->sb[1],
                       &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term, &h->gfirst,
                       &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos, &h->bslot,
-                      &h->bint, &h->outbuf, &h->sort.sa0, &h->sort.sa1, &h->sort.k0,
-                      &h->sort.k1, &h->sort.segs_a, &h->sort.segs_b, &h->sort.small_a,
-                      &h->sort.small_b, &h->sort.chunks, &h->sort.hist, &h->sort.ctr,
-                      &h->sort.gtot, &h->sort.groups, &h->sort2.sa0, &h->sort2.sa1,
-                      &h->sort2.k0, &h->sort2.k1, &h->sort2.segs_a, &h->sort2.segs_b,
-                      &h->sort2.small_a, &h->sort2.small_b, &h->sort2.chunks, &h->sort2.hist,
-                      &h->sort2.ctr, &h->sort2.gtot, &h->sort2.groups};
+                      &h->bint, &h->outbuf};
+    for (SortScratch& ws : h->sort) ws.free_all();
     for (DevBuf* b : bufs) free_buf(*b);
     free_buf(h->stage_in);
     free_buf(h->stage_out);
     if (h->hdict) cudaFreeHost(h->hdict);
-    if (h->sort_stream) cudaStreamSynchronize(h->sort_stream);
-    if (h->sort_stream2) cudaStreamSynchronize(h->sort_stream2);
-    for (cudaEvent_t ev : {h->ev_start, h->ev_sorted[0], h->ev_sorted[1], h->ev_used[0],
-                           h->ev_used[1]})
-        if (ev) cudaEventDestroy(ev);
-    if (h->sort_stream) cudaStreamDestroy(h->sort_stream);
-    if (h->sort_stream2) cudaStreamDestroy(h->sort_stream2);
+    for (cudaStream_t ls : h->lane_stream)
+        if (ls) cudaStreamSynchronize(ls);
+    if (h->ev_start) cudaEventDestroy(h->ev_start);
+    for (int l = 0; l < setbwte_s::kMaxLanes; ++l) {
+        if (h->ev_sorted[l]) cudaEventDestroy(h->ev_sorted[l]);
+        if (h->ev_used[l]) cudaEventDestroy(h->ev_used[l]);
+        if (h->lane_stream[l]) cudaStreamDestroy(h->lane_stream[l]);
+    }
     if (h->copy_stream) {
         cudaStreamSynchronize(h->copy_stream);
         cudaStreamDestroy(h->copy_stream);
@@ -1169,7 +1181,7 @@ setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const u
     API_CHECK(h, ensure(h->pos, n_suf, &pos));
     API_CHECK(h, ensure(h->bint, n_suf, &bint));
     API_CHECK(h, ensure(h->outbuf, n_suf, &asc));
-    API_CHECK(h, sort_block(h->prof, h->stream, h->sort, po.pk.text, po.pk.term, 0,
+    API_CHECK(h, sort_block(h->prof, h->stream, h->sort[0], po.pk.text, po.pk.term, 0,
                             (uint32_t)n_suf, saf, nullptr, false, h->sopt));
     API_CHECK(h, launch_gather(h->prof, h->stream, po.pk.text, po.pk.term, 0, saf, nullptr,
                                (uint32_t)n_suf, pos, 8, bint, nullptr, 0, nullptr,
@@ -1250,7 +1262,7 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;
     } else if (!strcmp(key, "sort_lanes")) {
-        if (value > 2) return SETBWTE_E_INVALID_ARG;
+        if (value > (uint64_t)setbwte_s::kMaxLanes) return SETBWTE_E_INVALID_ARG;
         h->sort_lanes = (int)value;
     } else if (!strcmp(key, "rank_ilp")) {
         if (value < 1 || value > 4) return SETBWTE_E_INVALID_ARG;
