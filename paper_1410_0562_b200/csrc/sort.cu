@@ -28,6 +28,7 @@
 // Ties are only ever broken by slot order, which every pass preserves
 // (stable), so the result is the unique SA of the block (reading R15).
 #include <algorithm>
+#include <cstring>
 
 #include "internal.h"
 
@@ -1731,9 +1732,14 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         SB_LAUNCH(prof, s, "sort_ctl", 0, 0, reset_counts_kernel<<<1, 32, 0, s>>>(in.cnt, misc));
         SB_CHECK(cudaGetLastError());
         std::swap(in, out);
-        SB_CHECK(cudaMemcpyAsync(h_cnt, in.cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
-        SB_CHECK(cudaMemcpyAsync(h_misc, misc, sizeof(h_misc), cudaMemcpyDeviceToHost, s));
+        // one read-back of both count lists and misc (contiguous in ctr); a
+        // pageable destination makes the copy return when the data is here
+        // (its in-driver wait measured faster than pinned + stream sync)
+        uint32_t h_all[2 * NCLASS + M_N];
+        SB_CHECK(cudaMemcpyAsync(h_all, ctr, sizeof(h_all), cudaMemcpyDeviceToHost, s));
         SB_CHECK(cudaStreamSynchronize(s));
+        memcpy(h_cnt, h_all + (in.cnt - ctr), sizeof(h_cnt));
+        memcpy(h_misc, h_all + 2 * NCLASS, sizeof(h_misc));
         if (h_misc[M_ACTIVE] != prev_active) {
             const uint32_t delta = h_misc[M_ACTIVE] - prev_active;
             act_local += delta;
