@@ -181,6 +181,7 @@ struct setbwte_s {
     int rank = 0, world = 1;
     bool insert_split = false;
     SortOpts sopt;                           // options "sa_payload", "kw1_min"
+    SortPattern sort_pattern;                // recorded launch pattern (sopt.pattern)
     int g_width = 0;                         // option "g_width": 0 auto, 8 = always u64
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
@@ -702,6 +703,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         h->prof.total_launches += lanes[l].prof.total_launches;
         h->sstats.digit_passes += lanes[l].st.digit_passes;
         h->sstats.rounds += lanes[l].st.rounds;
+        h->sstats.replayed += lanes[l].st.replayed;
+        h->sstats.after_replay += lanes[l].st.after_replay;
         h->sstats.active_per_pass.insert(h->sstats.active_per_pass.end(),
                                          lanes[l].st.active_per_pass.begin(),
                                          lanes[l].st.active_per_pass.end());
@@ -723,6 +726,8 @@ void build_stats(setbwte_t h) {
              (unsigned long long)(h->hdict_cap * sizeof(Blk)));
     s += buf;
     s += "\"sort\": {\"digit_passes\": " + std::to_string(h->sstats.digit_passes) +
+         ", \"replayed_blocks\": " + std::to_string(h->sstats.replayed) +
+         ", \"rounds_after_replay\": " + std::to_string(h->sstats.after_replay) +
          ", \"active_per_pass\": [";
     for (size_t i = 0; i < h->sstats.active_per_pass.size(); ++i) {
         if (i) s += ", ";
@@ -913,6 +918,7 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_used[l], cudaEventDisableTiming);
     }
     h->stream = h->own_stream;
+    h->sopt.pattern = &h->sort_pattern;
     uint8_t* dc = nullptr;
     uint8_t* ds = nullptr;
     uint64_t* dC = nullptr;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -143,6 +144,8 @@ struct SortStats {
     uint64_t digit_passes = 0;
     uint64_t rounds = 0;
     std::vector<uint64_t> active_per_pass;  // elements entering each digit pass
+    uint64_t replayed = 0;      // blocks sorted by replaying a recorded launch pattern
+    uint64_t after_replay = 0;  // host-driven rounds that had to follow a replay
 };
 struct SortOpts;
 cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf, const SortOpts& opts);
@@ -162,9 +165,21 @@ __host__ __device__ inline uint32_t sa_slot_mask(uint64_t n_suf, uint64_t limit 
 }
 cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n, uint64_t limit);
 // per-handle sort options (setbwte_set_option "sa_payload", "kw1_min")
+// The launch pattern of one host-driven sort (per round: the segment count of
+// every size class), recorded once per handle from a block of >= 2^20
+// suffixes and replayed for blocks of about the same size without reading
+// counts back between rounds (the kernels read the real counts on the device;
+// a class the pattern skips keeps its segments for a later round).  One
+// read-back at the end decides whether host-driven rounds must follow.
+struct SortPattern {
+    std::mutex mu;
+    uint32_t n = 0;                                   // block size it was recorded on
+    std::vector<std::vector<uint32_t>> rounds;        // NCLASS counts per round
+};
 struct SortOpts {
     uint64_t payload_limit = kPayloadLimit;
     uint64_t kw1_min = 1ull << 40;  // blocks from this size precompute key word 1 (off by default)
+    SortPattern* pattern = nullptr;  // launch-pattern replay (null: every round host-driven)
 };
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,

@@ -406,8 +406,10 @@ __global__ void init_kernel(uint32_t* __restrict__ sa0, uint32_t* __restrict__ s
     }
 }
 
-__global__ void reset_counts_kernel(uint32_t* cnt, uint32_t* misc) {
-    if (threadIdx.x < NCLASS) cnt[threadIdx.x] = 0;
+// Consumed lists: the counts of the classes processed this round (mask) are
+// zeroed; an unprocessed class keeps its segments for a later round.
+__global__ void reset_counts_kernel(uint32_t* cnt, uint32_t* misc, uint32_t mask) {
+    if (threadIdx.x < NCLASS && ((mask >> threadIdx.x) & 1u)) cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
         misc[M_CHUNKS] = 0;
         misc[M_GROUPS] = 0;
@@ -1643,24 +1645,25 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_LAUNCH(prof, s, "sort_init", n <= kCapM ? 4.0 * n : 0.0, n,
               init_kernel<<<n <= kCapM ? grid_for(n, 256) : 1u, 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc, B));
     SB_CHECK(cudaGetLastError());
-    uint32_t h_cnt[NCLASS] = {0};
+    uint32_t h_cnt[NCLASS] = {0}, h_oth[NCLASS] = {0};  // counts of in / out
     if (n > 1) h_cnt[class_of(Seg{0u, (uint32_t)n, 0u, 24u | (1u << 9)})] = 1;
     Lists in = A, out = Bl;
     uint32_t prev_active = 0;
-    uint64_t act_local = 0;
     uint32_t h_misc[M_N] = {0};
-    for (;;) {
-        uint32_t any = 0;
-        for (int c = 0; c < NCLASS; ++c) any |= h_cnt[c];
-        if (!any) break;
+    // one round: the kernels of every class with a (recorded or read-back)
+    // non-zero count, the consumed counts reset, the lists swapped
+    auto run_round = [&](const uint32_t* cnt) -> cudaError_t {
+        uint32_t mask = 0;
+        for (int c = 0; c < NCLASS; ++c)
+            if (cnt[c]) mask |= 1u << c;
         {
             const int cls[4] = {BIT2, BIT4, BIT8, BIT16};
             const char* nm[4] = {"sort_bitonic64", "sort_bitonic128", "sort_bitonic256",
                                  "sort_bitonic512"};
             for (int q = 0; q < 4; ++q) {
-                const uint32_t cnt = h_cnt[cls[q]];
-                if (!cnt) continue;
-                const unsigned grid = grid_for((uint64_t)cnt * 32, kWarpCta * 32, 148u * 16u);
+                const uint32_t c = cnt[cls[q]];
+                if (!c) continue;
+                const unsigned grid = grid_for((uint64_t)c * 32, kWarpCta * 32, 148u * 16u);
                 switch (q) {
                     case 0: SB_LAUNCH(prof, s, nm[q], 0, 0, bitonic_kernel<2><<<grid, kWarpCta * 32, 0, s>>>(in, out, BIT2, B, misc)); break;
                     case 1: SB_LAUNCH(prof, s, nm[q], 0, 0, bitonic_kernel<4><<<grid, kWarpCta * 32, 0, s>>>(in, out, BIT4, B, misc)); break;
@@ -1670,41 +1673,41 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                 SB_CHECK(cudaGetLastError());
             }
         }
-        if (h_cnt[TINY]) {
+        if (cnt[TINY]) {
             SB_LAUNCH(prof, s, "sort_tiny", 0, 0,
-                      tiny_kernel<<<grid_for(((uint64_t)h_cnt[TINY] + kTinyPerWarp - 1) / kTinyPerWarp * 32,
+                      tiny_kernel<<<grid_for(((uint64_t)cnt[TINY] + kTinyPerWarp - 1) / kTinyPerWarp * 32,
                                              256, 148u * 16u), 256, 0,
                                     s>>>(in, B, misc));
             SB_CHECK(cudaGetLastError());
         }
-        if (h_cnt[SMALL]) {
+        if (cnt[SMALL]) {
             SB_LAUNCH(prof, s, "sort_small", 0, 0,
-                      warp_sort_kernel<<<grid_for((uint64_t)h_cnt[SMALL] * 32, kWarpCta * 32,
+                      warp_sort_kernel<<<grid_for((uint64_t)cnt[SMALL] * 32, kWarpCta * 32,
                                                   148u * 8u),
                                          kWarpCta * 32, 0, s>>>(in, out, B, misc));
             SB_CHECK(cudaGetLastError());
         }
-        if (h_cnt[MED1K]) {
+        if (cnt[MED1K]) {
             SB_LAUNCH(prof, s, "sort_medium", 0, 0,
-                      (local_kernel<1024, 128><<<std::min<uint32_t>(h_cnt[MED1K], 148u * 12u), 128,
+                      (local_kernel<1024, 128><<<std::min<uint32_t>(cnt[MED1K], 148u * 12u), 128,
                                                   sm_m1, s>>>(in, out, MED1K, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
-        if (h_cnt[MED2K]) {
+        if (cnt[MED2K]) {
             SB_LAUNCH(prof, s, "sort_medium", 0, 0,
-                      (local_kernel<2048, 256><<<std::min<uint32_t>(h_cnt[MED2K], 148u * 6u), 256,
+                      (local_kernel<2048, 256><<<std::min<uint32_t>(cnt[MED2K], 148u * 6u), 256,
                                                   sm_m2, s>>>(in, out, MED2K, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
-        if (h_cnt[MEDIUM]) {
+        if (cnt[MEDIUM]) {
             SB_LAUNCH(prof, s, "sort_medium", 0, 0,
-                      (local_kernel<kCapM, kNtM><<<std::min<uint32_t>(h_cnt[MEDIUM], 148u * 3u),
+                      (local_kernel<kCapM, kNtM><<<std::min<uint32_t>(cnt[MEDIUM], 148u * 3u),
                                                    kNtM, sm_m, s>>>(in, out, MEDIUM, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
-        if (h_cnt[LARGE]) {
+        if (cnt[LARGE]) {
             SB_LAUNCH(prof, s, "sort_chunkify", 0, 0,
-                      chunkify_kernel<<<grid_for((uint64_t)h_cnt[LARGE] * 32, 128), 128, 0, s>>>(
+                      chunkify_kernel<<<grid_for((uint64_t)cnt[LARGE] * 32, 128), 128, 0, s>>>(
                           in, segx, chunks, groups, misc));
             SB_CHECK(cudaGetLastError());
             const unsigned g_dig = 148u * 8u;
@@ -1715,7 +1718,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                       group_scan_kernel<<<148u * 8u, 256, 0, s>>>(groups, misc, hist, gtot));
             SB_CHECK(cudaGetLastError());
             SB_LAUNCH(prof, s, "digit_scan", 0, 0,
-                      digit_scan_kernel<<<std::min<uint32_t>(h_cnt[LARGE], 148u * 8u), 256, 0, s>>>(
+                      digit_scan_kernel<<<std::min<uint32_t>(cnt[LARGE], 148u * 8u), 256, 0, s>>>(
                           in, out, segx, gtot, dbase));
             SB_CHECK(cudaGetLastError());
             if (B.key1[0]) {
@@ -1729,27 +1732,75 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
             }
             SB_CHECK(cudaGetLastError());
         }
-        SB_LAUNCH(prof, s, "sort_ctl", 0, 0, reset_counts_kernel<<<1, 32, 0, s>>>(in.cnt, misc));
+        SB_LAUNCH(prof, s, "sort_ctl", 0, 0,
+                  reset_counts_kernel<<<1, 32, 0, s>>>(in.cnt, misc, mask));
         SB_CHECK(cudaGetLastError());
         std::swap(in, out);
-        // one read-back of both count lists and misc (contiguous in ctr); a
-        // pageable destination makes the copy return when the data is here
-        // (its in-driver wait measured faster than pinned + stream sync)
+        return cudaSuccess;
+    };
+    // one read-back of both count lists and misc (contiguous in ctr); a
+    // pageable destination makes the copy return when the data is here (its
+    // in-driver wait measured faster than pinned memory + a stream sync)
+    auto read_back = [&]() -> cudaError_t {
         uint32_t h_all[2 * NCLASS + M_N];
         SB_CHECK(cudaMemcpyAsync(h_all, ctr, sizeof(h_all), cudaMemcpyDeviceToHost, s));
         SB_CHECK(cudaStreamSynchronize(s));
         memcpy(h_cnt, h_all + (in.cnt - ctr), sizeof(h_cnt));
+        memcpy(h_oth, h_all + (out.cnt - ctr), sizeof(h_oth));
         memcpy(h_misc, h_all + 2 * NCLASS, sizeof(h_misc));
         if (h_misc[M_ACTIVE] != prev_active) {
-            const uint32_t delta = h_misc[M_ACTIVE] - prev_active;
-            act_local += delta;
             if (st) {
-                st->active_per_pass.push_back(delta);
+                st->active_per_pass.push_back(h_misc[M_ACTIVE] - prev_active);
                 st->digit_passes++;
             }
             prev_active = h_misc[M_ACTIVE];
         }
+        return cudaSuccess;
+    };
+    // replay a recorded launch pattern (no read-backs), then finish host-driven
+    SortPattern* pat = opts.pattern;
+    bool replayable = false;
+    std::vector<std::vector<uint32_t>> rounds;
+    if (pat && n >= (1u << 20)) {
+        std::lock_guard<std::mutex> lk(pat->mu);
+        if (!pat->rounds.empty() && pat->n + pat->n / 16 >= n && n + n / 16 >= pat->n) {
+            rounds = pat->rounds;
+            replayable = true;
+        }
     }
+    if (replayable) {
+        for (const std::vector<uint32_t>& r : rounds) SB_CHECK(run_round(r.data()));
+        SB_CHECK(read_back());
+        if (st) st->replayed++;
+    }
+    std::vector<std::vector<uint32_t>> rec;
+    for (;;) {
+        uint32_t any_in = 0, any_out = 0;
+        for (int c = 0; c < NCLASS; ++c) {
+            any_in |= h_cnt[c];
+            any_out |= h_oth[c];
+        }
+        if (!any_in && !any_out) break;
+        if (!any_in) {
+            // only carried-over segments left (a replayed round skipped their
+            // class): they sit in the other list
+            std::swap(in, out);
+            std::swap(h_cnt, h_oth);
+            continue;
+        }
+        if (!replayable) rec.emplace_back(h_cnt, h_cnt + NCLASS);
+        else if (st) st->after_replay++;
+        SB_CHECK(run_round(h_cnt));
+        SB_CHECK(read_back());
+    }
+    if (pat && !replayable && n >= (1u << 20)) {
+        std::lock_guard<std::mutex> lk(pat->mu);
+        if (pat->rounds.empty()) {
+            pat->n = n;
+            pat->rounds = rec;
+        }
+    }
+    const uint64_t act_local = h_misc[M_ACTIVE];
     if (st) st->rounds++;
     // algorithmic bytes: a digit pass reads/writes the
     // (slot, key) pair -- histogram 8 B, scatter 16 B per active element; the

@@ -609,3 +609,46 @@ def test_option_validation(SetBWTE):
             idx.set_option(key, bad)
     idx.append_strings(["ACGT"])
     assert idx.bwt().decode() == "T$ACG"
+
+
+@pytest.mark.parametrize("kind", ["uniform", "genome"])
+def test_replayed_sort_pattern(SetBWTE, kind):
+    """Blocks of >= 2^20 suffixes replay the launch pattern recorded on an
+    earlier block (no count read-backs between rounds).  Segments of a class
+    the pattern skips carry over to a later round; the genome-sampled reads
+    (deep, uneven LCPs) make the replayed pattern miss rounds."""
+    if kind == "uniform":
+        d, o = synth.uniform(40000, 100, seed=21)
+    else:
+        d, o = synth.genome_sampled(40000, 100, 1_500_000, seed=22)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 20)
+    idx.append(d, o)          # the first block records, later full blocks replay
+    assert idx.bwt() == want
+    idx.clear()
+    idx.append(d, o)          # every full block replays
+    assert idx.bwt() == want
+    st = idx.stats()["sort"]
+    assert st["replayed_blocks"] >= 3, st
+
+
+def test_replayed_pattern_that_does_not_fit(SetBWTE):
+    """A pattern recorded on uniform reads replayed on genome-sampled and
+    all-A blocks of the same size: the replay misses classes and rounds, the
+    skipped segments carry over and host-driven rounds finish the sort."""
+    du, ou = synth.uniform(20000, 100, seed=23)
+    dg, og = synth.genome_sampled(20000, 100, 300_000, seed=24)
+    da, oa = synth.adversarial("all_A", 12000, 100)
+    parts = [(du, ou), (dg, og), (da, oa)]
+    d = np.concatenate([p[0] for p in parts])
+    offs = [np.asarray(ou, dtype=np.uint64)]
+    for p in parts[1:]:
+        offs.append(np.asarray(p[1][1:], dtype=np.uint64) + offs[-1][-1])
+    o = np.concatenate(offs)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 20)
+    for pd, po in parts:
+        idx.append(pd, po)
+    assert idx.bwt() == want
+    st = idx.stats()["sort"]
+    assert st["replayed_blocks"] >= 1 and st["rounds_after_replay"] >= 1, st
