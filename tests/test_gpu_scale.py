@@ -84,3 +84,35 @@ def test_genome_sampled_deep_lcp():
     idx = SetBWTE(A, block_suffixes=1 << 24)
     idx.append(d, o)
     assert idx.bwt() == want
+
+
+@pytest.mark.slow
+def test_c4_full_sampled():
+    """configs[3] at full size: 1M reads of U[1000, 10000] bp (~5.5 Gbp),
+    M = 2^30, u64 ranks -- the launch configuration of bench.py --workload c4."""
+    from paper_1410_0562_b200 import SetBWTE
+    d, o = synth.uniform_var(1_000_000, 1000, 10000, seed=1)
+    idx = SetBWTE(A, block_suffixes=1 << 30)
+    idx.append(d, o)
+    assert idx.stats()["blocks"] >= 5
+    _sampled_checks(idx, d, o, n_samples=2, seed=5)
+
+
+@pytest.mark.slow
+def test_c5_full_sampled():
+    """configs[4] at full size: 10M reads appended into a 50M-read index whose
+    B_ext is host-tiered (pinned host memory), M = 2^27 -- as bench.py
+    --workload c5 runs it."""
+    from paper_1410_0562_b200 import SetBWTE
+    bd, bo = synth.uniform(50_000_000, 100, seed=1)
+    ad, ao = synth.uniform(10_000_000, 100, seed=2)
+    idx = SetBWTE(A, block_suffixes=1 << 27)
+    idx.append(bd, bo)
+    idx.set_option("host_tier", 1)
+    idx.append(ad, ao)
+    assert idx.stats()["host_tier"]
+    d = np.concatenate([bd, ad])
+    o = np.concatenate([np.asarray(bo, dtype=np.uint64),
+                        np.asarray(ao[1:], dtype=np.uint64) + np.uint64(bo[-1])])
+    del bd, ad
+    _sampled_checks(idx, d, o, n_samples=2, seed=6)
