@@ -908,8 +908,15 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     h->sigma = (int)sigma;
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+    // the sort lanes run at the highest stream priority: a launch on a lane
+    // starts as soon as SM slots free up instead of queueing behind the
+    // rank/insert stream (same throughput; per-launch event times then track
+    // the kernels' own execution more closely)
+    int prio_low = 0, prio_high = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
     for (int l = 0; l < setbwte_s::kMaxLanes; ++l)
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->lane_stream[l], cudaStreamNonBlocking);
+        if (e == cudaSuccess)
+            e = cudaStreamCreateWithPriority(&h->lane_stream[l], cudaStreamNonBlocking, prio_high);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->derr_host, sizeof(DevErr), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
