@@ -133,7 +133,9 @@ struct setbwte_s {
     cudaStream_t stream = nullptr;       // main stream (user's, or own_stream)
     static constexpr int kMaxLanes = 4;
     cudaStream_t lane_stream[kMaxLanes] = {};  // ConstructSA of upcoming blocks, one per sort lane
-    cudaStream_t copy_stream = nullptr;   // H2D of an append's bytes + packing, block by block
+    cudaStream_t copy_stream = nullptr;   // packing of an append's bytes, block by block
+    cudaStream_t h2d_stream = nullptr;    // H2D of host input, in chunks (starts before the partition)
+    std::vector<cudaEvent_t> ev_chunk;    // per H2D chunk: its bytes are on the device
     std::vector<cudaEvent_t> ev_packed;   // per block: its slots (and the next block's first group) packed
     DevErr* derr_host = nullptr;          // pinned landing spot for the validation result
     cudaEvent_t ev_start = nullptr, ev_sorted[kMaxLanes] = {}, ev_used[kMaxLanes] = {};
@@ -781,6 +783,26 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     API_CHECK(h, ensure(h->gfirst, n_groups + 2, &pk.gfirst));
     DevErr* derr;
     API_CHECK(h, ensure(h->err, 1, &derr));
+    // host input: the bytes start travelling now, in chunks, while the
+    // offsets are checked and the blocks partitioned (they do not depend on
+    // either); each block's packing waits for the chunks covering it
+    const uint64_t chunk = std::max<uint64_t>(16ull << 20, (n_bytes + 7) / 8);
+    const uint64_t n_chunks = host_bytes && n_bytes ? (n_bytes + chunk - 1) / chunk : 0;
+    if (n_chunks) {
+        while (h->ev_chunk.size() < n_chunks) {
+            cudaEvent_t ev;
+            API_CHECK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            h->ev_chunk.push_back(ev);
+        }
+        API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));  // the buffer is free
+        API_CHECK(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_start, 0));
+        for (uint64_t c = 0; c < n_chunks; ++c) {
+            const uint64_t b0 = c * chunk, b1 = std::min(n_bytes, b0 + chunk);
+            API_CHECK(h, cudaMemcpyAsync(const_cast<uint8_t*>(d_bytes) + b0, host_bytes + b0, b1 - b0,
+                                         cudaMemcpyHostToDevice, h->h2d_stream));
+            API_CHECK(h, cudaEventRecord(h->ev_chunk[c], h->h2d_stream));
+        }
+    }
     *h->derr_host = DevErr{~0ull, 0, 0};
     API_CHECK(h, cudaMemcpyAsync(derr, h->derr_host, sizeof(DevErr), cudaMemcpyHostToDevice,
                                  h->stream));
@@ -790,18 +812,31 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     API_CHECK(h, ensure(h->bounds, 2 * (m + 2) + 2, &d_bounds));
     uint64_t* d_k = d_bounds + 2 * (m + 2);
     API_CHECK(h, launch_partition(h->prof, h->stream, pk.slot_off, m, h->M, d_bounds, d_k));
+    // one round trip for K, the CSR check and (usually all of) the bounds
     uint64_t K = 0;
+    const uint64_t pre = std::min<uint64_t>(m + 1, 1024);  // bounds pairs read speculatively
+    std::vector<uint64_t> bounds(2 * pre);
     API_CHECK(h, cudaMemcpyAsync(&K, d_k, sizeof(K), cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaMemcpyAsync(h->derr_host, derr, sizeof(DevErr), cudaMemcpyDeviceToHost,
                                  h->stream));
-    API_CHECK(h, cudaStreamSynchronize(h->stream));
-    if (h->derr_host->bad_offsets) return SETBWTE_E_INVALID_ARG;
-    std::vector<uint64_t> bounds(2 * (K + 1));
-    API_CHECK(h, cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(uint64_t) * 2 * (K + 1),
+    API_CHECK(h, cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(uint64_t) * 2 * pre,
                                  cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
+    // an early return must not leave H2D copies reading the caller's buffer
+    auto abort_with = [&](setbwte_status st) {
+        cudaStreamSynchronize(h->h2d_stream);
+        return st;
+    };
+    if (h->derr_host->bad_offsets) return abort_with(SETBWTE_E_INVALID_ARG);
+    if (K + 1 > pre) {
+        bounds.resize(2 * (K + 1));
+        API_CHECK(h, cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(uint64_t) * 2 * (K + 1),
+                                     cudaMemcpyDeviceToHost, h->stream));
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+    }
     for (uint64_t b = 0; b < K; ++b) {
-        if (bounds[2 * b + 3] - bounds[2 * b + 1] >= (1ull << 31)) return SETBWTE_E_UNSUPPORTED;
+        if (bounds[2 * b + 3] - bounds[2 * b + 1] >= (1ull << 31))
+            return abort_with(SETBWTE_E_UNSUPPORTED);
     }
     h->last_bases = n_bytes;
     h->last_blocks = K;
@@ -817,12 +852,15 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     }
     API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
     API_CHECK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_start, 0));
+    uint64_t waited = 0;  // chunks the pack stream already waits for
     for (uint64_t k = 0; k < K; ++k) {
-        if (host_bytes) {
-            const uint64_t b0 = host_off[blocks[k].j0], b1 = host_off[blocks[k].j1];
-            if (b1 > b0)
-                API_CHECK(h, cudaMemcpyAsync(const_cast<uint8_t*>(d_bytes) + b0, host_bytes + b0,
-                                             b1 - b0, cudaMemcpyHostToDevice, h->copy_stream));
+        if (n_chunks) {
+            // the block's bytes, plus the staging window its last pack warp
+            // reads beyond them (< 1104 bytes)
+            const uint64_t last = std::min(n_bytes, host_off[blocks[k].j1] + 2048);
+            const uint64_t need = std::min(n_chunks, (last + chunk - 1) / chunk);
+            for (; waited < need; ++waited)
+                API_CHECK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_chunk[waited], 0));
         }
         const uint64_t g0 = k == 0 ? 0 : blocks[k].S0 >> 5;
         const uint64_t g1 = k + 1 < K ? blocks[k + 1].S0 >> 5 : n_groups;
@@ -918,6 +956,7 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
         if (e == cudaSuccess)
             e = cudaStreamCreateWithPriority(&h->lane_stream[l], cudaStreamNonBlocking, prio_high);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->derr_host, sizeof(DevErr), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
     for (int l = 0; l < setbwte_s::kMaxLanes; ++l) {
@@ -968,6 +1007,11 @@ void setbwte_destroy(setbwte_t h) {
         if (h->ev_used[l]) cudaEventDestroy(h->ev_used[l]);
         if (h->lane_stream[l]) cudaStreamDestroy(h->lane_stream[l]);
     }
+    if (h->h2d_stream) {
+        cudaStreamSynchronize(h->h2d_stream);
+        cudaStreamDestroy(h->h2d_stream);
+    }
+    for (cudaEvent_t ev : h->ev_chunk) cudaEventDestroy(ev);
     if (h->copy_stream) {
         cudaStreamSynchronize(h->copy_stream);
         cudaStreamDestroy(h->copy_stream);
