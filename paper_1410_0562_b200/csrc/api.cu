@@ -751,7 +751,7 @@ void build_stats(setbwte_t h) {
 }
 
 // One append (Algorithm 1 over its blocks).  Host input (host_bytes != NULL):
-// the bytes travel block by block on the copy stream and each block is packed
+// the bytes travel in chunks on the H2D stream and each block is packed
 // as soon as its bytes are on the device, so sorting starts while later blocks
 // are still in flight; the whole input is validated before the first Insert
 // (all-or-nothing).  Device input: d_bytes already holds everything.
@@ -844,7 +844,7 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     for (uint64_t b = 0; b < K; ++b)
         blocks[b] = BlockDesc{bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1], bounds[2 * b + 3],
                               std::min(b + 1, K - 1)};
-    // bytes in (host input) and packing, block by block on the copy stream
+    // packing, block by block on the pack ("copy") stream, each after its chunks
     while (h->ev_packed.size() < K) {
         cudaEvent_t ev;
         API_CHECK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
