@@ -201,6 +201,16 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *   "host_tier"       1: move B_ext to the host tier now (and keep it there).
  *   "g_width"         width of g / pos: 0 or 4 (default) = u32 while the new
  *                     index has < 2^32 symbols, else u64; 8 = always u64.
+ *   "shard_dict"      1: (after setbwte_set_partition with 2..8 ranks, on an
+ *                     empty index) B_ext's dictionary is sharded by output
+ *                     superblock range: each rank keeps
+ *                     only its shard; Insert is split by range, and every
+ *                     kernel reads other ranks' shards through their device
+ *                     pointers, exchanged each block through the allgather
+ *                     callback.  The ranks must share one address space (one
+ *                     process driving several GPUs with peer access, or
+ *                     several handles on one GPU).  Not with the host tier
+ *                     or setbwte_merge (SETBWTE_E_UNSUPPORTED).
  *   "sa_payload"      1 (default): while a block has < 2^29 suffixes, its SA
  *                     entries carry the B_int symbol in their top 3 bits; 0:
  *                     never (as for larger blocks: ComputeRanks records B_int

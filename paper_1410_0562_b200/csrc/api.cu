@@ -182,6 +182,13 @@ struct setbwte_s {
     // data-parallel ComputeRanks (and, with insert_split, Insert by output range)
     int rank = 0, world = 1;
     bool insert_split = false;
+    // NEXT-3: B_ext sharded by output superblock range across the ranks;
+    // every rank keeps only its shard (ping-pong) and reads the others'
+    // through their device pointers (peer / UVA)
+    bool sharded = false;
+    DevBuf shard_buf[2], shard_ptrs;
+    int shard_cur = 0;
+    Dict shard_dict = make_dict(nullptr);
     SortOpts sopt;                           // options "sa_payload", "kw1_min"
     SortPattern sort_pattern;                // recorded launch pattern (sopt.pattern)
     int g_width = 0;                         // option "g_width": 0 auto, 8 = always u64
@@ -268,6 +275,8 @@ inline const Blk* cur_blk(setbwte_t h) {
     return h->host_tier ? h->hdict_dev : (const Blk*)h->blk[h->cur].p;
 }
 inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cur].p; }
+// The current B_ext Blks as a (possibly sharded) Dict.
+inline Dict cur_dict(setbwte_t h) { return h->sharded ? h->shard_dict : make_dict(cur_blk(h)); }
 
 // ComputeRanks for strings [j0, j1) of a packed append, into g (block-local
 // slots starting at slot_base).  With world > 1, only this rank's slice is
@@ -282,7 +291,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     }
     if (h->world <= 1) {
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
-                                          slot_base, cur_blk(h), cur_sb(h),
+                                          slot_base, cur_dict(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
                                           n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot, bing));
         return SETBWTE_OK;
@@ -304,7 +313,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     const uint64_t a = sl[h->rank], b = sl[h->rank + 1];
     const uint64_t steps = (slot_of[h->rank + 1] - slot_of[h->rank]) - (b - a);
     API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
-                                      cur_blk(h), cur_sb(h), (const uint64_t*)h->d_C.p,
+                                      cur_dict(h), cur_sb(h), (const uint64_t*)h->d_C.p,
                                       h->prepending ? 0 : h->m, steps, g, gw, h->rank_ilp));
     std::vector<uint64_t> bytes(h->world);
     for (int r = 0; r < h->world; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
@@ -383,7 +392,7 @@ setbwte_status host_insert(setbwte_t h, const void* pos, int gw, const uint8_t* 
             API_CHECK(h, cudaMemcpyAsync(sin, h->hdict + bE0, (bE1 - bE0) * sizeof(Blk),
                                          cudaMemcpyHostToDevice, h->stream));
         }
-        API_CHECK(h, launch_insert_range(h->prof, h->stream, sin - bE0, n_in, pos, gw, bint, n_suf,
+        API_CHECK(h, launch_insert_range(h->prof, h->stream, make_dict(sin - bE0), n_in, pos, gw, bint, n_suf,
                                          sout - (sa << (kSbShift - 6)), tot, sb_start, sa, sbe));
         const uint64_t b0 = sa << (kSbShift - 6), b1 = std::min(sbe << (kSbShift - 6), nblk);
         API_CHECK(h, cudaMemcpyAsync(h->hdict + b0, sout, (b1 - b0) * sizeof(Blk),
@@ -405,7 +414,7 @@ setbwte_status insert_prepare(setbwte_t h, uint64_t n_ins, InsertBufs* ib) {
     const uint64_t nblk = (n_out >> 6) + 1;
     ib->nsb = (n_out >> kSbShift) + 1;
     const int nxt = 1 - h->cur;
-    if (!h->host_tier && nblk * sizeof(Blk) > h->hbm_budget) {
+    if (!h->host_tier && !h->sharded && nblk * sizeof(Blk) > h->hbm_budget) {
         // the dictionary outgrows its HBM budget: move B_ext to the host tier
         // (after this block's ComputeRanks, which still reads the HBM copy)
         setbwte_status st2 = host_reserve(h, nblk, cur_blk(h), true, h->n ? (h->n >> 6) + 1 : 0);
@@ -414,7 +423,7 @@ setbwte_status insert_prepare(setbwte_t h, uint64_t n_ins, InsertBufs* ib) {
         free_buf(h->blk[0]);
         free_buf(h->blk[1]);
     }
-    if (!h->host_tier) API_CHECK(h, ensure(h->blk[nxt], nblk, &ib->ob));
+    if (!h->host_tier && !h->sharded) API_CHECK(h, ensure(h->blk[nxt], nblk, &ib->ob));
     API_CHECK(h, ensure(h->sb[nxt], ib->nsb * 4, &ib->osb));
     API_CHECK(h, ensure(h->sb_tot, ib->nsb * 5 + 8, &ib->tot));  // totals + sb_start
     ib->sb_start = ib->tot + 4 * (ib->nsb + 1);
@@ -428,6 +437,48 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
     if (h->host_tier) {
         setbwte_status st = host_insert(h, pos, gw, bint, n_ins, ib.osb, ib.tot, ib.sb_start, m_new);
         if (st != SETBWTE_OK) return st;
+    } else if (h->sharded) {
+        // NEXT-3: rank r merges output superblocks [nsb*r/P, nsb*(r+1)/P) into
+        // its own new shard (reading the old B_ext from every shard); only the
+        // superblock totals and the shard pointers are exchanged -- no rank
+        // holds the whole dictionary
+        const uint64_t n_out = h->n + n_ins;
+        const uint64_t nblk = (n_out >> 6) + 1;
+        const uint64_t P = (uint64_t)h->world;
+        std::vector<uint64_t> tot_bytes(P);
+        for (uint64_t r = 0; r < P; ++r)
+            tot_bytes[r] = (ib.nsb * (r + 1) / P - ib.nsb * r / P) * 4 * sizeof(uint64_t);
+        const uint64_t a = ib.nsb * h->rank / P, b = ib.nsb * (h->rank + 1) / P;
+        const uint64_t fb = std::min(a * kBlkPerSb, nblk);
+        const uint64_t own = std::min(b * kBlkPerSb, nblk) - fb;
+        Blk* shard;
+        API_CHECK(h, ensure(h->shard_buf[1 - h->shard_cur], own + 8, &shard));
+        API_CHECK(h, launch_insert_range(h->prof, h->stream, cur_dict(h), h->n, pos, gw, bint, n_ins,
+                                         shard - a * kBlkPerSb, ib.tot, ib.sb_start, a, b));
+        // shard pointers (first Blk, device pointer) of every rank
+        uint64_t* d_ptrs;
+        API_CHECK(h, ensure(h->shard_ptrs, 2 * P + 8, &d_ptrs));
+        uint64_t mine[2] = {fb, (uint64_t)(uintptr_t)shard};
+        API_CHECK(h, cudaMemcpyAsync(d_ptrs + 2 * h->rank, mine, sizeof(mine), cudaMemcpyHostToDevice,
+                                     h->stream));
+        std::vector<uint64_t> ptr_bytes(P, 2 * sizeof(uint64_t));
+        if (h->allgather(ib.tot, tot_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx) ||
+            h->allgather(d_ptrs, ptr_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
+            return SETBWTE_E_STATE;
+        API_CHECK(h, launch_sb_scan(h->prof, h->stream, ib.tot, ib.nsb, ib.osb, m_new,
+                                    (uint64_t*)h->d_C.p));
+        std::vector<uint64_t> all(2 * P);
+        API_CHECK(h, cudaMemcpyAsync(all.data(), d_ptrs, sizeof(uint64_t) * 2 * P,
+                                     cudaMemcpyDeviceToHost, h->stream));
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+        Dict d = make_dict(nullptr);
+        d.P = (int)P;
+        for (uint64_t r = 0; r < P; ++r) {
+            d.first[r] = all[2 * r];
+            d.ptr[r] = reinterpret_cast<const Blk*>((uintptr_t)all[2 * r + 1]);
+        }
+        h->shard_dict = d;
+        h->shard_cur = 1 - h->shard_cur;
     } else if (h->world > 1 && h->insert_split && h->allgather) {
         // Insert split by output range: rank r merges output
         // superblocks [nsb*r/P, nsb*(r+1)/P) only; the new dictionary's Blks and
@@ -444,7 +495,7 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
             tot_bytes[r] = (b - a) * 4 * sizeof(uint64_t);
         }
         const uint64_t a = ib.nsb * h->rank / P, b = ib.nsb * (h->rank + 1) / P;
-        API_CHECK(h, launch_insert_range(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_ins,
+        API_CHECK(h, launch_insert_range(h->prof, h->stream, cur_dict(h), h->n, pos, gw, bint, n_ins,
                                          ib.ob, ib.tot, ib.sb_start, a, b));
         if (h->allgather(ib.ob, blk_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx) ||
             h->allgather(ib.tot, tot_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
@@ -452,7 +503,7 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
         API_CHECK(h, launch_sb_scan(h->prof, h->stream, ib.tot, ib.nsb, ib.osb, m_new,
                                     (uint64_t*)h->d_C.p));
     } else {
-        API_CHECK(h, launch_insert(h->prof, h->stream, cur_blk(h), h->n, pos, gw, bint, n_ins, ib.ob,
+        API_CHECK(h, launch_insert(h->prof, h->stream, cur_dict(h), h->n, pos, gw, bint, n_ins, ib.ob,
                                    ib.osb, ib.tot, ib.sb_start, m_new, (uint64_t*)h->d_C.p));
     }
     h->cur = 1 - h->cur;
@@ -993,7 +1044,7 @@ void setbwte_destroy(setbwte_t h) {
     DevBuf* bufs[] = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0], &h->sb[1],
                       &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term, &h->gfirst,
                       &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos, &h->bslot,
-                      &h->bint, &h->outbuf};
+                      &h->bint, &h->outbuf, &h->shard_buf[0], &h->shard_buf[1], &h->shard_ptrs};
     for (SortScratch& ws : h->sort) ws.free_all();
     for (DevBuf* b : bufs) free_buf(*b);
     free_buf(h->stage_in);
@@ -1072,7 +1123,8 @@ setbwte_status setbwte_merge(setbwte_t h, setbwte_t other) {
     API_ENTER(h);
     if (!other || other == h) return SETBWTE_E_INVALID_ARG;
     if (other->failed) return SETBWTE_E_STATE;
-    if (other->device != h->device || strcmp(other->alpha, h->alpha) != 0)
+    if (other->device != h->device || strcmp(other->alpha, h->alpha) != 0 || h->sharded ||
+        other->sharded)
         return SETBWTE_E_UNSUPPORTED;
     return merge_impl(h, other);
 }
@@ -1104,7 +1156,7 @@ static setbwte_status bwt_impl(setbwte_t h, uint8_t* out, uint64_t cap, uint64_t
     if (h->n == 0) return SETBWTE_OK;
     uint8_t* target = out;
     if (!dev) API_CHECK(h, ensure(h->outbuf, h->n, &target));
-    API_CHECK(h, launch_decode(h->prof, h->stream, cur_blk(h), h->n, (const uint8_t*)h->d_sym.p,
+    API_CHECK(h, launch_decode(h->prof, h->stream, cur_dict(h), h->n, (const uint8_t*)h->d_sym.p,
                                target));
     if (!dev)
         API_CHECK(h, cudaMemcpyAsync(out, target, h->n, cudaMemcpyDeviceToHost, h->stream));
@@ -1134,7 +1186,7 @@ setbwte_status setbwte_rank(setbwte_t h, uint8_t c, uint64_t k, uint64_t* out) {
     uint8_t* dc = reinterpret_cast<uint8_t*>(d + 2);
     API_CHECK(h, cudaMemcpyAsync(d, &k, 8, cudaMemcpyHostToDevice, h->stream));
     API_CHECK(h, cudaMemcpyAsync(dc, &c, 1, cudaMemcpyHostToDevice, h->stream));
-    API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_blk(h), cur_sb(h), h->n,
+    API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_dict(h), cur_sb(h), h->n,
                                    (const uint8_t*)h->d_code_of.p, dc, d, 1, d + 1));
     uint64_t r = 0;
     API_CHECK(h, cudaMemcpyAsync(&r, d + 1, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -1163,7 +1215,7 @@ setbwte_status setbwte_rank_batch(setbwte_t h, const uint8_t* c_dev, const uint6
         API_CHECK(h, cudaMemcpy(out_dev, r.data(), q * 8, cudaMemcpyHostToDevice));
         return SETBWTE_OK;
     }
-    API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_blk(h), cur_sb(h), h->n,
+    API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_dict(h), cur_sb(h), h->n,
                                    (const uint8_t*)h->d_code_of.p, c_dev, k_dev, q, out_dev));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
     return SETBWTE_OK;
@@ -1175,7 +1227,7 @@ static setbwte_status count_impl(setbwte_t h, const uint8_t* d_pat, const uint64
         API_CHECK(h, cudaMemsetAsync(d_out, 0, q * sizeof(uint64_t), h->stream));
         return SETBWTE_OK;
     }
-    API_CHECK(h, launch_count(h->prof, h->stream, cur_blk(h), cur_sb(h), h->n,
+    API_CHECK(h, launch_count(h->prof, h->stream, cur_dict(h), cur_sb(h), h->n,
                               (const uint64_t*)h->d_C.p, (const uint8_t*)h->d_code_of.p, d_pat,
                               d_off, q, d_out));
     return SETBWTE_OK;
@@ -1292,6 +1344,7 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "host_tier")) {
         // 1: move B_ext's dictionary to pinned host memory now (and keep it there)
         if (value != 1) return SETBWTE_E_INVALID_ARG;
+        if (h->sharded) return SETBWTE_E_UNSUPPORTED;
         h->hbm_budget = 0;
         if (!h->host_tier) {
             cudaError_t e = cudaSetDevice(h->device);
@@ -1315,6 +1368,12 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "kw1_min")) {
         if (value == 0) return SETBWTE_E_INVALID_ARG;
         h->sopt.kw1_min = value;
+    } else if (!strcmp(key, "shard_dict")) {
+        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        // needs the partition (world > 1, P <= 8), an empty index and no host tier
+        if (value && (h->world <= 1 || h->world > kMaxShards || h->host_tier || h->n != 0))
+            return SETBWTE_E_UNSUPPORTED;
+        h->sharded = value != 0;
     } else if (!strcmp(key, "insert_split")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;

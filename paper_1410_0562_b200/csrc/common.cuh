@@ -84,6 +84,39 @@ __device__ __forceinline__ uint64_t match_plane(uint32_t c, uint64_t lo, uint64_
     return a & b & ~dol;
 }
 
+// The Blk array of B_ext, possibly split into shards held by different
+// handles / GPUs (NEXT-3): shard q holds Blks [first[q], first[q+1]).  P = 1
+// is the ordinary single array.  Device pointers of other shards are peer
+// (UVA) pointers: reads of a remote shard go over NVLink.
+constexpr int kMaxShards = 8;
+struct Dict {
+    const Blk* ptr[kMaxShards];
+    uint64_t first[kMaxShards];
+    int P;
+};
+__host__ __device__ inline Dict make_dict(const Blk* p) {
+    Dict d;
+    for (int q = 0; q < kMaxShards; ++q) {
+        d.ptr[q] = nullptr;
+        d.first[q] = ~0ull;
+    }
+    d.ptr[0] = p;
+    d.first[0] = 0;
+    d.P = 1;
+    return d;
+}
+__device__ __forceinline__ const Blk* dict_blk(const Dict& d, uint64_t b) {
+    int q = 0;
+    for (int r = 1; r < d.P; ++r) {
+        if (b < d.first[r]) break;
+        q = r;
+    }
+    return d.ptr[q] + (b - d.first[q]);
+}
+
+__device__ __forceinline__ const Blk* blk_at(const Blk* p, uint64_t b) { return p + b; }
+__device__ __forceinline__ const Blk* blk_at(const Dict& d, uint64_t b) { return dict_blk(d, b); }
+
 // rank(c, i, B_ext) for a real symbol code c (Eq.(2)) -- one 32-byte Blk
 // sector plus one superblock counter.
 __device__ __forceinline__ uint64_t dict_rank(const Blk* __restrict__ blk,
@@ -92,6 +125,19 @@ __device__ __forceinline__ uint64_t dict_rank(const Blk* __restrict__ blk,
     const Blk* b = blk + (i >> 6);
     const uint64_t base = __ldg(sb + ((i >> kSbShift) << 2) + c);
     // the whole 32-byte Blk (one sector) in one 256-bit load
+    uint64_t w0, w1, w2, w3;
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+        : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
+        : "l"(b));
+    const uint32_t r = (uint32_t)((w0 >> (16 * c)) & 0xFFFFu);
+    const uint64_t mask = (1ull << (i & 63)) - 1ull;
+    return base + r + (uint64_t)__popcll(match_plane(c, w1, w2, w3) & mask);
+}
+
+__device__ __forceinline__ uint64_t dict_rank(const Dict& d, const uint64_t* __restrict__ sb,
+                                              uint32_t c, uint64_t i) {
+    const Blk* b = dict_blk(d, i >> 6);
+    const uint64_t base = __ldg(sb + ((i >> kSbShift) << 2) + c);
     uint64_t w0, w1, w2, w3;
     asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
         : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)

@@ -108,14 +108,16 @@ __device__ __forceinline__ void merge_word(uint32_t (&oo)[2][3], uint64_t xl, ui
 // memory): enough for a block that adds up to ~60 % new symbols
 constexpr uint32_t kStage = 40960;
 
-template <class G>
+// D = const Blk* (one array) or Dict (a sharded dictionary, NEXT-3)
+template <class G, class D>
 __global__ void __launch_bounds__(kInsNt) insert_kernel(
-    const Blk* __restrict__ in_blk, uint64_t n_in, const G* __restrict__ pos,
+    const D in_blk, uint64_t n_in, const G* __restrict__ pos,
     const uint8_t* __restrict__ bint, uint64_t n_ins, Blk* __restrict__ out_blk, uint64_t n_out,
     uint64_t* __restrict__ sb_tot, const uint64_t* __restrict__ sb_start, uint64_t sb_begin,
     uint64_t sb_end) {
     // in_blk / out_blk are indexed by absolute Blk number; the host-tier path
-    // passes pointers biased by its staging window (only the window is touched)
+    // and a sharded index pass pointers biased by their window (only the
+    // window is touched); in_blk may be split into shards (Dict)
     __shared__ uint32_t wcnt[kBlkPerSb];
     extern __shared__ uint16_t ent[];  // kStage: (offset in word) | (B_int code+$ << 6)
     __shared__ uint32_t wsum[4][kInsWarps];
@@ -171,11 +173,12 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
                 const uint32_t sh = (uint32_t)(e0 & 63);
                 uint64_t b0[4], b1[4] = {0, 0, 0, 0};
                 asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
-                    : "=l"(b0[0]), "=l"(b0[1]), "=l"(b0[2]), "=l"(b0[3]) : "l"(in_blk + eb));
+                    : "=l"(b0[0]), "=l"(b0[1]), "=l"(b0[2]), "=l"(b0[3])
+                    : "l"(blk_at(in_blk, eb)));
                 if (sh != 0 && ((eb + 1) << 6) < n_in)
                     asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
                         : "=l"(b1[0]), "=l"(b1[1]), "=l"(b1[2]), "=l"(b1[3])
-                        : "l"(in_blk + eb + 1));
+                        : "l"(blk_at(in_blk, eb + 1)));
                 xl = funnel(b0[1], b1[1], sh);
                 xh = funnel(b0[2], b1[2], sh);
                 xd = funnel(b0[3], b1[3], sh);
@@ -315,7 +318,31 @@ __global__ void __launch_bounds__(1024) sb_scan_kernel(const uint64_t* __restric
     }
 }
 
-cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+template <class D>
+cudaError_t launch_insert_kernel(Profiler& prof, cudaStream_t s, const D in_blk, uint64_t n_in,
+                                 const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
+                                 Blk* out_blk, uint64_t n_out, uint64_t* sb_tot,
+                                 const uint64_t* sb_start, uint64_t sb_begin, uint64_t sb_end,
+                                 unsigned grid, double bytes, double frac) {
+    SB_CHECK(cudaFuncSetAttribute(insert_kernel<uint32_t, D>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kStage * 2)));
+    SB_CHECK(cudaFuncSetAttribute(insert_kernel<uint64_t, D>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kStage * 2)));
+    if (gw == 4) {
+        SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
+                  (insert_kernel<uint32_t, D><<<grid, kInsNt, kStage * 2, s>>>(
+                      in_blk, n_in, (const uint32_t*)pos, bint, n_ins, out_blk, n_out, sb_tot,
+                      sb_start, sb_begin, sb_end)));
+    } else {
+        SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
+                  (insert_kernel<uint64_t, D><<<grid, kInsNt, kStage * 2, s>>>(
+                      in_blk, n_in, (const uint64_t*)pos, bint, n_ins, out_blk, n_out, sb_tot,
+                      sb_start, sb_begin, sb_end)));
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,
                                 const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                                 Blk* out_blk, uint64_t* sb_tot, const uint64_t* sb_start,
                                 uint64_t sb_begin, uint64_t sb_end) {
@@ -327,24 +354,15 @@ cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Blk* in_bl
     const double frac = (double)nsb_r / (double)((n_out >> kSbShift) + 1);
     const double bytes = frac * (0.5 * (double)n_in + 0.5 * (double)n_out + (gw + 1.0) * (double)n_ins);
     const unsigned grid = (unsigned)(nsb_r < 148u * 64u ? nsb_r : 148u * 64u);
-    SB_CHECK(cudaFuncSetAttribute(insert_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kStage * 2)));
-    SB_CHECK(cudaFuncSetAttribute(insert_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kStage * 2)));
-    if (gw == 4) {
-        SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
-                  insert_kernel<uint32_t><<<grid, kInsNt, kStage * 2, s>>>(in_blk, n_in, (const uint32_t*)pos,
-                                                                   bint, n_ins, out_blk, n_out,
-                                                                   sb_tot, sb_start, sb_begin,
-                                                                   sb_end));
-    } else {
-        SB_LAUNCH(prof, s, "insert", bytes, (uint64_t)(frac * n_out),
-                  insert_kernel<uint64_t><<<grid, kInsNt, kStage * 2, s>>>(in_blk, n_in, (const uint64_t*)pos,
-                                                                   bint, n_ins, out_blk, n_out,
-                                                                   sb_tot, sb_start, sb_begin,
-                                                                   sb_end));
-    }
-    return cudaGetLastError();
+    if (in_blk.P == 1)
+        SB_CHECK((launch_insert_kernel<const Blk*>(prof, s, in_blk.ptr[0], n_in, pos, gw, bint, n_ins,
+                                                   out_blk, n_out, sb_tot, sb_start, sb_begin,
+                                                   sb_end, grid, bytes, frac)));
+    else
+        SB_CHECK((launch_insert_kernel<Dict>(prof, s, in_blk, n_in, pos, gw, bint, n_ins, out_blk,
+                                             n_out, sb_tot, sb_start, sb_begin, sb_end, grid, bytes,
+                                             frac)));
+    return cudaSuccess;
 }
 
 cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_tot, uint64_t nsb,
@@ -354,7 +372,7 @@ cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_to
     return cudaGetLastError();
 }
 
-cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
                           const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C) {
@@ -370,7 +388,7 @@ cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uin
 // processed tail): per pattern P, for k = |P|-1..0: c = P[k];
 // lo = C[c] + rank(c, lo), hi = C[c] + rank(c, hi); count = hi - lo.
 // A byte outside the alphabet makes the count 0; the empty pattern counts n.
-__global__ void count_kernel(const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+__global__ void count_kernel(const Dict blk, const uint64_t* __restrict__ sb,
                              uint64_t n, const uint64_t* __restrict__ Cd,
                              const uint8_t* __restrict__ code_of, const uint8_t* __restrict__ pat,
                              const uint64_t* __restrict__ poff, uint64_t q,
@@ -394,7 +412,7 @@ __global__ void count_kernel(const Blk* __restrict__ blk, const uint64_t* __rest
     }
 }
 
-cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Dict& blk, const uint64_t* sb,
                          uint64_t n, const uint64_t* d_C, const uint8_t* code_of,
                          const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out) {
     if (q == 0) return cudaSuccess;
@@ -404,7 +422,7 @@ cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Blk* blk, const u
     return cudaGetLastError();
 }
 
-__global__ void rank_batch_kernel(const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+__global__ void rank_batch_kernel(const Dict blk, const uint64_t* __restrict__ sb,
                                   uint64_t n, const uint8_t* __restrict__ code_of,
                                   const uint8_t* __restrict__ cq, const uint64_t* __restrict__ kq,
                                   uint64_t q, uint64_t* __restrict__ out) {
@@ -427,7 +445,7 @@ __global__ void rank_batch_kernel(const Blk* __restrict__ blk, const uint64_t* _
     }
 }
 
-cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Dict& blk, const uint64_t* sb,
                               uint64_t n, const uint8_t* code_of, const uint8_t* c,
                               const uint64_t* k, uint64_t q, uint64_t* out) {
     if (q == 0) return cudaSuccess;
@@ -438,7 +456,7 @@ cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, co
 }
 
 // BWT decode: one thread per 64-symbol Blk, 4 x 16-byte stores of ASCII.
-__global__ void decode_kernel(const Blk* __restrict__ blk, uint64_t n,
+__global__ void decode_kernel(const Dict blk, uint64_t n,
                               const uint8_t* __restrict__ sym_ascii, uint8_t* __restrict__ out) {
     // code -> byte lookup via byte_perm: selector nibble c picks sym[c]
     const uint32_t tab = (uint32_t)sym_ascii[0] | ((uint32_t)sym_ascii[1] << 8) |
@@ -448,7 +466,7 @@ __global__ void decode_kernel(const Blk* __restrict__ blk, uint64_t n,
          b += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t w[4];
         asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
-            : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(blk + b));
+            : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(dict_blk(blk, b)));
         const uint64_t lo = w[1], hi = w[2], dl = w[3];
         uint32_t o[16];
 #pragma unroll
@@ -476,7 +494,7 @@ __global__ void decode_kernel(const Blk* __restrict__ blk, uint64_t n,
     }
 }
 
-cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Blk* blk, uint64_t n,
+cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Dict& blk, uint64_t n,
                           const uint8_t* sym_ascii, uint8_t* out) {
     if (n == 0) return cudaSuccess;
     SB_LAUNCH(prof, s, "decode", 1.5 * n, n,

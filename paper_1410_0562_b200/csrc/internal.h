@@ -191,7 +191,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
 // fused A2/A4 extraction + gather (Alg.1).
 cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
-                                 uint64_t slot_base, const Blk* blk, const uint64_t* sb,
+                                 uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
                                  int gw, int ilp, uint8_t* bslot = nullptr, bool bing = false);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64).
@@ -213,25 +213,25 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           bool bing = false);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
-cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
                           const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C);
 // Insert restricted to output superblocks [sb_begin, sb_end) (host tier)
 // and the closing superblock scan.
-cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Blk* in_blk, uint64_t n_in,
+cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,
                                 const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                                 Blk* out_blk, uint64_t* sb_tot, const uint64_t* sb_start,
                                 uint64_t sb_begin, uint64_t sb_end);
 cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_tot, uint64_t nsb,
                            uint64_t* out_sb, uint64_t m_new, uint64_t* d_C);
-cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Dict& blk, const uint64_t* sb,
                               uint64_t n, const uint8_t* code_of, const uint8_t* c,
                               const uint64_t* k, uint64_t q, uint64_t* out);
-cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Blk* blk, const uint64_t* sb,
+cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Dict& blk, const uint64_t* sb,
                          uint64_t n, const uint64_t* d_C, const uint8_t* code_of,
                          const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out);
-cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Blk* blk, uint64_t n,
+cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Dict& blk, uint64_t n,
                           const uint8_t* sym_ascii, uint8_t* out);
 // Debug/export: SA + B_int ASCII of a sorted block.
 cudaError_t launch_bint_ascii(Profiler& prof, cudaStream_t s, const uint8_t* bint,

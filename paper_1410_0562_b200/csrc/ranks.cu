@@ -40,10 +40,11 @@ __device__ __forceinline__ void store4<uint64_t>(uint64_t* dst, uint64_t a, uint
                  "l"(d));
 }
 
-template <class G>
+// D = const Blk* (one array) or Dict (a sharded dictionary, NEXT-3)
+template <class G, class D>
 __global__ void __launch_bounds__(256) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
-    uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+    uint64_t j1, uint64_t slot_base, const D blk, const uint64_t* __restrict__ sb,
     const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot,
     bool bing) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) compute_ranks_kernel(
 template <class G, int K>
 __global__ void __launch_bounds__(256) compute_ranks_ilp_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
-    uint64_t j1, uint64_t slot_base, const Blk* __restrict__ blk, const uint64_t* __restrict__ sb,
+    uint64_t j1, uint64_t slot_base, const Dict blk, const uint64_t* __restrict__ sb,
     const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
@@ -154,7 +155,8 @@ __global__ void __launch_bounds__(256) compute_ranks_ilp_kernel(
                     }
                     const uint32_t c = (word[k] >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
                     const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
-                    i[k] = Cc + dict_rank(blk, sb, c, i[k]);
+                    i[k] = Cc + (blk.P == 1 ? dict_rank(blk.ptr[0], sb, c, i[k])
+                                            : dict_rank(blk, sb, c, i[k]));
                     g[q] = (G)i[k];
                 }
             }
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(256) compute_ranks_ilp_kernel(
 
 cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
-                                 uint64_t slot_base, const Blk* blk, const uint64_t* sb,
+                                 uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
                                  int gw, int ilp, uint8_t* bslot, bool bing) {
     if (j1 <= j0) return cudaSuccess;
@@ -189,13 +191,27 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
     }
     const unsigned grid = grid_for(nstr, 256, 1u << 20);
     if (gw == 4) {
-        SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                  compute_ranks_kernel<uint32_t><<<grid, 256, 0, s>>>(
-                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g, bslot, false));
+        if (blk.P == 1)
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_kernel<uint32_t, const Blk*><<<grid, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
+                          (uint32_t*)g, bslot, false)));
+        else
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_kernel<uint32_t, Dict><<<grid, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g,
+                          bslot, false)));
     } else {
-        SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                  compute_ranks_kernel<uint64_t><<<grid, 256, 0, s>>>(
-                      text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g, bslot, bing));
+        if (blk.P == 1)
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_kernel<uint64_t, const Blk*><<<grid, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
+                          (uint64_t*)g, bslot, bing)));
+        else
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_kernel<uint64_t, Dict><<<grid, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g,
+                          bslot, bing)));
     }
     return cudaGetLastError();
 }

@@ -46,7 +46,7 @@ def _loopback(world):
     return make
 
 
-def _run_ranks(world, split, appends, M):
+def _run_ranks(world, split, appends, M, shard=False, keep=False):
     from paper_1410_0562_b200 import SetBWTE
     make = _loopback(world)
     idx = []
@@ -54,6 +54,8 @@ def _run_ranks(world, split, appends, M):
         h = SetBWTE(A, block_suffixes=M)
         h.set_partition(r, world, make(r))
         h.set_option("insert_split", split)
+        if shard:
+            h.set_option("shard_dict", 1)
         idx.append(h)
     errs = [None] * world
 
@@ -70,7 +72,8 @@ def _run_ranks(world, split, appends, M):
     for t in th:
         t.join(timeout=600)
     assert errs == [None] * world, errs
-    return [h.bwt() for h in idx]
+    out = [h.bwt() for h in idx]
+    return (out, idx) if keep else out
 
 
 def _split_appends(d, o, cuts):
@@ -101,3 +104,34 @@ def test_multirank_c1(world, split):
     apps = _split_appends(d, o, [300, 700])
     for got in _run_ranks(world, split, apps, M=25250):
         assert got == want
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("seed", range(3))
+def test_sharded_dictionary_random_sets(world, seed):
+    """NEXT-3: B_ext sharded by output superblock range; every rank holds only
+    its shard and reads the others' through their device pointers."""
+    d, o = synth.random_set(18000 + seed, max_m=64, max_len=60)
+    want = oracle.bwt(A, d, o)
+    m = len(o) - 1
+    apps = _split_appends(d, o, [m // 2] if m > 2 else [])
+    for got in _run_ranks(world, 1, apps, M=120, shard=True):
+        assert got == want
+
+
+def test_sharded_dictionary_c1_queries():
+    d, o = synth.uniform(3000, 100, seed=9)
+    want = oracle.bwt(A, d, o, threads=None)
+    apps = _split_appends(d, o, [1000, 2000])
+    outs, idx = _run_ranks(3, 1, apps, M=40000, shard=True, keep=True)
+    for got in outs:
+        assert got == want
+    # rank / count queries read every shard
+    rng = np.random.default_rng(2)
+    B = np.frombuffer(want, dtype=np.uint8)
+    for k in rng.integers(0, len(want) + 1, size=6):
+        for c in "$ACGT":
+            assert idx[1].rank(c, int(k)) == int((B[:int(k)] == ord(c)).sum())
+    starts = rng.integers(0, len(d) - 10, size=30)
+    pats = [bytes(d[a:a + 7]).decode() for a in starts]
+    assert np.array_equal(idx[2].count(pats), oracle.count(A, d, o, pats))
