@@ -207,10 +207,13 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     only its shard; Insert is split by range, and every
  *                     kernel reads other ranks' shards through their device
  *                     pointers, exchanged each block through the allgather
- *                     callback.  The ranks must share one address space (one
+ *                     callback.  1: the ranks share one address space (one
  *                     process driving several GPUs with peer access, or
- *                     several handles on one GPU).  Not with the host tier
- *                     or setbwte_merge (SETBWTE_E_UNSUPPORTED).
+ *                     several handles on one GPU) and exchange device
+ *                     pointers; 2: one process per rank, exchanging CUDA IPC
+ *                     handles of the shard allocations (opened once each).
+ *                     Not with the host tier or setbwte_merge
+ *                     (SETBWTE_E_UNSUPPORTED).
  *   "sa_payload"      1 (default): while a block has < 2^29 suffixes, its SA
  *                     entries carry the B_int symbol in their top 3 bits; 0:
  *                     never (as for larger blocks: ComputeRanks records B_int

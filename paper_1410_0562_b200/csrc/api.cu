@@ -3,6 +3,7 @@
 // ping-pong B_ext dictionary, error state and statistics.
 #include <ctype.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -188,6 +189,9 @@ struct setbwte_s {
     bool sharded = false;
     DevBuf shard_buf[2], shard_ptrs;
     int shard_cur = 0;
+    bool shard_ipc = false;  // ranks are separate processes: exchange CUDA IPC handles
+    std::vector<std::pair<uint64_t, void*>> ipc_open[kMaxShards];  // peer address -> opened mapping
+    std::vector<void*> shard_retired;  // outgrown shard allocations (freed at destroy)
     Dict shard_dict = make_dict(nullptr);
     SortOpts sopt;                           // options "sa_payload", "kw1_min"
     SortPattern sort_pattern;                // recorded launch pattern (sopt.pattern)
@@ -213,10 +217,17 @@ setbwte_status from_cuda(setbwte_t h, cudaError_t e) {
     return SETBWTE_E_CUDA;
 }
 
-#define API_CHECK(h, expr)                                    \
-    do {                                                      \
-        cudaError_t _e = (expr);                              \
-        if (_e != cudaSuccess) return from_cuda((h), _e);     \
+// A failing CUDA call: with SETBWTE_DEBUG set in the environment, its error
+// and source line go to stderr (the C ABI itself only returns E_CUDA / E_NOMEM).
+#define API_CHECK(h, expr)                                                          \
+    do {                                                                            \
+        cudaError_t _e = (expr);                                                    \
+        if (_e != cudaSuccess) {                                                    \
+            if (getenv("SETBWTE_DEBUG"))                                            \
+                fprintf(stderr, "setbwte: %s at api.cu:%d\n", cudaGetErrorString(_e), \
+                        __LINE__);                                                  \
+            return from_cuda((h), _e);                                              \
+        }                                                                           \
     } while (0)
 
 #define API_ENTER(h)                                          \
@@ -452,30 +463,69 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
         const uint64_t fb = std::min(a * kBlkPerSb, nblk);
         const uint64_t own = std::min(b * kBlkPerSb, nblk) - fb;
         Blk* shard;
-        API_CHECK(h, ensure(h->shard_buf[1 - h->shard_cur], own + 8, &shard));
+        {
+            // grow without freeing: with CUDA IPC, peers may still map the old
+            // allocation (freed at destroy), and a freed-and-reused range
+            // cannot be re-imported while mapped
+            DevBuf& sbuf = h->shard_buf[1 - h->shard_cur];
+            const size_t need = (own + 8) * sizeof(Blk);
+            if (sbuf.cap < need) {
+                if (sbuf.p) h->shard_retired.push_back(sbuf.p);
+                sbuf.p = nullptr;
+                sbuf.cap = 0;
+                const size_t cap = need + need / 2;
+                API_CHECK(h, cudaMalloc(&sbuf.p, cap));
+                sbuf.cap = cap;
+            }
+            shard = static_cast<Blk*>(sbuf.p);
+        }
         API_CHECK(h, launch_insert_range(h->prof, h->stream, cur_dict(h), h->n, pos, gw, bint, n_ins,
                                          shard - a * kBlkPerSb, ib.tot, ib.sb_start, a, b));
-        // shard pointers (first Blk, device pointer) of every rank
-        uint64_t* d_ptrs;
-        API_CHECK(h, ensure(h->shard_ptrs, 2 * P + 8, &d_ptrs));
-        uint64_t mine[2] = {fb, (uint64_t)(uintptr_t)shard};
-        API_CHECK(h, cudaMemcpyAsync(d_ptrs + 2 * h->rank, mine, sizeof(mine), cudaMemcpyHostToDevice,
+        // every rank's (first Blk, shard address): a device pointer when the
+        // ranks share an address space (shard_dict = 1), a CUDA IPC handle of
+        // the shard allocation when they are separate processes (= 2)
+        struct ShardEntry {
+            uint64_t first, ptr;
+            cudaIpcMemHandle_t ipc;
+        };
+        ShardEntry* d_ent;
+        API_CHECK(h, ensure(h->shard_ptrs, P + 1, &d_ent));
+        ShardEntry mine{};
+        mine.first = fb;
+        mine.ptr = (uint64_t)(uintptr_t)shard;
+        if (h->shard_ipc) API_CHECK(h, cudaIpcGetMemHandle(&mine.ipc, shard));
+        API_CHECK(h, cudaMemcpyAsync(d_ent + h->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice,
                                      h->stream));
-        std::vector<uint64_t> ptr_bytes(P, 2 * sizeof(uint64_t));
+        std::vector<uint64_t> ent_bytes(P, sizeof(ShardEntry));
         if (h->allgather(ib.tot, tot_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx) ||
-            h->allgather(d_ptrs, ptr_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
+            h->allgather(d_ent, ent_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
             return SETBWTE_E_STATE;
         API_CHECK(h, launch_sb_scan(h->prof, h->stream, ib.tot, ib.nsb, ib.osb, m_new,
                                     (uint64_t*)h->d_C.p));
-        std::vector<uint64_t> all(2 * P);
-        API_CHECK(h, cudaMemcpyAsync(all.data(), d_ptrs, sizeof(uint64_t) * 2 * P,
+        std::vector<ShardEntry> all(P);
+        API_CHECK(h, cudaMemcpyAsync(all.data(), d_ent, sizeof(ShardEntry) * P,
                                      cudaMemcpyDeviceToHost, h->stream));
         API_CHECK(h, cudaStreamSynchronize(h->stream));
         Dict d = make_dict(nullptr);
         d.P = (int)P;
         for (uint64_t r = 0; r < P; ++r) {
-            d.first[r] = all[2 * r];
-            d.ptr[r] = reinterpret_cast<const Blk*>((uintptr_t)all[2 * r + 1]);
+            d.first[r] = all[r].first;
+            const Blk* ptr = reinterpret_cast<const Blk*>((uintptr_t)all[r].ptr);
+            if (h->shard_ipc && (int)r != h->rank) {
+                // open each peer allocation once, keyed by its address in the
+                // peer (allocations are never freed before destroy)
+                auto& cache = h->ipc_open[r];
+                void* opened = nullptr;
+                for (auto& kv : cache)
+                    if (kv.first == all[r].ptr) opened = kv.second;
+                if (!opened) {
+                    API_CHECK(h, cudaIpcOpenMemHandle(&opened, all[r].ipc,
+                                                      cudaIpcMemLazyEnablePeerAccess));
+                    cache.push_back({all[r].ptr, opened});
+                }
+                ptr = reinterpret_cast<const Blk*>(opened);
+            }
+            d.ptr[r] = ptr;
         }
         h->shard_dict = d;
         h->shard_cur = 1 - h->shard_cur;
@@ -1045,6 +1095,9 @@ void setbwte_destroy(setbwte_t h) {
                       &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term, &h->gfirst,
                       &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos, &h->bslot,
                       &h->bint, &h->outbuf, &h->shard_buf[0], &h->shard_buf[1], &h->shard_ptrs};
+    for (auto& cache : h->ipc_open)
+        for (auto& kv : cache) cudaIpcCloseMemHandle(kv.second);
+    for (void* p : h->shard_retired) cudaFree(p);
     for (SortScratch& ws : h->sort) ws.free_all();
     for (DevBuf* b : bufs) free_buf(*b);
     free_buf(h->stage_in);
@@ -1369,11 +1422,13 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
         if (value == 0) return SETBWTE_E_INVALID_ARG;
         h->sopt.kw1_min = value;
     } else if (!strcmp(key, "shard_dict")) {
-        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        // 1: ranks share one address space; 2: separate processes (CUDA IPC)
+        if (value > 2) return SETBWTE_E_INVALID_ARG;
         // needs the partition (world > 1, P <= 8), an empty index and no host tier
         if (value && (h->world <= 1 || h->world > kMaxShards || h->host_tier || h->n != 0))
             return SETBWTE_E_UNSUPPORTED;
         h->sharded = value != 0;
+        h->shard_ipc = value == 2;
     } else if (!strcmp(key, "insert_split")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;
