@@ -212,13 +212,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     def new_index():
         ix = SetBWTE("ACGT", block_suffixes=M)
+        after = ("insert_split", "shard_dict", "sort_split")  # need the partition first
         for kv in args.option:
             k, v = kv.split("=", 1)
-            ix.set_option(k, int(v))
+            if k not in after:
+                ix.set_option(k, int(v))
         ix.set_stream(stream)
         if world > 1:
+            # N > 1: ComputeRanks split by string and block k sorted on rank
+            # k mod N (its SA_int broadcast); Insert replicated (--option
+            # insert_split=1 / shard_dict=2 select the split / sharded forms)
             from paper_1410_0562_b200.dist import make_allgather
             ix.set_partition(rank, world, make_allgather())
+            ix.set_option("sort_split", 1)
+        for kv in args.option:
+            k, v = kv.split("=", 1)
+            if k in after:
+                ix.set_option(k, int(v))
         return ix
 
     base = None

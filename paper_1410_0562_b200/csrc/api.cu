@@ -183,6 +183,7 @@ struct setbwte_s {
     // data-parallel ComputeRanks (and, with insert_split, Insert by output range)
     int rank = 0, world = 1;
     bool insert_split = false;
+    bool sort_split = false;  // rank (k mod P) sorts block k, SA_int shared (NEXT-1 / C3)
     // NEXT-3: B_ext sharded by output superblock range across the ranks;
     // every rank keeps only its shard (ping-pong) and reads the others'
     // through their device pointers (peer / UVA)
@@ -632,6 +633,21 @@ setbwte_status merge_impl(setbwte_t h, setbwte_t o) {
     return SETBWTE_OK;
 }
 
+// sort_split (NEXT-1 across GPUs, C3): block k was sorted on rank k mod P
+// only; its SA_int reaches every rank through the allgather callback (a
+// one-contributor all-gather = a broadcast), queued on the main stream.
+setbwte_status share_sa(setbwte_t h, const BlockDesc& b, size_t k, uint32_t* saf) {
+    if (!h->sort_split || h->world <= 1) return SETBWTE_OK;
+    if (!h->allgather) return SETBWTE_E_STATE;
+    std::vector<uint64_t> bytes(h->world, 0);
+    bytes[k % (size_t)h->world] = 4 * (b.S1 - b.S0);
+    // the slices are laid out in rank order: the owner's starts at offset 0
+    // only if every earlier rank contributes 0 bytes, which holds here
+    if (h->allgather(saf, bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
+        return SETBWTE_E_STATE;
+    return SETBWTE_OK;
+}
+
 // Run Algorithm 1 over all blocks with the two-stage pipeline.
 // Run Algorithm 1 over all blocks.  ConstructSA has no B_ext dependency, so
 // two host threads ("sort lanes", one CUDA stream each) sort blocks k+1 and
@@ -699,10 +715,12 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
                 setbwte_status st0 = validate();
                 if (st0 != SETBWTE_OK) return st0;
             }
-            API_CHECK(h, sort_block(h->prof, h->stream, h->sort[0], pk.text, pk.term, blocks[k].S0,
-                                    (uint32_t)(blocks[k].S1 - blocks[k].S0), saf2, &h->sstats,
-                                    false, h->sopt));
-            setbwte_status st1 = rank_insert_stage(h, pk, blocks[k], saf2);
+            if (!h->sort_split || (int)(k % (size_t)h->world) == h->rank)
+                API_CHECK(h, sort_block(h->prof, h->stream, h->sort[0], pk.text, pk.term,
+                                        blocks[k].S0, (uint32_t)(blocks[k].S1 - blocks[k].S0),
+                                        saf2, &h->sstats, false, h->sopt));
+            setbwte_status st1 = share_sa(h, blocks[k], k, saf2);
+            if (st1 == SETBWTE_OK) st1 = rank_insert_stage(h, pk, blocks[k], saf2);
             if (st1 != SETBWTE_OK) {
                 if (k > 0) h->failed = true;
                 return st1;
@@ -735,9 +753,12 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
                 e = cudaStreamWaitEvent(L.stream, h->ev_used[l], 0);
                 if (e != cudaSuccess) break;
             }
-            e = sort_block(L.prof, L.stream, *L.ws, pk.text, pk.term, blocks[k].S0,
-                           (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st, false,
-                           h->sopt);
+            // sort_split: rank (k mod P) sorts block k; the others receive its SA_int
+            const bool mine = !h->sort_split || (int)(k % (size_t)h->world) == h->rank;
+            if (mine)
+                e = sort_block(L.prof, L.stream, *L.ws, pk.text, pk.term, blocks[k].S0,
+                               (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st, false,
+                               h->sopt);
             if (e == cudaSuccess) e = cudaEventRecord(L.ev_sorted, L.stream);
             std::lock_guard<std::mutex> lk(mu);
             if (e != cudaSuccess) {
@@ -769,7 +790,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         if (e != cudaSuccess) {
             st = from_cuda(h, e);
         } else {
-            st = rank_insert_stage(h, pk, blocks[k], lanes[l].saf);
+            st = share_sa(h, blocks[k], k, lanes[l].saf);
+            if (st == SETBWTE_OK) st = rank_insert_stage(h, pk, blocks[k], lanes[l].saf);
             if (st == SETBWTE_OK) {
                 e = cudaEventRecord(h->ev_used[l], h->stream);
                 if (e != cudaSuccess) st = from_cuda(h, e);
@@ -1429,6 +1451,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
             return SETBWTE_E_UNSUPPORTED;
         h->sharded = value != 0;
         h->shard_ipc = value == 2;
+    } else if (!strcmp(key, "sort_split")) {
+        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        h->sort_split = value != 0;
     } else if (!strcmp(key, "insert_split")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;

@@ -46,7 +46,7 @@ def _loopback(world):
     return make
 
 
-def _run_ranks(world, split, appends, M, shard=False, keep=False):
+def _run_ranks(world, split, appends, M, shard=False, keep=False, sort_split=False, lanes=None):
     from paper_1410_0562_b200 import SetBWTE
     make = _loopback(world)
     idx = []
@@ -56,6 +56,10 @@ def _run_ranks(world, split, appends, M, shard=False, keep=False):
         h.set_option("insert_split", split)
         if shard:
             h.set_option("shard_dict", 1)
+        if sort_split:
+            h.set_option("sort_split", 1)
+        if lanes is not None:
+            h.set_option("sort_lanes", lanes)
         idx.append(h)
     errs = [None] * world
 
@@ -135,3 +139,15 @@ def test_sharded_dictionary_c1_queries():
     starts = rng.integers(0, len(d) - 10, size=30)
     pats = [bytes(d[a:a + 7]).decode() for a in starts]
     assert np.array_equal(idx[2].count(pats), oracle.count(A, d, o, pats))
+
+
+@pytest.mark.parametrize("world,shard,lanes", [(2, False, None), (3, True, None), (2, True, 0),
+                                               (4, False, 1)])
+def test_sort_split(world, shard, lanes):
+    """Block k sorted on rank k mod P only; its SA_int is shared through the
+    exchange (NEXT-1 across GPUs)."""
+    d, o = synth.uniform(4000, 100, seed=31)
+    want = oracle.bwt(A, d, o, threads=None)
+    apps = _split_appends(d, o, [1500])
+    for got in _run_ranks(world, 1, apps, M=30000, shard=shard, sort_split=True, lanes=lanes):
+        assert got == want
