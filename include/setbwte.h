@@ -259,6 +259,22 @@ typedef int (*setbwte_allgather_fn)(void* buf, const uint64_t* bytes_per_rank, i
 setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,
                                      setbwte_allgather_fn allgather, void* ctx);
 
+/* Route the handle's DEVICE scratch and dictionary allocations through a
+ * caller allocator (e.g. the PyTorch caching allocator).
+ * alloc(bytes, ctx) returns a device pointer on the handle's device, 256-byte
+ * aligned, or NULL (the call that needed it then fails with
+ * SETBWTE_E_NOMEM); free_(ptr, ctx) releases one.  Both NULL restores
+ * cudaMalloc/cudaFree.  Takes effect for every allocation made after the call;
+ * a buffer is always released through the allocator that produced it, and the
+ * library drains the device (cudaDeviceSynchronize) before calling free_, so
+ * the allocator may hand the memory out again at once.  The callbacks may be
+ * invoked from the library's sort-lane threads.  Not routed: the sharded
+ * dictionary's buffers (option "shard_dict"; CUDA IPC needs cudaMalloc
+ * allocations) and pinned host memory (host tier, staging).
+ * Errors: h NULL or exactly one of alloc/free_ NULL -> SETBWTE_E_INVALID_ARG. */
+setbwte_status setbwte_set_allocator(setbwte_t h, void* (*alloc)(size_t bytes, void* ctx),
+                                     void (*free_)(void* ptr, void* ctx), void* ctx);
+
 /* Per-stage statistics of the last append as a NUL-terminated JSON object
  * written into HOST buffer out (cap bytes); *n receives the length needed
  * (including NUL).  out == NULL -> size query.  Includes per-kernel launch

@@ -26,6 +26,8 @@ _u32p = ctypes.POINTER(ctypes.c_uint32)
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, _u64p, ctypes.c_int,
                                 ctypes.c_void_p, ctypes.c_void_p)
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
 
 #: every symbol include/setbwte.h declares
 EXPORTS = [
@@ -35,7 +37,7 @@ EXPORTS = [
     "setbwte_rank", "setbwte_rank_batch", "setbwte_count", "setbwte_count_device",
     "setbwte_construct_sa", "setbwte_compute_ranks",
     "setbwte_set_option", "setbwte_set_profile", "setbwte_set_stream", "setbwte_set_partition",
-    "setbwte_stats",
+    "setbwte_set_allocator", "setbwte_stats",
     "setbwte_last_error",
 ]
 
@@ -83,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         "setbwte_set_profile": ([vp, ctypes.c_int, ctypes.c_char_p], ctypes.c_int),
         "setbwte_set_partition": ([vp, ctypes.c_int, ctypes.c_int, ALLGATHER_FN, vp],
                                   ctypes.c_int),
+        "setbwte_set_allocator": ([vp, ALLOC_FN, FREE_FN, vp], ctypes.c_int),
         "setbwte_stats": ([vp, ctypes.c_char_p, c64, _u64p], ctypes.c_int),
         "setbwte_last_error": ([vp, _u64p, _u8p], ctypes.c_int),
     }
@@ -187,6 +190,35 @@ class SetBWTE:
         self._allgather_ref = cb
         self._check(self._lib.setbwte_set_partition(self._h, rank, world, cb, None),
                     "set_partition")
+
+    def set_allocator(self, alloc=None, free=None):
+        """Route the handle's device allocations through alloc(nbytes) -> int
+        device pointer (0 = out of memory) and free(ptr).  None, None restores
+        cudaMalloc.  See setbwte_set_allocator."""
+        if alloc is None and free is None:
+            a, f = ALLOC_FN(), FREE_FN()
+        else:
+            def _a(nbytes, ctx):
+                try:
+                    return int(alloc(int(nbytes))) or None
+                except Exception:  # surfaced as SETBWTE_E_NOMEM
+                    return None
+
+            def _f(ptr, ctx):
+                free(int(ptr))
+            a, f = ALLOC_FN(_a), FREE_FN(_f)
+        self._check(self._lib.setbwte_set_allocator(self._h, a, f, None), "set_allocator")
+        # earlier callbacks stay referenced: buffers they produced are
+        # released through them
+        self._alloc_refs = getattr(self, "_alloc_refs", []) + [a, f]
+
+    def use_torch_allocator(self, device=None):
+        """Share PyTorch's CUDA caching allocator (memory shows up in
+        torch.cuda.memory_allocated and is reused across calls)."""
+        import torch
+        dev = torch.cuda.current_device() if device is None else device
+        self.set_allocator(lambda n: torch.cuda.caching_allocator_alloc(n, device=dev),
+                           torch.cuda.caching_allocator_delete)
 
     # -- append --------------------------------------------------------------
     def append(self, data, offsets):

@@ -24,34 +24,56 @@ using namespace setbwte;
 // ---------------------------------------------------------------------------
 namespace setbwte {
 
+static cudaError_t release(DevBuf& b) {
+    cudaError_t e = cudaSuccess;
+    if (b.p && b.fr) {
+        // a user allocator does not order its free against our streams (a
+        // caching allocator may hand the block out again at once): drain first
+        e = cudaDeviceSynchronize();
+        b.fr(b.p, b.fctx);
+    } else if (b.p) {
+        e = cudaFree(b.p);  // synchronises implicitly
+    }
+    b.p = nullptr;
+    b.cap = 0;
+    b.fr = nullptr;
+    b.fctx = nullptr;
+    return e;
+}
+
 cudaError_t ensure_bytes(DevBuf& b, size_t bytes) {
     if (bytes <= b.cap && b.p) return cudaSuccess;
     if (b.p) {
-        cudaError_t e = cudaFree(b.p);
-        b.p = nullptr;
-        b.cap = 0;
+        cudaError_t e = release(b);
         if (e != cudaSuccess) return e;
     }
     size_t cap = bytes + bytes / 4;  // 1.25x headroom against regrowth
-    cudaError_t e = cudaMalloc(&b.p, cap);
-    if (e != cudaSuccess) {
-        b.p = nullptr;
-        return e;
+    const Allocator* al = b.owner;
+    if (al && al->alloc) {
+        b.p = al->alloc(cap, al->ctx);
+        if (!b.p) return cudaErrorMemoryAllocation;
+        b.fr = al->free_;
+        b.fctx = al->ctx;
+    } else {
+        cudaError_t e = cudaMalloc(&b.p, cap);
+        if (e != cudaSuccess) {
+            b.p = nullptr;
+            return e;
+        }
     }
     b.cap = cap;
     return cudaSuccess;
 }
 
-static void free_buf(DevBuf& b) {
-    if (b.p) cudaFree(b.p);
-    b.p = nullptr;
-    b.cap = 0;
+static void free_buf(DevBuf& b) { release(b); }
+
+std::vector<DevBuf*> SortScratch::bufs() {
+    return {&sa0, &sa1, &k0, &k1, &segs_a, &segs_b, &small_a, &small_b, &chunks, &hist,
+            &ctr, &gtot, &groups, &kw1, &kw1b};
 }
 
 void SortScratch::free_all() {
-    for (DevBuf* b : {&sa0, &sa1, &k0, &k1, &segs_a, &segs_b, &small_a, &small_b, &chunks, &hist,
-                      &ctr, &gtot, &groups, &kw1, &kw1b})
-        free_buf(*b);
+    for (DevBuf* b : bufs()) free_buf(*b);
 }
 
 cudaEvent_t Profiler::get_event() {
@@ -159,6 +181,7 @@ struct setbwte_s {
     DevBuf in_bytes, in_off, text, term, slot_off, gfirst, bounds, err, small;
     DevBuf saf, g, pos, bint, outbuf, bslot;
     SortScratch sort[kMaxLanes];  // sort[0] also serves the inline (sort_lanes = 0) path
+    Allocator user_alloc;         // setbwte_set_allocator (empty: cudaMalloc)
 
     // options
     uint64_t M = 1ull << 24;
@@ -1047,6 +1070,19 @@ const char* setbwte_strerror(setbwte_status s) {
     return "unknown status";
 }
 
+// Every growth buffer of the handle that may come from a user allocator.  The
+// shard buffers do not: CUDA IPC (shard_dict = 2) needs cudaMalloc'd bases.
+static std::vector<DevBuf*> pooled_bufs(setbwte_t h) {
+    std::vector<DevBuf*> v = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0],
+                              &h->sb[1], &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text,
+                              &h->term, &h->gfirst, &h->slot_off, &h->bounds, &h->err, &h->small,
+                              &h->saf, &h->g, &h->pos, &h->bslot, &h->bint, &h->outbuf,
+                              &h->shard_ptrs, &h->stage_in, &h->stage_out};
+    for (SortScratch& ws : h->sort)
+        for (DevBuf* b : ws.bufs()) v.push_back(b);
+    return v;
+}
+
 setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     if (!alphabet || !out) return SETBWTE_E_INVALID_ARG;
     *out = nullptr;
@@ -1088,6 +1124,7 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     }
     h->stream = h->own_stream;
     h->sopt.pattern = &h->sort_pattern;
+    for (DevBuf* b : pooled_bufs(h)) b->owner = &h->user_alloc;
     uint8_t* dc = nullptr;
     uint8_t* ds = nullptr;
     uint64_t* dC = nullptr;
@@ -1113,17 +1150,12 @@ void setbwte_destroy(setbwte_t h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    DevBuf* bufs[] = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0], &h->sb[1],
-                      &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text, &h->term, &h->gfirst,
-                      &h->slot_off, &h->bounds, &h->err, &h->small, &h->saf, &h->g, &h->pos, &h->bslot,
-                      &h->bint, &h->outbuf, &h->shard_buf[0], &h->shard_buf[1], &h->shard_ptrs};
     for (auto& cache : h->ipc_open)
         for (auto& kv : cache) cudaIpcCloseMemHandle(kv.second);
     for (void* p : h->shard_retired) cudaFree(p);
-    for (SortScratch& ws : h->sort) ws.free_all();
-    for (DevBuf* b : bufs) free_buf(*b);
-    free_buf(h->stage_in);
-    free_buf(h->stage_out);
+    for (DevBuf* b : pooled_bufs(h)) free_buf(*b);
+    free_buf(h->shard_buf[0]);
+    free_buf(h->shard_buf[1]);
     if (h->hdict) cudaFreeHost(h->hdict);
     for (cudaStream_t ls : h->lane_stream)
         if (ls) cudaStreamSynchronize(ls);
@@ -1492,6 +1524,15 @@ setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,
     h->world = world;
     h->allgather = allgather;
     h->allgather_ctx = ctx;
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_set_allocator(setbwte_t h, void* (*alloc)(size_t, void*),
+                                     void (*free_)(void*, void*), void* ctx) {
+    if (!h || (!alloc) != (!free_)) return SETBWTE_E_INVALID_ARG;
+    h->user_alloc.alloc = alloc;
+    h->user_alloc.free_ = free_;
+    h->user_alloc.ctx = ctx;
     return SETBWTE_OK;
 }
 

@@ -13,10 +13,22 @@
 
 namespace setbwte {
 
-// Growth-only device buffer (contents are NOT preserved on growth).
+// A user device allocator (setbwte_set_allocator); empty = cudaMalloc/cudaFree.
+struct Allocator {
+    void* (*alloc)(size_t, void*) = nullptr;
+    void (*free_)(void*, void*) = nullptr;
+    void* ctx = nullptr;
+};
+
+// Growth-only device buffer (contents are NOT preserved on growth).  `owner`
+// points at the handle's allocator slot (read at every growth); `fr`/`fctx`
+// remember how the current allocation must be released.
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    const Allocator* owner = nullptr;
+    void (*fr)(void*, void*) = nullptr;
+    void* fctx = nullptr;
 };
 
 cudaError_t ensure_bytes(DevBuf& b, size_t bytes);
@@ -139,6 +151,7 @@ struct SortScratch {
     DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr, gtot, groups;
     DevBuf kw1, kw1b;  // key word 1 in position order, ping-pong (large blocks only)
     void free_all();
+    std::vector<DevBuf*> bufs();
 };
 struct SortStats {
     uint64_t digit_passes = 0;

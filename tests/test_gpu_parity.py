@@ -652,3 +652,52 @@ def test_replayed_pattern_that_does_not_fit(SetBWTE):
     assert idx.bwt() == want
     st = idx.stats()["sort"]
     assert st["replayed_blocks"] >= 1 and st["rounds_after_replay"] >= 1, st
+
+
+# --- caller allocator (setbwte_set_allocator) --------------------
+
+def test_torch_caching_allocator(SetBWTE, c1):
+    """Every handle allocation comes from torch's caching allocator (also from
+    the sort-lane threads) and is handed back at destroy; results unchanged."""
+    import torch
+    d, o, want = c1
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    idx = SetBWTE(A, block_suffixes=20000)
+    idx.use_torch_allocator()
+    (a_d, a_o), (b_d, b_o) = _split(d, o, 300)
+    idx.append(a_d, a_o)
+    idx.append(b_d, b_o)  # larger: buffers regrow through the allocator
+    assert idx.bwt() == want
+    assert torch.cuda.memory_allocated() - base > 4 * len(d)
+    idx.close()
+    assert torch.cuda.memory_allocated() == base
+
+
+def test_counting_allocator_and_restore(SetBWTE):
+    import torch
+    live = {}
+
+    def alloc(n):
+        t = torch.empty(n, dtype=torch.uint8, device="cuda")
+        live[t.data_ptr()] = t
+        return t.data_ptr()
+
+    def free(p):
+        del live[p]
+    d, o = synth.uniform(40, 60, seed=77)
+    idx = SetBWTE(A, block_suffixes=100)
+    idx.append(d[: int(o[10])], o[:11])   # cudaMalloc'd buffers
+    idx.set_allocator(alloc, free)
+    idx.append(d[int(o[10]):], o[10:] - o[10])
+    assert idx.bwt() == oracle.bwt(A, d, o)
+    assert live
+    idx.set_allocator(None, None)
+    idx.close()
+    assert not live
+    # an allocator that fails: E_NOMEM, handle reports it
+    idx = SetBWTE(A)
+    idx.set_allocator(lambda n: 0, lambda p: None)
+    from paper_1410_0562_b200.binding import SetBWTEError
+    with pytest.raises(SetBWTEError, match="E_NOMEM"):
+        idx.append(d, o)
