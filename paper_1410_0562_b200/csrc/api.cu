@@ -76,6 +76,30 @@ void SortScratch::free_all() {
     for (DevBuf* b : bufs()) free_buf(*b);
 }
 
+static std::atomic<uint64_t> g_trace_ns[TR_N], g_trace_cnt[TR_N];
+
+bool trace_on() {
+    static const bool on = getenv("SETBWTE_TRACE") && atoi(getenv("SETBWTE_TRACE")) > 0;
+    return on;
+}
+
+void trace_add(int id, uint64_t ns) {
+    g_trace_ns[id] += ns;
+    g_trace_cnt[id] += 1;
+}
+
+void trace_dump() {
+    if (!trace_on()) return;
+    static const char* names[TR_N] = {"sort_readback", "meminfo", "append_sync", "validate",
+                                      "rank_wait", "lane_join", "final_sync", "total"};
+    fprintf(stderr, "[setbwte trace]");
+    for (int i = 0; i < TR_N; ++i) {
+        fprintf(stderr, " %s=%.2fms/%llu", names[i], g_trace_ns[i].exchange(0) / 1e6,
+                (unsigned long long)g_trace_cnt[i].exchange(0));
+    }
+    fprintf(stderr, "\n");
+}
+
 cudaEvent_t Profiler::get_event() {
     if (!pool.empty()) {
         cudaEvent_t e = pool.back();
@@ -187,6 +211,8 @@ struct setbwte_s {
     uint64_t M = 1ull << 24;
     int rank_ilp = 1;
     int sort_lanes = 3;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
+    uint64_t lanes_checked_suf = 0;  // largest block the lane count was checked against free memory
+    int lanes_checked_nl = 0;        // ... and the lane count that fitted
     uint64_t hbm_budget = ~0ull;  // max bytes of B_ext dictionary kept in HBM
 
     // host tier: B_ext's dictionary in pinned, mapped
@@ -698,14 +724,21 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         total += b.S1 - b.S0;
     }
     int NL = std::max(1, std::min<int>({h->sort_lanes, (int)K, setbwte_s::kMaxLanes}));
-    {
+    if (NL > 1 && (max_suf > h->lanes_checked_suf || NL > h->lanes_checked_nl)) {
         // each lane owns a sort scratch (~30 B per suffix of the largest
-        // block): keep the lanes within half of the free device memory
+        // block): keep the lanes within half of the free device memory.
+        // Queried only when the scratch may grow: cudaMemGetInfo measured
+        // up to 10 ms while other streams of the process are busy.
         size_t free_b = 0, total_b = 0;
+        TraceScope tr(TR_MEMINFO);
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
             const double per_lane = 30.0 * (double)max_suf;
             while (NL > 1 && per_lane * NL > 0.5 * (double)free_b) --NL;
         }
+        h->lanes_checked_suf = max_suf;
+        h->lanes_checked_nl = NL;
+    } else if (NL > 1) {
+        NL = std::min(NL, h->lanes_checked_nl);
     }
     // reserve everything up front: a cudaFree/cudaMalloc mid-loop would
     // serialise the streams
@@ -796,7 +829,11 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
     std::vector<std::thread> threads;
     for (int l = 0; l < NL; ++l) threads.emplace_back(lane_main, l);
 
-    setbwte_status st = validate();
+    setbwte_status st;
+    {
+        TraceScope tr(TR_VALIDATE);
+        st = validate();
+    }
     if (st != SETBWTE_OK) {
         std::lock_guard<std::mutex> lk(mu);
         abort = true;
@@ -804,6 +841,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
     }
     for (size_t k = 0; k < K && st == SETBWTE_OK; ++k) {
         {
+            TraceScope tr(TR_RANK_WAIT);
             std::unique_lock<std::mutex> lk(mu);
             cv.wait(lk, [&] { return sorted[k] || abort; });
             if (abort) break;
@@ -830,7 +868,10 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         used[k] = 1;
         cv.notify_all();
     }
-    for (std::thread& t : threads) t.join();
+    {
+        TraceScope tr(TR_LANE_JOIN);
+        for (std::thread& t : threads) t.join();
+    }
     if (st == SETBWTE_OK && lane_err != cudaSuccess) {
         if (h->n != 0) h->failed = true;
         st = from_cuda(h, lane_err);
@@ -967,7 +1008,10 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
                                  h->stream));
     API_CHECK(h, cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(uint64_t) * 2 * pre,
                                  cudaMemcpyDeviceToHost, h->stream));
-    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    {
+        TraceScope tr(TR_APPEND_SYNC);
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+    }
     // an early return must not leave H2D copies reading the caller's buffer
     auto abort_with = [&](setbwte_status st) {
         cudaStreamSynchronize(h->h2d_stream);
@@ -1043,7 +1087,10 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     API_CHECK(h, cudaEventRecord(h->ev_start, h->copy_stream));
     API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
     if (st != SETBWTE_OK) return st;
-    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    {
+        TraceScope tr(TR_FINAL_SYNC);
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+    }
     API_CHECK(h, h->prof.resolve());
     build_stats(h);
     return SETBWTE_OK;
@@ -1184,7 +1231,13 @@ static setbwte_status add_device(setbwte_t h, const uint8_t* d_strings, const ui
                                  uint64_t m, bool prepend) {
     API_ENTER(h);
     if (m > 0 && !d_offsets) return SETBWTE_E_INVALID_ARG;
-    return append_impl(h, nullptr, nullptr, d_strings, d_offsets, m, ~0ull, prepend);
+    setbwte_status st;
+    {
+        TraceScope tr(TR_TOTAL);
+        st = append_impl(h, nullptr, nullptr, d_strings, d_offsets, m, ~0ull, prepend);
+    }
+    trace_dump();
+    return st;
 }
 
 static setbwte_status add_host(setbwte_t h, const uint8_t* strings, const uint64_t* offsets,
@@ -1203,7 +1256,13 @@ static setbwte_status add_host(setbwte_t h, const uint8_t* strings, const uint64
     API_CHECK(h, ensure(h->in_off, m + 1, &dof));
     API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                  h->stream));
-    return append_impl(h, strings, offsets, db, dof, m, nb, prepend);
+    setbwte_status st;
+    {
+        TraceScope tr(TR_TOTAL);
+        st = append_impl(h, strings, offsets, db, dof, m, nb, prepend);
+    }
+    trace_dump();
+    return st;
 }
 
 setbwte_status setbwte_append_device(setbwte_t h, const uint8_t* d_strings,

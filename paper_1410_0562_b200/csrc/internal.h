@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <string>
@@ -249,5 +251,23 @@ cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Dict& blk, uint6
 // Debug/export: SA + B_int ASCII of a sorted block.
 cudaError_t launch_bint_ascii(Profiler& prof, cudaStream_t s, const uint8_t* bint,
                               uint32_t n_suf, const uint8_t* sym_ascii, uint8_t* out);
+
+// Host-side wait tracing (env SETBWTE_TRACE=1): wall time spent in each kind
+// of host wait, summed over all threads, printed to stderr after each append.
+enum TraceId { TR_SORT_READBACK, TR_MEMINFO, TR_APPEND_SYNC, TR_VALIDATE, TR_RANK_WAIT,
+               TR_LANE_JOIN, TR_FINAL_SYNC, TR_TOTAL, TR_N };
+bool trace_on();
+void trace_add(int id, uint64_t ns);
+void trace_dump();
+struct TraceScope {
+    int id;
+    std::chrono::steady_clock::time_point t0;
+    explicit TraceScope(int i) : id(i), t0(std::chrono::steady_clock::now()) {}
+    ~TraceScope() {
+        if (trace_on())
+            trace_add(id, (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                              std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 }  // namespace setbwte

@@ -1743,8 +1743,11 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     // in-driver wait measured faster than pinned memory + a stream sync)
     auto read_back = [&]() -> cudaError_t {
         uint32_t h_all[2 * NCLASS + M_N];
-        SB_CHECK(cudaMemcpyAsync(h_all, ctr, sizeof(h_all), cudaMemcpyDeviceToHost, s));
-        SB_CHECK(cudaStreamSynchronize(s));
+        {
+            TraceScope tr(TR_SORT_READBACK);
+            SB_CHECK(cudaMemcpyAsync(h_all, ctr, sizeof(h_all), cudaMemcpyDeviceToHost, s));
+            SB_CHECK(cudaStreamSynchronize(s));
+        }
         memcpy(h_cnt, h_all + (in.cnt - ctr), sizeof(h_cnt));
         memcpy(h_oth, h_all + (out.cnt - ctr), sizeof(h_oth));
         memcpy(h_misc, h_all + 2 * NCLASS, sizeof(h_misc));

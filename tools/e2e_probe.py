@@ -1,40 +1,69 @@
-"""Break the e2e step into its parts (append from device / host, BWT read-back)."""
-import os
+"""Where the end-to-end c2 step's time goes (GPU box): wall-clock of
+append_device / append from pinned host / bwt into pinned host / bwt_device."""
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
-import torch  # noqa: E402
+import numpy as np
+import torch
 
-import synth  # noqa: E402
+sys.path.insert(0, ".")
+import bench  # noqa: E402
 from paper_1410_0562_b200 import SetBWTE  # noqa: E402
 
-d, o = synth.uniform(1_000_000, 100, seed=1)
-pd = torch.from_numpy(d).pin_memory()
-po = torch.from_numpy(o.view(np.int64)).pin_memory()
-dd, do = pd.cuda(), po.cuda()
-out = torch.empty(int(o[-1]) + len(o) - 1, dtype=torch.uint8).pin_memory()
+data, offsets = bench.gen("c2")
+m = len(offsets) - 1
+dev = torch.device("cuda:0")
+d_data = torch.from_numpy(data).to(dev)
+d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
+pin_data = torch.from_numpy(data).pin_memory()
+pin_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
+np_data, np_off = pin_data.numpy(), pin_off.numpy().view(np.uint64)
 idx = SetBWTE("ACGT", block_suffixes=1 << 24)
+pin_out = torch.empty(int(offsets[-1]) + m, dtype=torch.uint8).pin_memory()
+d_out = torch.empty_like(pin_out, device=dev)
 
 
-def t(f, n=5):
-    for _ in range(2):
-        f()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(n):
-        t0 = time.perf_counter()
+def t(f, reps=12):
+    out = []
+    for _ in range(reps):
+        idx.clear()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
         f()
         torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
-    return 1000 * min(ts)
+        out.append((time.perf_counter() - a) * 1e3)
+    return "min %.2f med %.2f ms  all %s" % (min(out), sorted(out)[len(out) // 2],
+                                            " ".join("%.1f" % x for x in out))
 
 
-print("append_device ms", t(lambda: (idx.clear(), idx.append_device(dd, do))))
-print("append_host   ms", t(lambda: (idx.clear(), idx.append(pd.numpy(), po.numpy().view(np.uint64)))))
-print("bwt_host      ms", t(lambda: idx.bwt(out)))
-dev_out = torch.empty_like(out, device="cuda")
-print("bwt_device    ms", t(lambda: idx.bwt_device(dev_out)))
-print("h2d 100MB     ms", t(lambda: dd.copy_(pd, non_blocking=True)))
-print("d2h 101MB     ms", t(lambda: out.copy_(dev_out, non_blocking=True)))
+for _ in range(3):
+    idx.clear()
+    idx.append_device(d_data, d_off, m)
+torch.cuda.synchronize()
+print("append_device      ", t(lambda: idx.append_device(d_data, d_off, m)))
+print("append pinned host ", t(lambda: idx.append(np_data, np_off)))
+print("append pageable    ", t(lambda: idx.append(data, offsets)))
+print("append+bwt pinned  ", t(lambda: (idx.append(np_data, np_off), idx.bwt(pin_out))))
+print("append_device again", t(lambda: idx.append_device(d_data, d_off, m)))
+idx.clear()
+idx.append_device(d_data, d_off, m)
+torch.cuda.synchronize()
+
+
+def tb(f, reps=6):
+    out = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        f()
+        torch.cuda.synchronize()
+        out.append((time.perf_counter() - a) * 1e3)
+    return "min %.2f med %.2f ms" % (min(out), sorted(out)[len(out) // 2])
+
+
+print("bwt pinned host    ", tb(lambda: idx.bwt(pin_out)))
+print("bwt device         ", tb(lambda: idx.bwt_device(d_out)))
+print("torch H2D 108MB    ", tb(lambda: (d_data.copy_(pin_data, non_blocking=True), d_off.copy_(pin_off, non_blocking=True))))
+print("torch D2H 101MB    ", tb(lambda: pin_out.copy_(d_out, non_blocking=True)))
+import os
+print("cpus", os.cpu_count(), "load", os.getloadavg())
