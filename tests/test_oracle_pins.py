@@ -262,3 +262,26 @@ def test_oracle_count_pins():
         pats = ["".join(rng.choice(list("ACGT"), size=int(rng.integers(1, 5)))) for _ in range(20)]
         got = oracle.count(A, d, o, pats)
         assert list(got) == [brute.naive_count(p, strings) for p in pats]
+
+
+# --- sigma = 5 (N; NEXT-4 groundwork): the oracle is alphabet-generic
+
+A5 = "ACGTN"  # code order A < C < G < T < N (SPEC's default alphabet)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sigma5_bwt_and_ranks_equal_brute_force(seed):
+    d, o = synth.random_set(8000 + seed, max_m=12, max_len=14, alphabet=["ACGTN", "NA", "TN"][seed % 3])
+    strings = synth.to_strings(d, o)
+    assert oracle.bwt(A5, d, o).decode() == brute.brute_bwt(strings, A5)
+    cut = len(strings) // 2
+    g = list(oracle.compute_ranks(A5, d, o, m_ext=cut))
+    assert g == brute.brute_g(strings[:cut], strings[cut:], A5)
+    pats = ["N", "AN", "NN", "TNA", "GT"]
+    assert list(oracle.count(A5, d, o, pats)) == [brute.naive_count(p, strings) for p in pats]
+
+
+@pytest.mark.parametrize("s", ["NNNN", "GATNACA", "N", "ANTN"])
+def test_sigma5_single_string_is_textbook_bwt(s):
+    d, o = _fs([s])
+    assert oracle.bwt(A5, d, o).decode() == brute.rotation_bwt(s, A5)
