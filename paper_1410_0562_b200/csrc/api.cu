@@ -1081,8 +1081,26 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     std::vector<BlockDesc> order(blocks);
     if (prepend) std::reverse(order.begin(), order.end());
     h->prepending = prepend;
-    setbwte_status st = run_blocks(h, pk, order, validate);
+    // An empty index has nothing to roll back: the first Insert need not wait
+    // for the whole input to be on the device and validated (with host input,
+    // the last chunk arrives ~2 ms into a c2 call).  A bad byte found at the
+    // end empties the index again.
+    const bool defer = h->n == 0;
+    setbwte_status st = run_blocks(h, pk, order,
+                                   defer ? std::function<setbwte_status()>(
+                                               []() { return SETBWTE_OK; })
+                                         : std::function<setbwte_status()>(validate));
     h->prepending = false;
+    if (defer && st == SETBWTE_OK) {
+        st = validate();
+        if (st == SETBWTE_E_INVALID_CHAR) {
+            API_CHECK(h, cudaStreamSynchronize(h->stream));
+            h->n = 0;
+            h->m = 0;
+            h->cur = 0;
+            API_CHECK(h, cudaMemset(h->d_C.p, 0, 8 * sizeof(uint64_t)));
+        }
+    }
     // the main stream joins the copy stream (the bytes buffer is reused later)
     API_CHECK(h, cudaEventRecord(h->ev_start, h->copy_stream));
     API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));

@@ -701,3 +701,35 @@ def test_counting_allocator_and_restore(SetBWTE):
     from paper_1410_0562_b200.binding import SetBWTEError
     with pytest.raises(SetBWTEError, match="E_NOMEM"):
         idx.append(d, o)
+
+
+# --- invalid input into an EMPTY index: validation deferred to the end ----------
+
+@pytest.mark.parametrize("lanes", [0, 3])
+@pytest.mark.parametrize("device", [False, True])
+def test_invalid_char_into_empty_index(SetBWTE, lanes, device):
+    """An empty index validates host input only after the blocks were inserted
+    (nothing to roll back); a bad byte in a late block empties it again and
+    reports the same position as the eager check."""
+    import torch
+    from paper_1410_0562_b200 import SetBWTEError
+    d, o = synth.uniform(3000, 50, seed=5)
+    bad = d.copy()
+    bad_pos = int(o[2900]) + 7
+    bad[bad_pos] = ord("X")
+    idx = SetBWTE(A, block_suffixes=5000)
+    idx.set_option("sort_lanes", lanes)
+    with pytest.raises(SetBWTEError) as e:
+        if device:
+            idx.append_device(torch.from_numpy(bad).cuda(), torch.from_numpy(o.view(np.int64)).cuda())
+        else:
+            idx.append(bad, o)
+    assert e.value.name == "E_INVALID_CHAR"
+    assert idx.last_error() == (bad_pos, ord("X"))
+    assert idx.size() == (0, 0) and idx.bwt() == b""
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
+    # a non-empty index still rejects before its first Insert (unchanged)
+    with pytest.raises(SetBWTEError):
+        idx.append(bad, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
