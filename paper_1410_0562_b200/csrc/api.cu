@@ -1085,7 +1085,7 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     // for the whole input to be on the device and validated (with host input,
     // the last chunk arrives ~2 ms into a c2 call).  A bad byte found at the
     // end empties the index again.
-    const bool defer = h->n == 0;
+    const bool defer = h->n == 0 && !h->sharded && !h->host_tier;  // plain HBM index only
     setbwte_status st = run_blocks(h, pk, order,
                                    defer ? std::function<setbwte_status()>(
                                                []() { return SETBWTE_OK; })
