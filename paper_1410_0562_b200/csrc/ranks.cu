@@ -41,8 +41,11 @@ __device__ __forceinline__ void store4<uint64_t>(uint64_t* dst, uint64_t a, uint
 }
 
 // D = const Blk* (one array) or Dict (a sharded dictionary, NEXT-3)
+#ifndef SB_RANK_MINB
+#define SB_RANK_MINB 1
+#endif
 template <class G, class D>
-__global__ void __launch_bounds__(256) compute_ranks_kernel(
+__global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
     uint64_t j1, uint64_t slot_base, const D blk, const uint64_t* __restrict__ sb,
     const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot,
