@@ -88,13 +88,19 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        """Start sampling; returns once nvidia-smi produces lines (its start-up
+        can take longer than a short timed region), so every timed step is
+        covered.  The lines seen while waiting are dropped."""
+        self.ready = threading.Event()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            self.ready.wait(timeout=10.0)
+            self.lines = []
         except Exception:
             self.proc = None
 
@@ -108,6 +114,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
+            self.ready.set()
             if not self.paused:
                 self.lines.append(line.strip())
 
@@ -294,10 +301,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     launches = 0
     blocks = None
     sampler = ClockSampler(local_rank)
+    sampler.start()                          # returns once samples flow
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    sampler.start()
     times = []
     for _ in range(args.steps):
         if base is not None:
