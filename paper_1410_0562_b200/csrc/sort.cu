@@ -51,6 +51,12 @@ constexpr uint32_t kGroup = 32;    // chunks per prefix group
 #ifndef SB_DIG_IPT
 #define SB_DIG_IPT 8
 #endif
+// SB_SCATTER_L2: 0 = the scatter reads its input evict-first and writes the
+// next pass's (key, slot) with streaming stores; 1 = plain stores and
+// evict-normal reads, so a c2-sized pass can hit L2 in the next one
+#ifndef SB_SCATTER_L2
+#define SB_SCATTER_L2 0
+#endif
 constexpr int kDigNt = SB_DIG_NT;  // digit-pass CTA
 constexpr int kDigIpt = SB_DIG_IPT;
 constexpr int kDigTile = kDigNt * kDigIpt;
@@ -709,7 +715,11 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     const uint32_t nch = misc[M_CHUNKS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint64_t pol_ef;
+#if SB_SCATTER_L2
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_ef));
+#else
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+#endif
 
     // Tiles of this CTA's chunks in order; the next tile's keys (and slots)
     // are prefetched into shared memory with cp.async while the current one
@@ -836,9 +846,15 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
                 SB_ASSERT(gp < B.n);
                 __stcs(B.saf + gp, kv.y);
             } else {
+#if SB_SCATTER_L2
+                S2[gp] = kv.y;
+                K2[gp] = kv.x;
+                if (K1) K12[gp] = s_k1[i];
+#else
                 __stcs(S2 + gp, kv.y);
                 __stcs(K2 + gp, kv.x);
                 if (K1) __stcs(K12 + gp, s_k1[i]);
+#endif
             }
         }
     }
