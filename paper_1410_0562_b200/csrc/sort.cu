@@ -51,11 +51,11 @@ constexpr uint32_t kGroup = 32;    // chunks per prefix group
 #ifndef SB_DIG_IPT
 #define SB_DIG_IPT 8
 #endif
-// SB_SCATTER_L2: 0 = the scatter reads its input evict-first and writes the
+// SB_SCATTER_L2 (default 1): 0 = the scatter reads its input evict-first and writes the
 // next pass's (key, slot) with streaming stores; 1 = plain stores and
 // evict-normal reads, so a c2-sized pass can hit L2 in the next one
 #ifndef SB_SCATTER_L2
-#define SB_SCATTER_L2 0
+#define SB_SCATTER_L2 1
 #endif
 constexpr int kDigNt = SB_DIG_NT;  // digit-pass CTA
 constexpr int kDigIpt = SB_DIG_IPT;
