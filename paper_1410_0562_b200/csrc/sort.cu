@@ -465,7 +465,10 @@ __global__ void chunkify_kernel(Lists in, SegX* __restrict__ segx, Chunk* __rest
     }
 }
 
-__global__ void __launch_bounds__(kDigNt) digit_hist_kernel(Lists in, const Chunk* __restrict__ chunks,
+#ifndef SB_HIST_MINB
+#define SB_HIST_MINB 1
+#endif
+__global__ void __launch_bounds__(kDigNt, SB_HIST_MINB) digit_hist_kernel(Lists in, const Chunk* __restrict__ chunks,
                                                             const uint32_t* misc, Bufs B,
                                                             uint32_t* __restrict__ hist) {
     constexpr int NW = kDigNt / 32;
