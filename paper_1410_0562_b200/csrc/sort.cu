@@ -466,7 +466,7 @@ __global__ void chunkify_kernel(Lists in, SegX* __restrict__ segx, Chunk* __rest
 }
 
 #ifndef SB_HIST_MINB
-#define SB_HIST_MINB 1
+#define SB_HIST_MINB 4
 #endif
 __global__ void __launch_bounds__(kDigNt, SB_HIST_MINB) digit_hist_kernel(Lists in, const Chunk* __restrict__ chunks,
                                                             const uint32_t* misc, Bufs B,
