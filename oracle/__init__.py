@@ -17,6 +17,10 @@ Functions and the passage each follows (P:<line> = /root/reference/PAPER.md):
 * ``suffix_rank``   -- SA position of one suffix by counting (definition)
 * ``count``         -- substring occurrences by literal comparison (what the
                        FM-index count answers)
+* ``bwt_bucketed``  -- ``bwt`` in bucketed low-memory mode: suffixes
+                       partitioned by their first h symbols ($ first), each
+                       bucket sorted with the same comparator and emitted in
+                       key order, streamed to a callback (configs c3-c5)
 
 Pins for each are in ``tests/test_oracle_pins.py``; see DESIGN.md "Oracle pins".
 """
@@ -35,6 +39,7 @@ _lib = None
 
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 _u8p = ctypes.POINTER(ctypes.c_uint8)
+_EMIT = ctypes.CFUNCTYPE(None, _u8p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p)
 
 
 class OracleError(RuntimeError):
@@ -72,6 +77,9 @@ def _load():
         lib.oracle_suffix_rank.argtypes = [ctypes.c_char_p, _u8p, _u64p, ctypes.c_uint64,
                                            ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_int,
                                            _u64p]
+        lib.oracle_bwt_bucketed.argtypes = [ctypes.c_char_p, _u8p, _u64p, ctypes.c_uint64,
+                                            ctypes.c_int, ctypes.c_uint64, _EMIT,
+                                            ctypes.c_void_p, ctypes.c_int, _u64p]
         _lib = lib
     return _lib
 
@@ -203,3 +211,30 @@ def count(alphabet: str, data, offsets, patterns, threads: int | None = 1) -> np
     if rc:
         raise OracleError("oracle error %d" % rc)
     return out[:len(bs)]
+
+
+def bwt_bucketed(alphabet: str, data, offsets, sink, h: int = 3,
+                 batch_cap: int = 1 << 29, threads: int | None = None) -> int:
+    """The one-shot BWT (Eq.(1)) in bucketed mode: ``sink(chunk: bytes, bucket: int)``
+    receives the BWT bucket by bucket, in order (their concatenation is
+    ``bwt(...)``).  Memory: the text codes plus ~9 B x ``batch_cap``.
+    Returns n."""
+    data, dp = _u8(data)
+    offsets, op = _u64(offsets)
+    m = len(offsets) - 1
+    err = []
+
+    def _emit(ptr, ln, bucket, _ctx):
+        try:
+            sink(ctypes.string_at(ptr, ln), int(bucket))
+        except BaseException as e:  # pragma: no cover - surfaced below
+            err.append(e)
+
+    cb = _EMIT(_emit)
+    bad = ctypes.c_uint64(0)
+    rc = _load().oracle_bwt_bucketed(alphabet.encode(), dp, op, m, int(h), int(batch_cap), cb,
+                                     None, _threads(threads), ctypes.byref(bad))
+    if err:
+        raise err[0]
+    _check(rc, bad)
+    return int(offsets[-1]) + m

@@ -167,6 +167,107 @@ int oracle_bwt(const char* alphabet, const uint8_t* bytes, const uint64_t* off, 
     return 0;
 }
 
+/* The same one-shot BWT (Eq.(1) P:33-35 on T of P:36-37) in a BUCKETED,
+ * low-memory mode (SURVEY.md section 8(c) "Bucketed mode"), for sets whose
+ * suffix ids do not fit in RAM at once (configs c3-c5, up to 6 G suffixes).
+ *
+ *   1. Every suffix (j,k) gets a bucket key: its first h symbols as the digits
+ *      of a base-(sigma+1) number, the terminator and every position after it
+ *      written as digit 0 (the smallest symbol).  If two suffixes have
+ *      different keys, the first differing digit is a position where both are
+ *      still inside their strings, or where exactly one of them meets its
+ *      terminator; either way suf_less decides the same way as the keys.  So
+ *      bucket order is suffix order, and sorting each bucket with suf_less
+ *      and emitting the buckets in key order is the full sort.
+ *   2. Count the members of every bucket (one pass over all suffixes).
+ *   3. Take the buckets in key order, as many as fit in `batch_cap` suffixes
+ *      (at least one), collect their members, sort each bucket with suf_less
+ *      (the library sort, as in oracle_bwt) and emit B for it (Eq.(1)).
+ *
+ * Output: `emit(chunk, len, bucket_key, ctx)` is called once per non-empty
+ * bucket, in order; the concatenation of the chunks is oracle_bwt's output.
+ * Memory: the codes of the text plus batch_cap * 9 bytes. */
+typedef void (*oracle_emit_fn)(const uint8_t* chunk, uint64_t len, uint64_t bucket, void* ctx);
+
+int oracle_bwt_bucketed(const char* alphabet, const uint8_t* bytes, const uint64_t* off,
+                        uint64_t m, int h, uint64_t batch_cap, oracle_emit_fn emit, void* ctx,
+                        int threads, uint64_t* bad_pos) {
+    if (h < 1 || h > 8 || !emit || batch_cap == 0) return -1;
+    Text t;
+    int rc = encode(alphabet, bytes, off, m, &t, bad_pos);
+    if (rc) return rc;
+    if (m >= 0xffffffffull) return -1;
+    const uint64_t base = (uint64_t)strlen(alphabet) + 1;
+    uint64_t nb = 1;
+    for (int d = 0; d < h; ++d) nb *= base;
+    if (nb > (1ull << 24)) return -1;
+    if (threads < 1) threads = 1;
+    auto key_of = [&](uint32_t j, uint64_t k) {
+        const uint64_t L = len_of(t, j);
+        uint64_t key = 0;
+        for (int d = 0; d < h; ++d) {
+            const uint64_t p = k + (uint64_t)d;
+            const uint64_t x = p < L ? (uint64_t)t.code[t.off[j] + p] : 0; /* $ and after */
+            key = key * base + x;
+        }
+        return key;
+    };
+    /* 2. bucket sizes, per thread (static schedule: the same string ranges
+     *    per thread in every pass below). */
+    std::vector<std::vector<uint64_t>> cnt(threads, std::vector<uint64_t>(nb, 0));
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t j = 0; j < (int64_t)m; ++j) {
+        std::vector<uint64_t>& c = cnt[omp_get_thread_num()];
+        const uint64_t L = len_of(t, (uint32_t)j);
+        for (uint64_t k = 0; k <= L; ++k) ++c[key_of((uint32_t)j, k)];
+    }
+    std::vector<uint64_t> total(nb, 0);
+    for (int th = 0; th < threads; ++th)
+        for (uint64_t b = 0; b < nb; ++b) total[b] += cnt[th][b];
+    std::vector<Suf> v;
+    std::vector<uint8_t> out;
+    for (uint64_t b0 = 0; b0 < nb;) {
+        /* 3. the batch [b0, b1) */
+        uint64_t b1 = b0, size = 0;
+        while (b1 < nb && (b1 == b0 || size + total[b1] <= batch_cap)) size += total[b1++];
+        if (size == 0) { b0 = b1; continue; }
+        /* where each thread writes each bucket's members inside the batch */
+        std::vector<uint64_t> start(b1 - b0 + 1, 0);
+        for (uint64_t b = b0; b < b1; ++b) start[b - b0 + 1] = start[b - b0] + total[b];
+        std::vector<std::vector<uint64_t>> wr(threads, std::vector<uint64_t>(b1 - b0));
+        for (uint64_t b = b0; b < b1; ++b) {
+            uint64_t acc = start[b - b0];
+            for (int th = 0; th < threads; ++th) { wr[th][b - b0] = acc; acc += cnt[th][b]; }
+        }
+        v.assign(size, Suf{0, 0});
+#pragma omp parallel for num_threads(threads) schedule(static)
+        for (int64_t j = 0; j < (int64_t)m; ++j) {
+            std::vector<uint64_t>& w = wr[omp_get_thread_num()];
+            const uint64_t L = len_of(t, (uint32_t)j);
+            for (uint64_t k = 0; k <= L; ++k) {
+                const uint64_t key = key_of((uint32_t)j, k);
+                if (key >= b0 && key < b1) v[w[key - b0]++] = Suf{(uint32_t)j, (uint32_t)k};
+            }
+        }
+        out.resize(size);
+        for (uint64_t b = b0; b < b1; ++b) {
+            const uint64_t s0 = start[b - b0], s1 = start[b - b0 + 1];
+            if (s0 == s1) continue;
+            std::vector<Suf> bucket(v.begin() + s0, v.begin() + s1);
+            sort_sufs(t, bucket, threads);
+            /* B[i] = T[(SA[i]-1) mod n], Eq.(1): S_j[k-1] if k > 0, else '$' */
+            for (uint64_t i = 0; i < bucket.size(); ++i) {
+                const Suf& s = bucket[i];
+                out[s0 + i] = s.k > 0 ? (uint8_t)alphabet[t.code[off[s.j] + s.k - 1] - 1]
+                                      : (uint8_t)'$';
+            }
+            emit(out.data() + s0, s1 - s0, b, ctx);
+        }
+        b0 = b1;
+    }
+    return 0;
+}
+
 /* ConstructSA of one block (Alg.1): the block's strings are sorted among
  * themselves only, terminators ordered by string index.  sa_out
  * receives n_suf slot ids, slot(j,k) = off[j] + j + k (string-major layout,

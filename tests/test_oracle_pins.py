@@ -285,3 +285,60 @@ def test_sigma5_bwt_and_ranks_equal_brute_force(seed):
 def test_sigma5_single_string_is_textbook_bwt(s):
     d, o = _fs([s])
     assert oracle.bwt(A5, d, o).decode() == brute.rotation_bwt(s, A5)
+
+
+# --- bucketed low-memory mode (used for the c3-c5 golden digests)
+
+def _bucketed(alpha, d, o, h, cap, threads=2):
+    parts, keys = [], []
+    oracle.bwt_bucketed(alpha, d, o, lambda c, b: (parts.append(c), keys.append(b)),
+                        h=h, batch_cap=cap, threads=threads)
+    return b"".join(parts), keys, parts
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_bucketed_bwt_equals_brute_force(seed):
+    """Bucketed mode against the brute force over the materialised integer
+    text (tests/brute.py, different code), for h = 1..4 and batch caps that
+    force one bucket per batch, a few buckets per batch, and one batch."""
+    alpha = ["ACGT", "AC", "A", "ACGTN"][seed % 4]
+    d, o = synth.random_set(9100 + seed, max_m=20, max_len=16,
+                            alphabet=alpha if alpha != "ACGTN" else "ACGTN")
+    strings = synth.to_strings(d, o)
+    want = brute.brute_bwt(strings, alpha).encode()
+    for h in (1, 2, 3, 4):
+        for cap in (1, 5, 1 << 20):
+            got, _, _ = _bucketed(alpha, d, o, h, cap)
+            assert got == want, (h, cap)
+
+
+def test_bucketed_bucket_sizes_and_order():
+    """Each emitted chunk is exactly the bucket of suffixes sharing that
+    h-symbol prefix ($ and after as digit 0), emitted in increasing key order:
+    counted here by slicing the strings in Python."""
+    d, o = synth.random_set(9301, max_m=30, max_len=12)
+    strings = synth.to_strings(d, o)
+    h, base = 2, 5
+    want = {}
+    for s in strings:
+        for k in range(len(s) + 1):
+            key = 0
+            for p in range(k, k + h):
+                key = key * base + ("ACGT".index(s[p]) + 1 if p < len(s) else 0)
+            want[key] = want.get(key, 0) + 1
+    _, keys, parts = _bucketed(A, d, o, h, 3)
+    assert keys == sorted(want)
+    assert [len(p) for p in parts] == [want[k] for k in keys]
+
+
+@pytest.mark.parametrize("m,L", [(7, 5), (40, 1), (3, 30)])
+def test_bucketed_closed_form_identical_A_reads(m, L):
+    d, o = _fs(["A" * L] * m)
+    got, _, _ = _bucketed(A, d, o, 3, 2)
+    assert got == b"A" * (m * L) + b"$" * m
+
+
+def test_bucketed_matches_oracle_on_reads():
+    d, o = synth.uniform(3000, 100, seed=5)
+    got, _, _ = _bucketed(A, d, o, 3, 50_000, threads=4)
+    assert got == oracle.bwt(A, d, o, threads=4)
