@@ -4,14 +4,17 @@
 One STEP = one whole pass of the hot path over one batch: clear the index and
 append the workload's reads (Algorithm 1 over all its blocks: pack, ConstructSA,
 B_int, ComputeRanks, g->g_sa gather, Insert + dictionary rebuild), inputs
-already resident in HBM.  Default workload = BASELINE configs[1] ("c2"):
-1M uniform reads x 100 bp, blocks of M = 2^24 suffixes (K = 7).
+already resident in HBM.  Default workload = BASELINE configs[2] ("c3"), the
+config BASELINE.json's metric ("at 1/2/4/8 B200") is quoted on: 20M uniform
+reads x 100 bp, blocks of M = 2^27 suffixes (K = 16).  configs[1] (c2) and the
+others are selected with --workload.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 (torchrun, one rank per GPU, NCCL): every rank builds the same index;
-ComputeRanks is split by string across ranks and g is all-gathered
- -> strong scaling of one build.  Prints ONE JSON line on rank 0.
+ComputeRanks is split by string across ranks and g is all-gathered by the
+library itself over NCCL (setbwte_set_comm) -> strong scaling
+of one build.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -55,6 +58,54 @@ STAGE_OF = {
     "compute_ranks": "rank", "slices": "rank", "gather": "gather", "insert": "insert",
     "sb_scan": "insert",
 }
+
+
+# algorithmic bytes of ConstructSA per suffix for uniform
+# reads (24 B per active suffix-pass x 1.044 passes + 4 B SA write, rounded)
+SORT_MODEL_B_PER_SUFFIX = 29.0
+
+
+def stage_fractions(kern: dict, stages: dict, peak_gbs: float, n_suf: int):
+    """Per stage (Table 2's taxonomy): algorithmic bytes / stage
+    time / HBM peak, with the times of the serialised warm-up step (every
+    stage on one stream, every launch timed).  Sort: SURVEY 8(d)'s model
+    bytes (29 B/suffix) and the library's own count (every 8-bit digit pass
+    and finish pass it ran); gather / insert / pack: the library's counts
+    (DESIGN.md section 7); rank: LF steps/s against the measured random
+    32-byte sector ceiling (profiles/r01_microbench.json) and HBM bytes."""
+    def kb(names):
+        return sum(v["bytes"] for k, v in kern.items() if k in names)
+    out = {"timing": "serialised warm-up step (stage_ms_per_step)"}
+    sort_names = [k for k in kern if k.startswith(("sort_", "digit_"))]
+    for st, names in (("sort", sort_names), ("gather", ["gather"]),
+                      ("insert", ["insert", "sb_scan"]), ("pack", ["pack", "slot_offsets"]),
+                      ("rank", ["compute_ranks"])):
+        ms = stages.get(st, 0.0)
+        if ms <= 0:
+            continue
+        b = kb(names)
+        e = {"ms": round(ms, 4), "bytes_lib": b,
+             "frac_lib": round(b / (ms / 1e3) / 1e9 / peak_gbs, 4)}
+        if st == "sort":
+            mb = SORT_MODEL_B_PER_SUFFIX * n_suf
+            e["bytes_model"] = mb
+            e["frac_model"] = round(mb / (ms / 1e3) / 1e9 / peak_gbs, 4)
+        if st == "rank":
+            mbp = os.path.join(ROOT, "profiles", "r01_microbench.json")
+            cr = kern.get("compute_ranks")
+            if cr and os.path.exists(mbp):
+                ceil = json.load(open(mbp)).get("gather32_hbm_gsectors_s")
+                if ceil:
+                    q = cr["units"] / (ms / 1e3)
+                    e["lf_steps_per_s"] = q
+                    e["frac_random_sector_ceiling"] = round(q / (ceil * 1e9), 4)
+        out[st] = e
+    return out
+
+
+def golden_digest(workload: str):
+    p = os.path.join(ROOT, "tests", "golden", "%s_bwt_digest.json" % workload)
+    return json.load(open(p)) if os.path.exists(p) else None
 
 
 def gen(workload: str, seed: int = 1):
@@ -229,8 +280,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             # N > 1: ComputeRanks split by string and block k sorted on rank
             # k mod N (its SA_int broadcast); Insert replicated (--option
             # insert_split=1 / shard_dict=2 select the split / sharded forms)
-            from paper_1410_0562_b200.dist import make_allgather
-            ix.set_partition(rank, world, make_allgather())
+            # the exchange runs inside the library on NCCL, on its stream
+            from paper_1410_0562_b200.dist import nccl_comm
+            ix.set_comm(nccl_comm(), rank, world)
             ix.set_option("sort_split", 1)
         for kv in args.option:
             k, v = kv.split("=", 1)
@@ -411,6 +463,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         stages[sname] = stages.get(sname, 0.0) + v["ms"]
     cr = warm_kern.get("compute_ranks")
     qps = (cr["units"] / (cr["ms"] / 1000.0)) if cr and cr["ms"] > 0 else None
+    stage_frac = stage_fractions(warm_kern, stages, peak, n_suf=bases + m)
 
     # ---- oracle beside it (rank 0, N = 1 only), + parity of this run ----
     cpu = None
@@ -429,6 +482,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "sample": "first %d reads (%d bases) of %s, one build" % (m_s, int(o_s[-1]), wl)}
         if m_s == m:
             parity = "bit-exact" if bytes(pin_out.numpy()[:n_total]) == want else "MISMATCH"
+    if rank == 0 and parity is None:
+        # full-size parity through the oracle-written digest (tests/golden,
+        # tools/make_golden_digests.py: bucketed oracle, BLAKE2b-128)
+        gd = golden_digest(wl)
+        if gd is not None and gd["n"] == n_total:
+            import hashlib
+            h = hashlib.blake2b(digest_size=16)
+            h.update(memoryview(pin_out.numpy()[:n_total]))
+            parity = ("bit-exact (BLAKE2b-128 of the whole BWT == oracle digest)"
+                      if h.hexdigest() == gd["digest"]["hex"] else "MISMATCH")
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
@@ -443,6 +506,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "blocks": blocks, "parallelism": "dp%d (ComputeRanks split by string)" % world,
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
             "compute_ranks_queries_per_s": qps, "stage_ms_per_step": stages,
+            "stage_frac": stage_frac,
             "profile_note": "stage/kernel ms and queries/s from the last warm-up step, run with "
                             "every stage on one stream and every launch timed (serialised, so they "
                             "add up to more than ms_per_step); roofline from the timed steps "
@@ -464,10 +528,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--block-suffixes", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-reads", type=int, default=1_000_000)

@@ -57,7 +57,8 @@ typedef enum {
     SETBWTE_E_NOMEM = 4,         /* device or pinned-host allocation failed */
     SETBWTE_E_CUDA = 5,          /* a CUDA runtime/kernel error (handle becomes sticky-failed) */
     SETBWTE_E_UNSUPPORTED = 6,   /* e.g. sigma > 4 on the 2-bit path, block too large */
-    SETBWTE_E_STATE = 7          /* handle previously failed, or call not valid now */
+    SETBWTE_E_STATE = 7,         /* handle previously failed, or call not valid now */
+    SETBWTE_E_NCCL = 8           /* setbwte_set_comm: NCCL not loadable, or an NCCL call failed */
 } setbwte_status;
 
 /* Create an empty index.  alphabet: NUL-terminated, 1..4 distinct bytes in
@@ -125,8 +126,11 @@ setbwte_status setbwte_clear(setbwte_t h);
 /* Current size: *n = sum(|S_j|+1) symbols of B, *m = number of strings. */
 setbwte_status setbwte_size(setbwte_t h, uint64_t* n, uint64_t* m);
 
-/* Write the BWT B[0..n) as ASCII ('$' for every terminator) into HOST buffer
- * out of capacity cap bytes.  out == NULL -> size query: *n set, OK.
+/* Write the BWT B[0..n) of the indexed string set -- Eq.(1) P:33-35,
+ * B[i] = T[(SA[i]-1) mod n] on T = S_0$_0...S_{m-1}$_{m-1} of P:36-37 -- as
+ * ASCII ('$' for every terminator, reading R5) into HOST buffer out of
+ * capacity cap bytes, decoded on the device from the B_ext rank dictionary
+ * (Sec.5).  out == NULL -> size query: *n set, OK.
  * cap < n -> SETBWTE_E_INVALID_ARG. */
 setbwte_status setbwte_bwt(setbwte_t h, uint8_t* out, uint64_t cap, uint64_t* n);
 
@@ -226,6 +230,9 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     of two random text lookups.  Results identical; measured
  *                     slower on c3 (the wider scatter costs more than the
  *                     lookups it saves), hence off by default.
+ *   "force_exchange"  1: (test hook) run the partitioned ComputeRanks and the
+ *                     exchange step even with world == 1 (one slice; with a
+ *                     communicator, one NCCL broadcast per exchange).
  *   "insert_split"    1: with setbwte_set_partition world > 1 and B_ext in HBM,
  *                     Insert is split by output range (rank r merges output
  *                     superblocks [nsb*r/P, nsb*(r+1)/P)) and the new
@@ -243,13 +250,16 @@ setbwte_status setbwte_set_profile(setbwte_t h, int mode, const char* kernel);
  * work instead of the private stream; NULL restores the private stream. */
 setbwte_status setbwte_set_stream(setbwte_t h, void* cuda_stream);
 
-/* Multi-process data parallelism over strings (Sec.8(e) of SURVEY.md):
- * ComputeRanks of every block runs only on this rank's contiguous slice of
- * the block's strings (balanced by suffix count), then `allgather` is called
- * to assemble the full g on every rank.  allgather(buf, bytes_per_rank, world,
- * stream, ctx): buf is a DEVICE buffer holding the concatenation of all
- * ranks' slices; this rank's slice is already filled; on return (work queued
- * on `stream` is allowed) every slice must be filled.  bytes_per_rank has
+/* Multi-process data parallelism over strings (Sec.8(e) of SURVEY.md), with
+ * the exchange done by a caller callback (setbwte_set_comm is the in-library
+ * NCCL form): ComputeRanks of every block runs only on this rank's contiguous
+ * slice of the block's strings (balanced by suffix count), then `allgather` is
+ * called to assemble the full g on every rank.  allgather(buf, bytes_per_rank,
+ * world, stream, ctx): buf is a DEVICE buffer holding the concatenation of all
+ * ranks' slices; this rank's slice is QUEUED on `stream` (not yet written when
+ * the callback runs), so the callback must order its work after `stream`'s;
+ * on return (work queued on `stream` is allowed) every slice must be filled,
+ * in stream order.  bytes_per_rank has
  * `world` entries.  world == 1 (the default) disables the exchange.  With
  * option "insert_split" the callback is also used, twice per block, for the
  * new B_ext dictionary (32-byte Blks) and its superblock totals (32 bytes per
@@ -258,6 +268,30 @@ typedef int (*setbwte_allgather_fn)(void* buf, const uint64_t* bytes_per_rank, i
                                     void* stream, void* ctx);
 setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,
                                      setbwte_allgather_fn allgather, void* ctx);
+
+/* In-library exchange over NCCL (the data-parallel split of
+ * P:225-228 "scattered ... insertion ... would require inter-node
+ * communication"): the same partition as setbwte_set_partition -- ComputeRanks
+ * of every block on this rank's suffix-balanced slice of the block's strings
+ * (Alg.2 P:110 "for all j" is independent per string) -- but every exchange
+ * (the all-gather-v of the g slices; with option "sort_split" the SA_int of
+ * the sorting rank; with "insert_split" / "shard_dict" the dictionary slices)
+ * is one NCCL group of `world` in-place ncclBroadcast calls issued by the
+ * library on its main stream, with no host synchronisation per block (the
+ * slices of all blocks are computed on the device and read back once per
+ * append).
+ *   nccl_comm : an ncclComm_t of exactly `world` ranks in which this process
+ *               is `rank` (e.g. torch's ProcessGroupNCCL._comm_ptr()), bound
+ *               to the handle's device.  Borrowed: it must outlive its use.
+ *               NULL detaches (back to world 1, or to a callback set before).
+ * NCCL is resolved at run time: the libnccl.so.2 already loaded in the
+ * process (the instance that created the communicator) is used, else the
+ * system's.  Errors: bad rank/world, or a communicator whose size/rank
+ * differ -> SETBWTE_E_INVALID_ARG; NCCL not loadable -> SETBWTE_E_NCCL (also
+ * returned by an append whose NCCL call fails); a sharded dictionary and a
+ * different world -> SETBWTE_E_UNSUPPORTED.  Replaces a callback set by
+ * setbwte_set_partition (and vice versa). */
+setbwte_status setbwte_set_comm(setbwte_t h, void* nccl_comm, int rank, int world);
 
 /* Route the handle's DEVICE scratch and dictionary allocations through a
  * caller allocator (e.g. the PyTorch caching allocator).

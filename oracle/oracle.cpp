@@ -186,7 +186,9 @@ int oracle_bwt(const char* alphabet, const uint8_t* bytes, const uint64_t* off, 
  *
  * Output: `emit(chunk, len, bucket_key, ctx)` is called once per non-empty
  * bucket, in order; the concatenation of the chunks is oracle_bwt's output.
- * Memory: the codes of the text plus batch_cap * 9 bytes. */
+ * Memory: the codes of the text plus batch_cap * 9 bytes.  The buckets of a
+ * batch are sorted in parallel (a library sort each); their order is fixed by
+ * the keys, so the schedule does not change the output. */
 typedef void (*oracle_emit_fn)(const uint8_t* chunk, uint64_t len, uint64_t bucket, void* ctx);
 
 int oracle_bwt_bucketed(const char* alphabet, const uint8_t* bytes, const uint64_t* off,
@@ -250,18 +252,34 @@ int oracle_bwt_bucketed(const char* alphabet, const uint8_t* bytes, const uint64
             }
         }
         out.resize(size);
+        /* sort every bucket of the batch with the library sort: the buckets
+         * in parallel (one thread each), a bucket holding more than a quarter
+         * of the batch with the parallel library sort */
+        auto cmp = [&t](const Suf& a, const Suf& b) { return suf_less(t, a, b); };
+        std::vector<uint64_t> big;
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
+        for (int64_t b = (int64_t)b0; b < (int64_t)b1; ++b) {
+            const uint64_t s0 = start[b - b0], s1 = start[b - b0 + 1];
+            if (s1 - s0 > size / 4 && threads > 1) {
+#pragma omp critical
+                big.push_back((uint64_t)b);
+                continue;
+            }
+            std::sort(v.begin() + s0, v.begin() + s1, cmp);
+        }
+        for (uint64_t b : big) {
+            omp_set_num_threads(threads);
+            __gnu_parallel::sort(v.begin() + start[b - b0], v.begin() + start[b - b0 + 1], cmp);
+        }
+        /* B[i] = T[(SA[i]-1) mod n], Eq.(1): S_j[k-1] if k > 0, else '$' */
+#pragma omp parallel for num_threads(threads) schedule(static)
+        for (int64_t i = 0; i < (int64_t)size; ++i) {
+            const Suf& s = v[i];
+            out[i] = s.k > 0 ? (uint8_t)alphabet[t.code[off[s.j] + s.k - 1] - 1] : (uint8_t)'$';
+        }
         for (uint64_t b = b0; b < b1; ++b) {
             const uint64_t s0 = start[b - b0], s1 = start[b - b0 + 1];
-            if (s0 == s1) continue;
-            std::vector<Suf> bucket(v.begin() + s0, v.begin() + s1);
-            sort_sufs(t, bucket, threads);
-            /* B[i] = T[(SA[i]-1) mod n], Eq.(1): S_j[k-1] if k > 0, else '$' */
-            for (uint64_t i = 0; i < bucket.size(); ++i) {
-                const Suf& s = bucket[i];
-                out[s0 + i] = s.k > 0 ? (uint8_t)alphabet[t.code[off[s.j] + s.k - 1] - 1]
-                                      : (uint8_t)'$';
-            }
-            emit(out.data() + s0, s1 - s0, b, ctx);
+            if (s0 != s1) emit(out.data() + s0, s1 - s0, b, ctx);
         }
         b0 = b1;
     }

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("SETBWTE_LIB") or os.path.join(_PKG, "libsetbwte.so")
 
 STATUS = {
     0: "OK", 1: "E_INVALID_ARG", 2: "E_INVALID_CHAR", 3: "E_OUT_OF_RANGE", 4: "E_NOMEM",
-    5: "E_CUDA", 6: "E_UNSUPPORTED", 7: "E_STATE",
+    5: "E_CUDA", 6: "E_UNSUPPORTED", 7: "E_STATE", 8: "E_NCCL",
 }
 
 _u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -37,7 +37,7 @@ EXPORTS = [
     "setbwte_rank", "setbwte_rank_batch", "setbwte_count", "setbwte_count_device",
     "setbwte_construct_sa", "setbwte_compute_ranks",
     "setbwte_set_option", "setbwte_set_profile", "setbwte_set_stream", "setbwte_set_partition",
-    "setbwte_set_allocator", "setbwte_stats",
+    "setbwte_set_comm", "setbwte_set_allocator", "setbwte_stats",
     "setbwte_last_error",
 ]
 
@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         "setbwte_set_profile": ([vp, ctypes.c_int, ctypes.c_char_p], ctypes.c_int),
         "setbwte_set_partition": ([vp, ctypes.c_int, ctypes.c_int, ALLGATHER_FN, vp],
                                   ctypes.c_int),
+        "setbwte_set_comm": ([vp, vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "setbwte_set_allocator": ([vp, ALLOC_FN, FREE_FN, vp], ctypes.c_int),
         "setbwte_stats": ([vp, ctypes.c_char_p, c64, _u64p], ctypes.c_int),
         "setbwte_last_error": ([vp, _u64p, _u8p], ctypes.c_int),
@@ -190,6 +191,13 @@ class SetBWTE:
         self._allgather_ref = cb
         self._check(self._lib.setbwte_set_partition(self._h, rank, world, cb, None),
                     "set_partition")
+
+    def set_comm(self, nccl_comm: int, rank: int, world: int):
+        """In-library NCCL exchange (setbwte_set_comm): nccl_comm is an
+        ncclComm_t address (paper_1410_0562_b200.dist.nccl_comm(group)); 0
+        detaches."""
+        self._check(self._lib.setbwte_set_comm(self._h, ctypes.c_void_p(int(nccl_comm) or None),
+                                               int(rank), int(world)), "set_comm")
 
     def set_allocator(self, alloc=None, free=None):
         """Route the handle's device allocations through alloc(nbytes) -> int

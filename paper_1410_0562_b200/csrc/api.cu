@@ -14,6 +14,9 @@
 #include <thread>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "internal.h"
 #include "setbwte.h"
 
@@ -54,6 +57,11 @@ cudaError_t ensure_bytes(DevBuf& b, size_t bytes) {
         if (!b.p) return cudaErrorMemoryAllocation;
         b.fr = al->free_;
         b.fctx = al->ctx;
+        // a caching allocator may return a block whose previous owner still
+        // has work queued on the allocator's stream, which our streams do not
+        // wait for: drain before the library writes it
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return e;
     } else {
         cudaError_t e = cudaMalloc(&b.p, cap);
         if (e != cudaSuccess) {
@@ -166,6 +174,43 @@ Profiler::~Profiler() {
 }  // namespace setbwte
 
 // ---------------------------------------------------------------------------
+// NCCL, resolved at run time (setbwte_set_comm).  A communicator must be used
+// with the NCCL instance that created it: libnccl.so.2 already loaded into
+// the process (e.g. by PyTorch) is taken first (RTLD_NOLOAD), else the
+// system's.  The library therefore has no link-time NCCL dependency.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    bool ok = false;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclCommCount) comm_count = nullptr;
+    decltype(&ncclCommUserRank) comm_user_rank = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) return a;
+        a.group_start = (decltype(a.group_start))dlsym(lib, "ncclGroupStart");
+        a.group_end = (decltype(a.group_end))dlsym(lib, "ncclGroupEnd");
+        a.broadcast = (decltype(a.broadcast))dlsym(lib, "ncclBroadcast");
+        a.comm_count = (decltype(a.comm_count))dlsym(lib, "ncclCommCount");
+        a.comm_user_rank = (decltype(a.comm_user_rank))dlsym(lib, "ncclCommUserRank");
+        a.error_string = (decltype(a.error_string))dlsym(lib, "ncclGetErrorString");
+        a.ok = a.group_start && a.group_end && a.broadcast && a.comm_count && a.comm_user_rank;
+        return a;
+    }();
+    return api;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // Handle
 // ---------------------------------------------------------------------------
 struct DevErr {
@@ -190,7 +235,7 @@ struct setbwte_s {
     bool failed = false;
 
     // alphabet
-    char alpha[5] = {0};
+    char alpha[6] = {0};
     int sigma = 0;
     uint8_t code_of[256];
     DevBuf d_code_of, d_sym;
@@ -198,11 +243,12 @@ struct setbwte_s {
     // the index: B_ext as a rank dictionary, ping-pong (reading: Sec.5)
     uint64_t n = 0, m = 0;
     DevBuf blk[2], sb[2];
+    DevBuf nblk[2], nsb[2], ntot;  // sigma = 5: the N plane (common.cuh NBlk), ping-pong
     int cur = 0;
     DevBuf d_C, sb_tot;
 
     // append scratch
-    DevBuf in_bytes, in_off, text, term, slot_off, gfirst, bounds, err, small;
+    DevBuf in_bytes, in_off, text, term, nbit, slot_off, gfirst, bounds, err, small;
     DevBuf saf, g, pos, bint, outbuf, bslot;
     SortScratch sort[kMaxLanes];  // sort[0] also serves the inline (sort_lanes = 0) path
     Allocator user_alloc;         // setbwte_set_allocator (empty: cudaMalloc)
@@ -228,6 +274,9 @@ struct setbwte_s {
     // reverse orientation: the strings of the running call go BEFORE
     // every string already indexed, so a new terminator is the smallest suffix
     bool prepending = false;
+    // the running append started on an empty index: a failure after its first
+    // Insert empties the index again instead of failing the handle
+    bool started_empty = false;
 
     // data-parallel ComputeRanks (and, with insert_split, Insert by output range)
     int rank = 0, world = 1;
@@ -248,6 +297,12 @@ struct setbwte_s {
     int g_width = 0;                         // option "g_width": 0 auto, 8 = always u64
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
+    ncclComm_t nccl = nullptr;       // setbwte_set_comm: exchanges run in-library on NCCL
+    bool force_exchange = false;     // option "force_exchange" (test hook: exchange at world 1)
+    // per block of the running append, this rank partition's string / slot
+    // boundaries for ComputeRanks: (world+1) string indices then (world+1)
+    // slot offsets (computed on the device, read back once per append)
+    std::vector<uint64_t> blk_slices;
 
     // diagnostics
     uint64_t err_pos = 0;
@@ -306,6 +361,7 @@ setbwte_status pack_input(setbwte_t h, const uint8_t* d_bytes, const uint64_t* d
     pk.n_slots = n_slots;
     API_CHECK(h, ensure(h->text, 2 * n_groups + 8, &pk.text));
     API_CHECK(h, ensure(h->term, n_groups + 8, &pk.term));
+    if (h->sigma == 5) API_CHECK(h, ensure(h->nbit, n_groups + 8, &pk.nbit));
     API_CHECK(h, ensure(h->slot_off, m + 2, &pk.slot_off));
     API_CHECK(h, ensure(h->gfirst, n_groups + 2, &pk.gfirst));
     DevErr* derr;
@@ -336,52 +392,103 @@ inline const Blk* cur_blk(setbwte_t h) {
     return h->host_tier ? h->hdict_dev : (const Blk*)h->blk[h->cur].p;
 }
 inline const uint64_t* cur_sb(setbwte_t h) { return (const uint64_t*)h->sb[h->cur].p; }
+// sigma = 5: the N plane of the current B_ext (and the text's code-4 plane)
+inline N5Dict cur_n5(setbwte_t h, const uint32_t* nbit = nullptr) {
+    N5Dict d;
+    d.nbit = nbit;
+    d.nblk = (const NBlk*)h->nblk[h->cur].p;
+    d.nsb = (const uint64_t*)h->nsb[h->cur].p;
+    return d;
+}
 // The current B_ext Blks as a (possibly sharded) Dict.
 inline Dict cur_dict(setbwte_t h) { return h->sharded ? h->shard_dict : make_dict(cur_blk(h)); }
 
+// True when the running appends split ComputeRanks across ranks.
+inline bool partitioned(setbwte_t h) { return h->world > 1 || h->force_exchange; }
+
+// The one exchange step of the data-parallel path: an
+// all-gather-v in place.  buf is a DEVICE buffer holding the concatenation of
+// every rank's slice (bytes_per_rank[r] bytes for rank r, in rank order);
+// this rank's slice is queued on the main stream; afterwards (in stream order)
+// every slice is filled.  With a communicator (setbwte_set_comm) it is one
+// NCCL group of `world` in-place broadcasts (root r sends slice r) on the main
+// stream -- no host synchronisation; else the setbwte_set_partition callback.
+setbwte_status exchange(setbwte_t h, void* buf, const uint64_t* bytes_per_rank) {
+    if (h->nccl) {
+        const NcclApi& nc = nccl_api();
+        if (!nc.ok) return SETBWTE_E_NCCL;
+        ncclResult_t r = nc.group_start();
+        uint64_t off = 0;
+        for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
+            if (bytes_per_rank[q]) {
+                char* p = static_cast<char*>(buf) + off;
+                r = nc.broadcast(p, p, bytes_per_rank[q], ncclUint8, q, h->nccl, h->stream);
+            }
+            off += bytes_per_rank[q];
+        }
+        const ncclResult_t r2 = nc.group_end();
+        if (r != ncclSuccess || r2 != ncclSuccess) {
+            if (getenv("SETBWTE_DEBUG") && nc.error_string)
+                fprintf(stderr, "setbwte: NCCL %s\n", nc.error_string(r != ncclSuccess ? r : r2));
+            return SETBWTE_E_NCCL;
+        }
+        return SETBWTE_OK;
+    }
+    if (h->world <= 1) return SETBWTE_OK;  // force_exchange without a communicator: nothing to do
+    if (!h->allgather) return SETBWTE_E_STATE;
+    if (h->allgather(buf, bytes_per_rank, h->world, (void*)h->stream, h->allgather_ctx) != 0)
+        return SETBWTE_E_STATE;
+    return SETBWTE_OK;
+}
+
 // ComputeRanks for strings [j0, j1) of a packed append, into g (block-local
 // slots starting at slot_base).  With world > 1, only this rank's slice is
-// computed and the slices are exchanged by the allgather callback.
+// computed and the slices are exchanged (exchange()).  `slices` (optional):
+// the block's precomputed partition, (world+1) string indices then (world+1)
+// slot offsets; without it the partition is computed and read back here.
 setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, uint64_t n_suf, void* g, int gw,
-                                 uint8_t* bslot = nullptr, bool bing = false) {
+                                 uint8_t* bslot = nullptr, bool bing = false,
+                                 const uint64_t* slices = nullptr) {
     if (h->n == 0) {
         // empty B_ext: every suffix has rank 0
         API_CHECK(h, cudaMemsetAsync(g, 0, n_suf * gw, h->stream));
         return SETBWTE_OK;
     }
-    if (h->world <= 1) {
+    const N5Dict n5 = cur_n5(h, pk.nbit);
+    const N5Dict* n5p = h->sigma == 5 ? &n5 : nullptr;
+    if (!partitioned(h)) {
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_dict(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
-                                          n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot, bing));
+                                          n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot, bing, n5p));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
-    uint64_t* d_sl;
-    API_CHECK(h, ensure(h->small, 2 * (size_t)h->world + 8, &d_sl));
-    API_CHECK(h, launch_slices(h->prof, h->stream, pk.slot_off, j0, j1, h->world, d_sl));
-    std::vector<uint64_t> sl(h->world + 1);
-    API_CHECK(h, cudaMemcpyAsync(sl.data(), d_sl, sizeof(uint64_t) * (h->world + 1),
-                                 cudaMemcpyDeviceToHost, h->stream));
-    API_CHECK(h, cudaStreamSynchronize(h->stream));
-    std::vector<uint64_t> slot_of(h->world + 1);
-    for (int r = 0; r <= h->world; ++r) {
-        API_CHECK(h, cudaMemcpyAsync(&slot_of[r], pk.slot_off + sl[r], sizeof(uint64_t),
+    const int P = h->world;
+    std::vector<uint64_t> own;
+    if (!slices) {
+        // one-off call (setbwte_compute_ranks): partition and read back here
+        uint64_t* d_sl;
+        API_CHECK(h, ensure(h->small, 2 * (size_t)P + 8, &d_sl));
+        API_CHECK(h, launch_slices(h->prof, h->stream, pk.slot_off, j0, j1, P, d_sl));
+        own.resize(2 * (P + 1));
+        API_CHECK(h, cudaMemcpyAsync(own.data(), d_sl, sizeof(uint64_t) * 2 * (P + 1),
                                      cudaMemcpyDeviceToHost, h->stream));
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+        slices = own.data();
     }
-    API_CHECK(h, cudaStreamSynchronize(h->stream));
+    const uint64_t* sl = slices;               // string boundaries
+    const uint64_t* slot_of = slices + P + 1;  // their slot offsets
     const uint64_t a = sl[h->rank], b = sl[h->rank + 1];
     const uint64_t steps = (slot_of[h->rank + 1] - slot_of[h->rank]) - (b - a);
     API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
                                       cur_dict(h), cur_sb(h), (const uint64_t*)h->d_C.p,
-                                      h->prepending ? 0 : h->m, steps, g, gw, h->rank_ilp));
-    std::vector<uint64_t> bytes(h->world);
-    for (int r = 0; r < h->world; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
-    if (!h->allgather) return SETBWTE_E_STATE;
-    int rc = h->allgather(g, bytes.data(), h->world, (void*)h->stream, h->allgather_ctx);
-    if (rc != 0) return SETBWTE_E_STATE;
-    return SETBWTE_OK;
+                                      h->prepending ? 0 : h->m, steps, g, gw, h->rank_ilp, nullptr,
+                                      false, n5p));
+    std::vector<uint64_t> bytes(P);
+    for (int r = 0; r < P; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
+    return exchange(h, g, bytes.data());
 }
 
 // Algorithm 1 for one block of strings [j0, j1) occupying slots
@@ -392,6 +499,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
 struct BlockDesc {
     uint64_t j0, j1, S0, S1;
     uint64_t ev;  // index of the ev_packed event after which its slots are packed
+    uint64_t id;  // block index in the append (h->blk_slices)
 };
 
 // Pinned mapped host buffer for the dictionary with >= nblk Blks, keeping
@@ -475,6 +583,15 @@ setbwte_status insert_prepare(setbwte_t h, uint64_t n_ins, InsertBufs* ib) {
     const uint64_t nblk = (n_out >> 6) + 1;
     ib->nsb = (n_out >> kSbShift) + 1;
     const int nxt = 1 - h->cur;
+    if (h->sigma == 5) {
+        // the N plane: ping-pong like the Blks, per-superblock totals as scratch
+        if (nblk * sizeof(Blk) > h->hbm_budget) return SETBWTE_E_UNSUPPORTED;  // no host tier
+        NBlk* nb;
+        uint64_t* ns;
+        API_CHECK(h, ensure(h->nblk[nxt], nblk, &nb));
+        API_CHECK(h, ensure(h->nsb[nxt], ib->nsb + 8, &ns));
+        API_CHECK(h, ensure(h->ntot, ib->nsb + 8, &ns));
+    }
     if (!h->host_tier && !h->sharded && nblk * sizeof(Blk) > h->hbm_budget) {
         // the dictionary outgrows its HBM budget: move B_ext to the host tier
         // (after this block's ComputeRanks, which still reads the HBM copy)
@@ -547,9 +664,9 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
         API_CHECK(h, cudaMemcpyAsync(d_ent + h->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice,
                                      h->stream));
         std::vector<uint64_t> ent_bytes(P, sizeof(ShardEntry));
-        if (h->allgather(ib.tot, tot_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx) ||
-            h->allgather(d_ent, ent_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
-            return SETBWTE_E_STATE;
+        setbwte_status xs = exchange(h, ib.tot, tot_bytes.data());
+        if (xs == SETBWTE_OK) xs = exchange(h, d_ent, ent_bytes.data());
+        if (xs != SETBWTE_OK) return xs;
         API_CHECK(h, launch_sb_scan(h->prof, h->stream, ib.tot, ib.nsb, ib.osb, m_new,
                                     (uint64_t*)h->d_C.p));
         std::vector<ShardEntry> all(P);
@@ -579,7 +696,7 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
         }
         h->shard_dict = d;
         h->shard_cur = 1 - h->shard_cur;
-    } else if (h->world > 1 && h->insert_split && h->allgather) {
+    } else if (partitioned(h) && h->insert_split && (h->allgather || h->nccl) && h->sigma != 5) {
         // Insert split by output range: rank r merges output
         // superblocks [nsb*r/P, nsb*(r+1)/P) only; the new dictionary's Blks and
         // the superblock totals are then all-gathered (slices in rank order),
@@ -597,14 +714,23 @@ setbwte_status insert_finish(setbwte_t h, const InsertBufs& ib, const void* pos,
         const uint64_t a = ib.nsb * h->rank / P, b = ib.nsb * (h->rank + 1) / P;
         API_CHECK(h, launch_insert_range(h->prof, h->stream, cur_dict(h), h->n, pos, gw, bint, n_ins,
                                          ib.ob, ib.tot, ib.sb_start, a, b));
-        if (h->allgather(ib.ob, blk_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx) ||
-            h->allgather(ib.tot, tot_bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
-            return SETBWTE_E_STATE;
+        setbwte_status xs = exchange(h, ib.ob, blk_bytes.data());
+        if (xs == SETBWTE_OK) xs = exchange(h, ib.tot, tot_bytes.data());
+        if (xs != SETBWTE_OK) return xs;
         API_CHECK(h, launch_sb_scan(h->prof, h->stream, ib.tot, ib.nsb, ib.osb, m_new,
                                     (uint64_t*)h->d_C.p));
     } else {
+        N5Ins n5;
+        if (h->sigma == 5) {
+            const int nxt = 1 - h->cur;
+            n5.in = (const NBlk*)h->nblk[h->cur].p;
+            n5.out = (NBlk*)h->nblk[nxt].p;
+            n5.ntot = (uint64_t*)h->ntot.p;
+            n5.nsb_out = (uint64_t*)h->nsb[nxt].p;
+        }
         API_CHECK(h, launch_insert(h->prof, h->stream, cur_dict(h), h->n, pos, gw, bint, n_ins, ib.ob,
-                                   ib.osb, ib.tot, ib.sb_start, m_new, (uint64_t*)h->d_C.p));
+                                   ib.osb, ib.tot, ib.sb_start, m_new, (uint64_t*)h->d_C.p,
+                                   h->sigma == 5 ? &n5 : nullptr));
     }
     h->cur = 1 - h->cur;
     h->n += n_ins;
@@ -626,12 +752,15 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // (with u64 g, B_int goes into g's top byte instead: bing)
     uint8_t* bslot = nullptr;
     bool bing = false;
-    if (!sa_payload(n_suf, h->sopt.payload_limit) && h->n != 0 && h->world <= 1) {
+    if (!sa_payload(n_suf, h->sopt.payload_limit) && h->n != 0 && !partitioned(h)) {
         if (gw == 8) bing = true;
         else API_CHECK(h, ensure(h->bslot, n_suf + 8, &bslot));
     }
     // g := ComputeRanks(S_jk, B_ext)
-    setbwte_status st = compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw, bslot, bing);
+    const uint64_t* slices =
+        partitioned(h) ? h->blk_slices.data() + b.id * 2 * (uint64_t)(h->world + 1) : nullptr;
+    setbwte_status st =
+        compute_ranks_for(h, pk, b.j0, b.j1, b.S0, n_suf, g, gw, bslot, bing, slices);
     if (st != SETBWTE_OK) return st;
     InsertBufs ib;
     st = insert_prepare(h, n_suf, &ib);
@@ -640,7 +769,7 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     // slices of pos, fused
     API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
                                (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb, bslot,
-                               h->sopt.payload_limit, bing));
+                               h->sopt.payload_limit, bing, pk.nbit));
     return insert_finish(h, ib, pos, gw, bint, n_suf, b.j1 - b.j0);
 }
 
@@ -686,15 +815,12 @@ setbwte_status merge_impl(setbwte_t h, setbwte_t o) {
 // only; its SA_int reaches every rank through the allgather callback (a
 // one-contributor all-gather = a broadcast), queued on the main stream.
 setbwte_status share_sa(setbwte_t h, const BlockDesc& b, size_t k, uint32_t* saf) {
-    if (!h->sort_split || h->world <= 1) return SETBWTE_OK;
-    if (!h->allgather) return SETBWTE_E_STATE;
+    if (!h->sort_split || !partitioned(h)) return SETBWTE_OK;
     std::vector<uint64_t> bytes(h->world, 0);
     bytes[k % (size_t)h->world] = 4 * (b.S1 - b.S0);
     // the slices are laid out in rank order: the owner's starts at offset 0
     // only if every earlier rank contributes 0 bytes, which holds here
-    if (h->allgather(saf, bytes.data(), h->world, (void*)h->stream, h->allgather_ctx))
-        return SETBWTE_E_STATE;
-    return SETBWTE_OK;
+    return exchange(h, saf, bytes.data());
 }
 
 // Run Algorithm 1 over all blocks with the two-stage pipeline.
@@ -711,6 +837,27 @@ struct SortLane {
     uint32_t* saf = nullptr;
     cudaEvent_t ev_sorted = nullptr;
 };
+
+// An append failed after some of its blocks were inserted.  On an index the
+// append started empty there is nothing to roll back to but the empty index:
+// reset it (unless a sticky CUDA error already failed the handle); otherwise
+// the handle is failed.  Either way the recorded sort launch pattern is
+// dropped (it may come from the failed call's blocks).
+void fail_partial(setbwte_t h) {
+    h->sort_pattern.drop();
+    if (h->started_empty && !h->failed) {
+        if (cudaStreamSynchronize(h->stream) == cudaSuccess &&
+            cudaMemsetAsync(h->d_C.p, 0, 8 * sizeof(uint64_t), h->stream) == cudaSuccess &&
+            cudaStreamSynchronize(h->stream) == cudaSuccess) {
+            h->n = 0;
+            h->m = 0;
+            h->cur = 0;
+            return;
+        }
+        cudaGetLastError();
+    }
+    h->failed = true;
+}
 
 // validate(): called on the main thread before the first Insert (the index is
 // untouched until then); a non-OK status aborts the append.
@@ -774,11 +921,11 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
             if (!h->sort_split || (int)(k % (size_t)h->world) == h->rank)
                 API_CHECK(h, sort_block(h->prof, h->stream, h->sort[0], pk.text, pk.term,
                                         blocks[k].S0, (uint32_t)(blocks[k].S1 - blocks[k].S0),
-                                        saf2, &h->sstats, false, h->sopt));
+                                        saf2, &h->sstats, false, h->sopt, pk.nbit));
             setbwte_status st1 = share_sa(h, blocks[k], k, saf2);
             if (st1 == SETBWTE_OK) st1 = rank_insert_stage(h, pk, blocks[k], saf2);
             if (st1 != SETBWTE_OK) {
-                if (k > 0) h->failed = true;
+                if (k > 0) fail_partial(h);
                 return st1;
             }
         }
@@ -814,7 +961,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
             if (mine)
                 e = sort_block(L.prof, L.stream, *L.ws, pk.text, pk.term, blocks[k].S0,
                                (uint32_t)(blocks[k].S1 - blocks[k].S0), L.saf, &L.st, false,
-                               h->sopt);
+                               h->sopt, pk.nbit);
             if (e == cudaSuccess) e = cudaEventRecord(L.ev_sorted, L.stream);
             std::lock_guard<std::mutex> lk(mu);
             if (e != cudaSuccess) {
@@ -860,7 +1007,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         }
         std::lock_guard<std::mutex> lk(mu);
         if (st != SETBWTE_OK) {
-            if (k > 0) h->failed = true;  // a partially applied append cannot be rolled back
+            if (k > 0) fail_partial(h);  // a partially applied append cannot be rolled back
             abort = true;
             cv.notify_all();
             break;
@@ -873,8 +1020,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         for (std::thread& t : threads) t.join();
     }
     if (st == SETBWTE_OK && lane_err != cudaSuccess) {
-        if (h->n != 0) h->failed = true;
         st = from_cuda(h, lane_err);
+        if (h->n != 0) fail_partial(h);
     }
     // the main stream joins the sort lanes; their statistics merge into the handle's
     for (int l = 0; l < NL; ++l) {
@@ -966,6 +1113,7 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     pk.n_slots = n_slots;
     API_CHECK(h, ensure(h->text, 2 * n_groups + 8, &pk.text));
     API_CHECK(h, ensure(h->term, n_groups + 8, &pk.term));
+    if (h->sigma == 5) API_CHECK(h, ensure(h->nbit, n_groups + 8, &pk.nbit));
     API_CHECK(h, ensure(h->slot_off, m + 2, &pk.slot_off));
     API_CHECK(h, ensure(h->gfirst, n_groups + 2, &pk.gfirst));
     DevErr* derr;
@@ -1033,7 +1181,21 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     std::vector<BlockDesc> blocks(K);
     for (uint64_t b = 0; b < K; ++b)
         blocks[b] = BlockDesc{bounds[2 * b], bounds[2 * b + 2], bounds[2 * b + 1], bounds[2 * b + 3],
-                              std::min(b + 1, K - 1)};
+                              std::min(b + 1, K - 1), b};
+    if (partitioned(h)) {
+        // every block's ComputeRanks partition across the ranks, computed on
+        // the device and read back once here: the per-block exchange then
+        // needs no host synchronisation
+        const uint64_t per = 2 * (uint64_t)(h->world + 1);
+        uint64_t* d_sl;
+        API_CHECK(h, ensure(h->small, K * per + 8, &d_sl));
+        API_CHECK(h, launch_slices_blocks(h->prof, h->stream, pk.slot_off, d_bounds, K, h->world,
+                                          d_sl));
+        h->blk_slices.resize(K * per);
+        API_CHECK(h, cudaMemcpyAsync(h->blk_slices.data(), d_sl, K * per * sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, h->stream));
+        API_CHECK(h, cudaStreamSynchronize(h->stream));
+    }
     // packing, block by block on the pack ("copy") stream, each after its chunks
     while (h->ev_packed.size() < K) {
         cudaEvent_t ev;
@@ -1086,14 +1248,17 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     // the last chunk arrives ~2 ms into a c2 call).  A bad byte found at the
     // end empties the index again.
     const bool defer = h->n == 0 && !h->sharded && !h->host_tier;  // plain HBM index only
+    h->started_empty = defer;
     setbwte_status st = run_blocks(h, pk, order,
                                    defer ? std::function<setbwte_status()>(
                                                []() { return SETBWTE_OK; })
                                          : std::function<setbwte_status()>(validate));
     h->prepending = false;
+    h->started_empty = false;
     if (defer && st == SETBWTE_OK) {
         st = validate();
         if (st == SETBWTE_E_INVALID_CHAR) {
+            h->sort_pattern.drop();
             API_CHECK(h, cudaStreamSynchronize(h->stream));
             h->n = 0;
             h->m = 0;
@@ -1131,6 +1296,7 @@ const char* setbwte_strerror(setbwte_status s) {
         case SETBWTE_E_CUDA: return "CUDA error";
         case SETBWTE_E_UNSUPPORTED: return "unsupported";
         case SETBWTE_E_STATE: return "handle in failed state";
+        case SETBWTE_E_NCCL: return "NCCL unavailable or an NCCL call failed";
     }
     return "unknown status";
 }
@@ -1142,7 +1308,8 @@ static std::vector<DevBuf*> pooled_bufs(setbwte_t h) {
                               &h->sb[1], &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text,
                               &h->term, &h->gfirst, &h->slot_off, &h->bounds, &h->err, &h->small,
                               &h->saf, &h->g, &h->pos, &h->bslot, &h->bint, &h->outbuf,
-                              &h->shard_ptrs, &h->stage_in, &h->stage_out};
+                              &h->shard_ptrs, &h->stage_in, &h->stage_out, &h->nbit,
+                              &h->nblk[0], &h->nblk[1], &h->nsb[0], &h->nsb[1], &h->ntot};
     for (SortScratch& ws : h->sort)
         for (DevBuf* b : ws.bufs()) v.push_back(b);
     return v;
@@ -1153,7 +1320,7 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     *out = nullptr;
     const size_t sigma = strlen(alphabet);
     if (sigma < 1) return SETBWTE_E_INVALID_ARG;
-    if (sigma > 4) return SETBWTE_E_UNSUPPORTED;
+    if (sigma > 5) return SETBWTE_E_UNSUPPORTED;
     setbwte_t h = new (std::nothrow) setbwte_s();
     if (!h) return SETBWTE_E_NOMEM;
     memset(h->code_of, 0xFF, sizeof(h->code_of));
@@ -1194,12 +1361,12 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
     uint8_t* ds = nullptr;
     uint64_t* dC = nullptr;
     if (e == cudaSuccess) e = ensure(h->d_code_of, 256, &dc);
-    if (e == cudaSuccess) e = ensure(h->d_sym, 4, &ds);
+    if (e == cudaSuccess) e = ensure(h->d_sym, 8, &ds);
     if (e == cudaSuccess) e = ensure(h->d_C, 8, &dC);
-    uint8_t sym[4] = {0, 0, 0, 0};
+    uint8_t sym[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (size_t i = 0; i < sigma; ++i) sym[i] = (uint8_t)alphabet[i];
     if (e == cudaSuccess) e = cudaMemcpy(dc, h->code_of, 256, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(ds, sym, 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(ds, sym, 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(dC, 0, 8 * sizeof(uint64_t));
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -1308,7 +1475,7 @@ setbwte_status setbwte_merge(setbwte_t h, setbwte_t other) {
     if (!other || other == h) return SETBWTE_E_INVALID_ARG;
     if (other->failed) return SETBWTE_E_STATE;
     if (other->device != h->device || strcmp(other->alpha, h->alpha) != 0 || h->sharded ||
-        other->sharded)
+        other->sharded || h->sigma == 5)
         return SETBWTE_E_UNSUPPORTED;
     return merge_impl(h, other);
 }
@@ -1341,7 +1508,7 @@ static setbwte_status bwt_impl(setbwte_t h, uint8_t* out, uint64_t cap, uint64_t
     uint8_t* target = out;
     if (!dev) API_CHECK(h, ensure(h->outbuf, h->n, &target));
     API_CHECK(h, launch_decode(h->prof, h->stream, cur_dict(h), h->n, (const uint8_t*)h->d_sym.p,
-                               target));
+                               target, h->sigma == 5 ? (const NBlk*)h->nblk[h->cur].p : nullptr));
     if (!dev)
         API_CHECK(h, cudaMemcpyAsync(out, target, h->n, cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
@@ -1370,8 +1537,10 @@ setbwte_status setbwte_rank(setbwte_t h, uint8_t c, uint64_t k, uint64_t* out) {
     uint8_t* dc = reinterpret_cast<uint8_t*>(d + 2);
     API_CHECK(h, cudaMemcpyAsync(d, &k, 8, cudaMemcpyHostToDevice, h->stream));
     API_CHECK(h, cudaMemcpyAsync(dc, &c, 1, cudaMemcpyHostToDevice, h->stream));
+    const N5Dict n5 = cur_n5(h);
     API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_dict(h), cur_sb(h), h->n,
-                                   (const uint8_t*)h->d_code_of.p, dc, d, 1, d + 1));
+                                   (const uint8_t*)h->d_code_of.p, dc, d, 1, d + 1,
+                                   h->sigma == 5 ? &n5 : nullptr));
     uint64_t r = 0;
     API_CHECK(h, cudaMemcpyAsync(&r, d + 1, 8, cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
@@ -1399,8 +1568,10 @@ setbwte_status setbwte_rank_batch(setbwte_t h, const uint8_t* c_dev, const uint6
         API_CHECK(h, cudaMemcpy(out_dev, r.data(), q * 8, cudaMemcpyHostToDevice));
         return SETBWTE_OK;
     }
+    const N5Dict n5 = cur_n5(h);
     API_CHECK(h, launch_rank_batch(h->prof, h->stream, cur_dict(h), cur_sb(h), h->n,
-                                   (const uint8_t*)h->d_code_of.p, c_dev, k_dev, q, out_dev));
+                                   (const uint8_t*)h->d_code_of.p, c_dev, k_dev, q, out_dev,
+                                   h->sigma == 5 ? &n5 : nullptr));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
     return SETBWTE_OK;
 }
@@ -1411,9 +1582,10 @@ static setbwte_status count_impl(setbwte_t h, const uint8_t* d_pat, const uint64
         API_CHECK(h, cudaMemsetAsync(d_out, 0, q * sizeof(uint64_t), h->stream));
         return SETBWTE_OK;
     }
+    const N5Dict n5 = cur_n5(h);
     API_CHECK(h, launch_count(h->prof, h->stream, cur_dict(h), cur_sb(h), h->n,
                               (const uint64_t*)h->d_C.p, (const uint8_t*)h->d_code_of.p, d_pat,
-                              d_off, q, d_out));
+                              d_off, q, d_out, h->sigma == 5 ? &n5 : nullptr));
     return SETBWTE_OK;
 }
 
@@ -1475,10 +1647,10 @@ setbwte_status setbwte_construct_sa(setbwte_t h, const uint8_t* strings, const u
     API_CHECK(h, ensure(h->bint, n_suf, &bint));
     API_CHECK(h, ensure(h->outbuf, n_suf, &asc));
     API_CHECK(h, sort_block(h->prof, h->stream, h->sort[0], po.pk.text, po.pk.term, 0,
-                            (uint32_t)n_suf, saf, nullptr, false, h->sopt));
+                            (uint32_t)n_suf, saf, nullptr, false, h->sopt, po.pk.nbit));
     API_CHECK(h, launch_gather(h->prof, h->stream, po.pk.text, po.pk.term, 0, saf, nullptr,
                                (uint32_t)n_suf, pos, 8, bint, nullptr, 0, nullptr,
-                               h->sopt.payload_limit));
+                               h->sopt.payload_limit, false, po.pk.nbit));
     API_CHECK(h, launch_bint_ascii(h->prof, h->stream, bint, (uint32_t)n_suf,
                                    (const uint8_t*)h->d_sym.p, asc));
     API_CHECK(h, launch_strip_payload(h->stream, saf, (uint32_t)n_suf, h->sopt.payload_limit));
@@ -1528,7 +1700,7 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "host_tier")) {
         // 1: move B_ext's dictionary to pinned host memory now (and keep it there)
         if (value != 1) return SETBWTE_E_INVALID_ARG;
-        if (h->sharded) return SETBWTE_E_UNSUPPORTED;
+        if (h->sharded || h->sigma == 5) return SETBWTE_E_UNSUPPORTED;
         h->hbm_budget = 0;
         if (!h->host_tier) {
             cudaError_t e = cudaSetDevice(h->device);
@@ -1556,7 +1728,8 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
         // 1: ranks share one address space; 2: separate processes (CUDA IPC)
         if (value > 2) return SETBWTE_E_INVALID_ARG;
         // needs the partition (world > 1, P <= 8), an empty index and no host tier
-        if (value && (h->world <= 1 || h->world > kMaxShards || h->host_tier || h->n != 0))
+        if (value && (h->world <= 1 || h->world > kMaxShards || h->host_tier || h->n != 0 ||
+                      h->sigma == 5))
             return SETBWTE_E_UNSUPPORTED;
         h->sharded = value != 0;
         h->shard_ipc = value == 2;
@@ -1569,6 +1742,11 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "sort_lanes")) {
         if (value > (uint64_t)setbwte_s::kMaxLanes) return SETBWTE_E_INVALID_ARG;
         h->sort_lanes = (int)value;
+    } else if (!strcmp(key, "force_exchange")) {
+        // test hook: run the partitioned ComputeRanks + exchange path even
+        // with world == 1 (one slice; with a communicator, one NCCL broadcast)
+        if (value > 1) return SETBWTE_E_INVALID_ARG;
+        h->force_exchange = value != 0;
     } else if (!strcmp(key, "rank_ilp")) {
         if (value < 1 || value > 4) return SETBWTE_E_INVALID_ARG;
         h->rank_ilp = (int)value;
@@ -1597,10 +1775,43 @@ setbwte_status setbwte_set_partition(setbwte_t h, int rank, int world,
     if (!h) return SETBWTE_E_INVALID_ARG;
     if (world < 1 || world > 1023 || rank < 0 || rank >= world) return SETBWTE_E_INVALID_ARG;
     if (world > 1 && !allgather) return SETBWTE_E_INVALID_ARG;
+    // a sharded dictionary is laid out for the partition it was created with
+    if (h->sharded && (world != h->world || world < 2 || world > kMaxShards))
+        return SETBWTE_E_UNSUPPORTED;
     h->rank = rank;
     h->world = world;
     h->allgather = allgather;
     h->allgather_ctx = ctx;
+    h->nccl = nullptr;  // the callback replaces a communicator
+    return SETBWTE_OK;
+}
+
+setbwte_status setbwte_set_comm(setbwte_t h, void* nccl_comm, int rank, int world) {
+    if (!h) return SETBWTE_E_INVALID_ARG;
+    if (h->failed) return SETBWTE_E_STATE;
+    if (!nccl_comm) {
+        // detach: back to a single rank (or to the callback, if one is set)
+        h->nccl = nullptr;
+        if (!h->allgather) {
+            if (h->sharded) return SETBWTE_E_UNSUPPORTED;
+            h->rank = 0;
+            h->world = 1;
+        }
+        return SETBWTE_OK;
+    }
+    if (world < 1 || world > 1023 || rank < 0 || rank >= world) return SETBWTE_E_INVALID_ARG;
+    if (h->sharded && (world != h->world || world < 2 || world > kMaxShards))
+        return SETBWTE_E_UNSUPPORTED;
+    const NcclApi& nc = nccl_api();
+    if (!nc.ok) return SETBWTE_E_NCCL;
+    ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+    int cnt = 0, me = 0;
+    if (nc.comm_count(comm, &cnt) != ncclSuccess || nc.comm_user_rank(comm, &me) != ncclSuccess)
+        return SETBWTE_E_NCCL;
+    if (cnt != world || me != rank) return SETBWTE_E_INVALID_ARG;
+    h->nccl = comm;
+    h->rank = rank;
+    h->world = world;
     return SETBWTE_OK;
 }
 

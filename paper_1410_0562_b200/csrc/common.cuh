@@ -76,6 +76,74 @@ __device__ __forceinline__ uint32_t suffix_key(const uint32_t* __restrict__ text
     return (syms << 4) | ended;
 }
 
+// ---- sigma = 5 (the fifth, largest symbol c_5, e.g. N of "ACGTN"; SPEC S:31,
+// P:28 Sec.2) ---------------------------------------------------------------
+// The packed text keeps its 2-bit plane; a third 1-bit-per-slot plane `nbit`
+// (big-endian, like `term`) marks the slots holding code 4, whose 2-bit code
+// is 0.  Key words then carry 3-bit symbols: 9 per word (kKeySyms5).
+constexpr int kKeySyms5 = 9;
+
+__device__ __forceinline__ uint32_t text_sym5(const uint32_t* __restrict__ text,
+                                              const uint32_t* __restrict__ nbit, uint64_t p) {
+    return term_bit(nbit, p) ? 4u : text_sym(text, p);
+}
+
+// Key word d of the suffix at slot p with 3-bit symbols (sigma = 5):
+//   bit 31     : 0
+//   bits 30..4 : the 9 symbols at slots q..q+8, q = p + 9d, 3 bits each
+//                (codes 0..4), symbols at and after the first terminator 0
+//   bits  3..0 : real symbols before the first terminator in the window,
+//                clamped to 9.
+// Same order argument as suffix_key (reading R6).
+__device__ __forceinline__ uint32_t suffix_key5(const uint32_t* __restrict__ text,
+                                                const uint32_t* __restrict__ term,
+                                                const uint32_t* __restrict__ nbit, uint64_t p,
+                                                uint32_t d) {
+    const uint64_t q = p + (uint64_t)kKeySyms5 * d;
+    const uint64_t w = q >> 4;
+    const uint32_t t = (uint32_t)(q & 15);
+    const uint64_t v = (((uint64_t)__ldg(text + w) << 32) | __ldg(text + w + 1)) << (2 * t);
+    const uint64_t tw = q >> 5;
+    const uint32_t tt = (uint32_t)(q & 31);
+    const uint64_t u = (((uint64_t)__ldg(term + tw) << 32) | __ldg(term + tw + 1)) << tt;
+    const uint64_t nn = (((uint64_t)__ldg(nbit + tw) << 32) | __ldg(nbit + tw + 1)) << tt;
+    uint32_t ended = (uint32_t)__clzll((long long)u);
+    ended = ended > (uint32_t)kKeySyms5 ? (uint32_t)kKeySyms5 : ended;
+    uint32_t syms = 0;
+#pragma unroll
+    for (int k = 0; k < kKeySyms5; ++k) {
+        const uint32_t c = (uint32_t)(v >> (62 - 2 * k)) & 3u;
+        const uint32_t isn = (uint32_t)(nn >> (63 - k)) & 1u;
+        syms = (syms << 3) | (isn ? 4u : c);
+    }
+    const uint32_t keep = 3 * ended;  // bits of real symbols to keep (from the top)
+    const uint32_t mask = keep == 0 ? 0u : (0x07FFFFFFu & ~((1u << (27 - keep)) - 1u));
+    syms &= mask;
+    return (syms << 4) | ended;
+}
+
+// The N plane of B_ext's dictionary (sigma = 5), beside the Blk array: per
+// 64 symbols the plane of code-4 symbols and their count since the enclosing
+// superblock; per superblock u64 nsb = code-4 symbols before it.  In the Blk
+// itself a code-4 symbol is stored like '$' (dol = 1, code 0), so the four
+// Blk counters and match_plane() never see it; '$' is dol & ~n.
+struct __align__(16) NBlk {
+    uint64_t n;
+    uint32_t cnt;
+    uint32_t pad;
+};
+static_assert(sizeof(NBlk) == 16, "NBlk is 16 bytes");
+
+// rank(c_5, i): code-4 symbols in B_ext[0, i)
+__device__ __forceinline__ uint64_t dict_rank_n(const NBlk* __restrict__ nblk,
+                                                const uint64_t* __restrict__ nsb, uint64_t i) {
+    const NBlk* b = nblk + (i >> 6);
+    uint64_t n, cw;
+    asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(n), "=l"(cw) : "l"(b));
+    const uint64_t mask = (1ull << (i & 63)) - 1ull;
+    return __ldg(nsb + (i >> kSbShift)) + (uint32_t)cw + (uint64_t)__popcll(n & mask);
+}
+
 // ---- rank dictionary ---------------------------------------------------------
 
 __device__ __forceinline__ uint64_t match_plane(uint32_t c, uint64_t lo, uint64_t hi, uint64_t dol) {

@@ -121,6 +121,7 @@ inline unsigned grid_for(uint64_t n, unsigned threads, unsigned cap = 148u * 32u
 struct Packed {
     uint32_t* text;       // 2-bit slot text
     uint32_t* term;       // terminator bitmap
+    uint32_t* nbit = nullptr;  // sigma = 5: code-4 bitmap (common.cuh), else null
     uint64_t* slot_off;   // m+1 slot offsets (slot_off[j] = offsets[j] + j)
     uint32_t* gfirst;     // string owning slot 32g, per 32-slot group
     uint64_t n_slots;
@@ -144,9 +145,15 @@ cudaError_t launch_partition(Profiler& prof, cudaStream_t s, const uint64_t* d_s
                              uint64_t m, uint64_t M, uint64_t* d_bounds, uint64_t* d_k);
 
 // Split strings [j0, j1) into `parts` contiguous slices balanced by suffix
-// count: out[r] = first string of slice r, out[parts] = j1.
+// count: out[r] = first string of slice r, out[parts] = j1, then
+// out[parts+1+r] = slot_off[out[r]] (the slices' slot boundaries).
 cudaError_t launch_slices(Profiler& prof, cudaStream_t s, const uint64_t* d_slot_off,
                           uint64_t j0, uint64_t j1, int parts, uint64_t* d_out);
+// The same for each of the K blocks of a partition (d_bounds as written by
+// launch_partition): 2*(parts+1) values per block, block after block.
+cudaError_t launch_slices_blocks(Profiler& prof, cudaStream_t s, const uint64_t* d_slot_off,
+                                 const uint64_t* d_bounds, uint64_t K, int parts,
+                                 uint64_t* d_out);
 
 // sort.cu -- A1 ConstructSA (Sec.3).
 struct SortScratch {
@@ -190,6 +197,13 @@ struct SortPattern {
     std::mutex mu;
     uint32_t n = 0;                                   // block size it was recorded on
     std::vector<std::vector<uint32_t>> rounds;        // NCLASS counts per round
+    uint32_t misses = 0;  // consecutive replays that needed host-driven rounds after it
+    void drop() {
+        std::lock_guard<std::mutex> lk(mu);
+        rounds.clear();
+        n = 0;
+        misses = 0;
+    }
 };
 struct SortOpts {
     uint64_t payload_limit = kPayloadLimit;
@@ -200,7 +214,22 @@ struct SortOpts {
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
                        uint32_t* d_sa_final, SortStats* st, bool reserve_only = false,
-                       const SortOpts& opts = SortOpts());
+                       const SortOpts& opts = SortOpts(), const uint32_t* nbit = nullptr);
+
+// sigma = 5 (common.cuh NBlk): the text's code-4 plane and the dictionary's
+// N plane + superblock counts, for the kernels that read them.
+struct N5Dict {
+    const uint32_t* nbit = nullptr;
+    const NBlk* nblk = nullptr;
+    const uint64_t* nsb = nullptr;
+};
+// ... and what Insert reads / writes of it.
+struct N5Ins {
+    const NBlk* in = nullptr;    // B_ext's N plane (n_in symbols; null when empty)
+    NBlk* out = nullptr;         // B_ext-new's N plane
+    uint64_t* ntot = nullptr;    // per output superblock code-4 total (scratch)
+    uint64_t* nsb_out = nullptr; // B_ext-new's N superblock counters
+};
 
 // ranks.cu -- A3 ComputeRanks (Lemma 1, Alg.2) and the
 // fused A2/A4 extraction + gather (Alg.1).
@@ -208,7 +237,8 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp, uint8_t* bslot = nullptr, bool bing = false);
+                                 int gw, int ilp, uint8_t* bslot = nullptr, bool bing = false,
+                                 const N5Dict* n5 = nullptr);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64).
 // Blocks without the SA payload get B_int from ComputeRanks: bslot (one byte
 // per slot) with u32 g, or bing = the top byte of each u64 g.
@@ -225,29 +255,32 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
                           uint64_t* sb_start = nullptr, uint64_t nsb = 0,
                           const uint8_t* bslot = nullptr, uint64_t payload_limit = kPayloadLimit,
-                          bool bing = false);
+                          bool bing = false, const uint32_t* nbit = nullptr);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,
                           const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                           Blk* out_blk, uint64_t* out_sb, uint64_t* sb_tot,
-                          const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C);
+                          const uint64_t* sb_start, uint64_t m_new, uint64_t* d_C,
+                          const N5Ins* n5 = nullptr);
 // Insert restricted to output superblocks [sb_begin, sb_end) (host tier)
 // and the closing superblock scan.
 cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,
                                 const void* pos, int gw, const uint8_t* bint, uint64_t n_ins,
                                 Blk* out_blk, uint64_t* sb_tot, const uint64_t* sb_start,
-                                uint64_t sb_begin, uint64_t sb_end);
+                                uint64_t sb_begin, uint64_t sb_end, const N5Ins* n5 = nullptr);
 cudaError_t launch_sb_scan(Profiler& prof, cudaStream_t s, const uint64_t* sb_tot, uint64_t nsb,
                            uint64_t* out_sb, uint64_t m_new, uint64_t* d_C);
 cudaError_t launch_rank_batch(Profiler& prof, cudaStream_t s, const Dict& blk, const uint64_t* sb,
                               uint64_t n, const uint8_t* code_of, const uint8_t* c,
-                              const uint64_t* k, uint64_t q, uint64_t* out);
+                              const uint64_t* k, uint64_t q, uint64_t* out,
+                              const N5Dict* n5 = nullptr);
 cudaError_t launch_count(Profiler& prof, cudaStream_t s, const Dict& blk, const uint64_t* sb,
                          uint64_t n, const uint64_t* d_C, const uint8_t* code_of,
-                         const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out);
+                         const uint8_t* pat, const uint64_t* poff, uint64_t q, uint64_t* out,
+                         const N5Dict* n5 = nullptr);
 cudaError_t launch_decode(Profiler& prof, cudaStream_t s, const Dict& blk, uint64_t n,
-                          const uint8_t* sym_ascii, uint8_t* out);
+                          const uint8_t* sym_ascii, uint8_t* out, const NBlk* nblk = nullptr);
 // Debug/export: SA + B_int ASCII of a sorted block.
 cudaError_t launch_bint_ascii(Profiler& prof, cudaStream_t s, const uint8_t* bint,
                               uint32_t n_suf, const uint8_t* sym_ascii, uint8_t* out);

@@ -41,7 +41,10 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
     const uint8_t* __restrict__ bytes, uint64_t n_bytes, const uint64_t* __restrict__ slot_off,
     const uint32_t* __restrict__ gfirst, uint64_t m, uint64_t n_slots,
     const uint8_t* __restrict__ code_of_g, uint32_t* __restrict__ text, uint32_t* __restrict__ term,
-    unsigned long long* __restrict__ err_pos, uint64_t g_begin, uint64_t g_end) {
+    uint32_t* __restrict__ nbit, unsigned long long* __restrict__ err_pos, uint64_t g_begin,
+    uint64_t g_end) {
+    // nbit (sigma = 5): code 4 is stored as 2-bit code 0 plus a set nbit bit
+    const uint32_t maxc = nbit ? 4u : 3u;
     __shared__ __align__(16) uint8_t sbuf[kPackWarps][1024 + 80];
     __shared__ uint8_t code_of[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) code_of[i] = code_of_g[i];
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
         if (gv) {
             const uint64_t s0 = g << 5;
             uint64_t next = slot_off[j + 1];
-            uint32_t w0 = 0, w1 = 0, tw = 0;
+            uint32_t w0 = 0, w1 = 0, tw = 0, nw5 = 0;
             const int cnt = (int)min((uint64_t)32, n_slots - s0);
             for (int t = 0; t < cnt; ++t) {
                 const uint64_t s = s0 + t;
@@ -85,7 +88,9 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
                     const uint64_t li = bp - al;
                     if (bp < n_bytes && li < 1024 + 80) {
                         const uint8_t c = code_of[sb[li]];
-                        if (c > 3) atomicMin(err_pos, (unsigned long long)bp); else code = c;
+                        if (c > maxc) atomicMin(err_pos, (unsigned long long)bp);
+                        else if (c == 4) nw5 |= 1u << (31 - t);
+                        else code = c;
                     }
                 }
                 if (t < 16) w0 |= code << (30 - 2 * t); else w1 |= code << (30 - 2 * (t - 16));
@@ -93,6 +98,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
             text[2 * g] = w0;
             text[2 * g + 1] = w1;
             term[g] = tw;
+            if (nbit) nbit[g] = nw5;
         }
         __syncwarp();
     }
@@ -108,6 +114,7 @@ cudaError_t launch_pack_prepare(Profiler& prof, cudaStream_t s, const uint64_t* 
     // padding words past the end must read as zero
     SB_CHECK(cudaMemsetAsync(pk.text + 2 * n_groups, 0, 4 * sizeof(uint32_t), s));
     SB_CHECK(cudaMemsetAsync(pk.term + n_groups, 0, 4 * sizeof(uint32_t), s));
+    if (pk.nbit) SB_CHECK(cudaMemsetAsync(pk.nbit + n_groups, 0, 4 * sizeof(uint32_t), s));
     return cudaSuccess;
 }
 
@@ -121,7 +128,7 @@ cudaError_t launch_pack_range(Profiler& prof, cudaStream_t s, const uint8_t* d_b
     SB_LAUNCH(prof, s, "pack", 1.375 * (double)slots, slots,
               pack_kernel<<<grid_for(n_warps, kPackWarps, 148u * 16u), kPackWarps * 32, 0, s>>>(
                   d_bytes, n_bytes, pk.slot_off, pk.gfirst, m, pk.n_slots, d_code_of, pk.text,
-                  pk.term, d_err_pos, g_begin, g_end));
+                  pk.term, pk.nbit, d_err_pos, g_begin, g_end));
     return cudaGetLastError();
 }
 
@@ -168,7 +175,15 @@ cudaError_t launch_partition(Profiler& prof, cudaStream_t s, const uint64_t* d_s
 }
 
 __global__ void slices_kernel(const uint64_t* __restrict__ slot_off, uint64_t j0, uint64_t j1,
-                              int parts, uint64_t* __restrict__ out) {
+                              const uint64_t* __restrict__ bounds, int parts,
+                              uint64_t* __restrict__ out) {
+    // one CTA per block: block k = strings [bounds[2k], bounds[2k+2]) when
+    // bounds is given (the whole append's partition), else [j0, j1)
+    if (bounds) {
+        j0 = bounds[2 * blockIdx.x];
+        j1 = bounds[2 * blockIdx.x + 2];
+    }
+    out += (uint64_t)blockIdx.x * 2 * (parts + 1);
     const int r = threadIdx.x;
     if (r > parts) return;
     const uint64_t S0 = slot_off[j0], S1 = slot_off[j1];
@@ -178,13 +193,24 @@ __global__ void slices_kernel(const uint64_t* __restrict__ slot_off, uint64_t j0
         const uint64_t mid = (lo + hi) >> 1;
         if (slot_off[mid] >= target) hi = mid; else lo = mid + 1;
     }
-    out[r] = r == parts ? j1 : lo;
+    const uint64_t j = r == parts ? j1 : lo;
+    out[r] = j;
+    out[parts + 1 + r] = slot_off[j];
 }
 
 cudaError_t launch_slices(Profiler& prof, cudaStream_t s, const uint64_t* d_slot_off,
                           uint64_t j0, uint64_t j1, int parts, uint64_t* d_out) {
     SB_LAUNCH(prof, s, "slices", 0, 0,
-              slices_kernel<<<1, 1024, 0, s>>>(d_slot_off, j0, j1, parts, d_out));
+              slices_kernel<<<1, 1024, 0, s>>>(d_slot_off, j0, j1, nullptr, parts, d_out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slices_blocks(Profiler& prof, cudaStream_t s, const uint64_t* d_slot_off,
+                                 const uint64_t* d_bounds, uint64_t K, int parts,
+                                 uint64_t* d_out) {
+    if (K == 0) return cudaSuccess;
+    SB_LAUNCH(prof, s, "slices", 0, 0,
+              slices_kernel<<<(unsigned)K, 1024, 0, s>>>(d_slot_off, 0, 0, d_bounds, parts, d_out));
     return cudaGetLastError();
 }
 

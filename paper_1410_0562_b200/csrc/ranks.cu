@@ -46,13 +46,17 @@ __device__ __forceinline__ void store4<uint64_t>(uint64_t* dst, uint64_t a, uint
 #ifndef SB_RANK_MINB
 #define SB_RANK_MINB 5
 #endif
-template <class G, class D>
+// N5 (sigma = 5): a symbol of code 4 (nbit plane) steps through the N plane
+// of the dictionary: i := C[4] + rank_n(i); B_int records it as 5.
+template <class G, class D, bool N5>
 __global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
     const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
     uint64_t j1, uint64_t slot_base, const D blk, const uint64_t* __restrict__ sb,
     const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot,
-    bool bing) {
+    bool bing, const uint32_t* __restrict__ nbit, const NBlk* __restrict__ nblk,
+    const uint64_t* __restrict__ nsb) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
+    const uint64_t C4 = N5 ? Cd[4] : 0;
     for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
          j += (uint64_t)gridDim.x * blockDim.x) {
         // local slot indices: [l0, le], le = terminator
@@ -66,18 +70,34 @@ __global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
         // suffix instead of two random text lookups
         if (bslot) bslot[l0] = 4;
         uint64_t lp = le;  // next step computes slot lp-1
-        uint64_t wi = ~0ull;
-        uint32_t word = 0;
-        auto step = [&](uint64_t q) -> uint64_t {  // LF step for local slot q
-            const uint64_t p = q + slot_base;
+        uint64_t wi = ~0ull, nwi = ~0ull;
+        uint32_t word = 0, nword = 0;
+        // the symbol at global slot p: code 0..3, or 4 (sigma = 5)
+        auto sym = [&](uint64_t p) -> uint32_t {
             if ((p >> 4) != wi) {
                 wi = p >> 4;
                 word = __ldg(text + wi);
             }
-            const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
-            if (bslot) bslot[q + 1] = (uint8_t)c;
-            const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
-            i = Cc + dict_rank(blk, sb, c, i);
+            uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
+            if (N5) {
+                if ((p >> 5) != nwi) {
+                    nwi = p >> 5;
+                    nword = __ldg(nbit + nwi);
+                }
+                if ((nword >> (31 - (uint32_t)(p & 31))) & 1u) c = 4u;
+            }
+            return c;
+        };
+        auto step = [&](uint64_t q) -> uint64_t {  // LF step for local slot q
+            const uint64_t p = q + slot_base;
+            const uint32_t c = sym(p);
+            if (bslot) bslot[q + 1] = (uint8_t)(c == 4u ? 5u : c);
+            if (N5 && c == 4u) {
+                i = C4 + dict_rank_n(nblk, nsb, i);
+            } else {
+                const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
+                i = Cc + dict_rank(blk, sb, c, i);
+            }
             return i;
         };
         if (sizeof(G) == 8 && bing) {
@@ -87,9 +107,8 @@ __global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
             uint64_t pq = le, pv = i;
             for (uint64_t q = le; q-- > l0;) {
                 const uint64_t v = step(q);
-                const uint64_t p = q + slot_base;
-                const uint32_t c = (word >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
-                g[pq] = (G)(pv | ((uint64_t)c << 56));
+                const uint32_t c = sym(q + slot_base);
+                g[pq] = (G)(pv | ((uint64_t)(c == 4u ? 5u : c) << 56));
                 pq = q;
                 pv = v;
             }
@@ -174,13 +193,28 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp, uint8_t* bslot, bool bing) {
+                                 int gw, int ilp, uint8_t* bslot, bool bing, const N5Dict* n5) {
     if (j1 <= j0) return cudaSuccess;
     // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
     // superblock counter + g write + 0.25 B packed symbol; per string: 16 B
     // slot offsets + the terminator g.  Units = LF steps.
     const uint64_t nstr = j1 - j0;
     const double bytes = (40.25 + gw) * (double)n_steps + (16.0 + gw) * (double)nstr;
+    if (n5) {
+        // sigma = 5 (never sharded): the plain-array kernel with the N plane
+        const unsigned grid = grid_for(nstr, 256, 1u << 20);
+        if (gw == 4)
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_kernel<uint32_t, const Blk*, true><<<grid, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
+                          (uint32_t*)g, bslot, false, n5->nbit, n5->nblk, n5->nsb)));
+        else
+            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
+                      (compute_ranks_kernel<uint64_t, const Blk*, true><<<grid, 256, 0, s>>>(
+                          text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
+                          (uint64_t*)g, bslot, bing, n5->nbit, n5->nblk, n5->nsb)));
+        return cudaGetLastError();
+    }
     if (ilp > 1 && !bslot && !bing) {
         const unsigned gi = grid_for((nstr + 3) / 4, 256, 1u << 20);
         if (gw == 4) {
@@ -198,25 +232,25 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
     if (gw == 4) {
         if (blk.P == 1)
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                      (compute_ranks_kernel<uint32_t, const Blk*><<<grid, 256, 0, s>>>(
+                      (compute_ranks_kernel<uint32_t, const Blk*, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
-                          (uint32_t*)g, bslot, false)));
+                          (uint32_t*)g, bslot, false, nullptr, nullptr, nullptr)));
         else
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                      (compute_ranks_kernel<uint32_t, Dict><<<grid, 256, 0, s>>>(
+                      (compute_ranks_kernel<uint32_t, Dict, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g,
-                          bslot, false)));
+                          bslot, false, nullptr, nullptr, nullptr)));
     } else {
         if (blk.P == 1)
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                      (compute_ranks_kernel<uint64_t, const Blk*><<<grid, 256, 0, s>>>(
+                      (compute_ranks_kernel<uint64_t, const Blk*, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
-                          (uint64_t*)g, bslot, bing)));
+                          (uint64_t*)g, bslot, bing, nullptr, nullptr, nullptr)));
         else
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                      (compute_ranks_kernel<uint64_t, Dict><<<grid, 256, 0, s>>>(
+                      (compute_ranks_kernel<uint64_t, Dict, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g,
-                          bslot, bing)));
+                          bslot, bing, nullptr, nullptr, nullptr)));
     }
     return cudaGetLastError();
 }
@@ -230,7 +264,7 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
                               const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
                               uint8_t* __restrict__ bint, uint64_t* __restrict__ sb_start,
                               uint64_t nsb, const uint8_t* __restrict__ bslot, bool bing,
-                              uint32_t smask) {
+                              uint32_t smask, const uint32_t* __restrict__ nbit) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t iters = (n_suf + stride - 1) / stride;  // warp-uniform trip count
@@ -258,8 +292,12 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
             } else {
                 const uint64_t p = slot_base + sl;
                 if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
+                else if (nbit && term_bit(nbit, p - 1)) b = 5;
                 else b = (uint8_t)text_sym(text, p - 1);
             }
+            // B_int byte: code bits 0-1, '$' flag 4; code 4 of sigma = 5 (carried
+            // as 5) is stored like '$' plus the N flag 8 (common.cuh NBlk)
+            if (b == 5) b = 12;
             __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
         }
         if (sb_start) {
@@ -285,7 +323,7 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
                           const void* g, uint32_t n_suf, void* pos, int gw, uint8_t* bint,
                           uint64_t* sb_start, uint64_t nsb, const uint8_t* bslot,
-                          uint64_t payload_limit, bool bing) {
+                          uint64_t payload_limit, bool bing, const uint32_t* nbit) {
     const uint32_t smask = sa_slot_mask(n_suf, payload_limit);
     // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol + term bit)
     const double bytes = (5.375 + 2.0 * gw) * n_suf;
@@ -294,12 +332,12 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint32_t*)g, n_suf,
-                                                               (uint32_t*)pos, bint, sb_start, nsb, bslot, false, smask));
+                                                               (uint32_t*)pos, bint, sb_start, nsb, bslot, false, smask, nbit));
     } else {
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint64_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
                                                                (const uint64_t*)g, n_suf,
-                                                               (uint64_t*)pos, bint, sb_start, nsb, bslot, bing, smask));
+                                                               (uint64_t*)pos, bint, sb_start, nsb, bslot, bing, smask, nbit));
     }
     return cudaGetLastError();
 }

@@ -94,19 +94,26 @@ struct Bufs {
     uint32_t smask;  // slot bits of an SA entry (sa_slot_mask); ~0 without payload
     uint32_t* key1[2];  // key word 1 in position order (large blocks), or null
     uint32_t n;         // suffixes of the block (debug bounds checks)
+    const uint32_t* nbit;  // sigma = 5: code-4 plane of the text (common.cuh), else null
+    uint32_t ksyms;        // symbols per key word: kKeySyms (14) or kKeySyms5 (9)
 };
 
 // Key word `word` of the suffix of an SA entry (text lookups).
 __device__ __forceinline__ uint32_t key_of(const Bufs& B, uint32_t entry, uint32_t word) {
+    if (B.nbit) return suffix_key5(B.text, B.term, B.nbit, B.base + (entry & B.smask), word);
     return suffix_key(B.text, B.term, B.base + (entry & B.smask), word);
 }
 
 // SA entry of block-local slot sl: the slot plus, with payload, its B_int
-// symbol (the symbol before the suffix, or 4 = '$' at a string start).
+// symbol (the symbol before the suffix: its code 0..3, 4 = '$' at a string
+// start, 5 = code 4 of sigma = 5).
 __device__ __forceinline__ uint32_t sa_entry(const Bufs& B, uint32_t sl) {
     if (B.smask == 0xFFFFFFFFu) return sl;
     const uint64_t p = B.base + sl;
-    const uint32_t b = (sl == 0 || term_bit(B.term, p - 1)) ? 4u : text_sym(B.text, p - 1);
+    uint32_t b;
+    if (sl == 0 || term_bit(B.term, p - 1)) b = 4u;
+    else if (B.nbit && term_bit(B.nbit, p - 1)) b = 5u;
+    else b = text_sym(B.text, p - 1);
     return sl | (b << kPayloadShift);
 }
 
@@ -247,7 +254,7 @@ __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint3
         const bool g_active = active;  // whole groups are active or not
         const bool eqp = g_active && lane > group && kp == key;
         const bool eqn = g_active && lane + 1 < gend && kn == key;
-        active = (eqp || eqn) && ((key & 15u) == (uint32_t)kKeySyms);
+        active = (eqp || eqn) && ((key & 15u) == B.ksyms);
         const uint32_t st2 = __ballot_sync(0xFFFFFFFFu, !active || !eqp);
         group = active ? 31u - __clz(st2 & (0xFFFFFFFFu >> (31 - lane))) : lane;
         if (!__any_sync(0xFFFFFFFFu, active)) break;
@@ -388,6 +395,14 @@ __global__ void keygen_kernel(const uint32_t* __restrict__ text, const uint32_t*
     }
 }
 
+// Key word 0 of every slot with 3-bit symbols (sigma = 5), one slot per thread.
+__global__ void keygen5_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
+                               const uint32_t* __restrict__ nbit, uint64_t base, uint32_t n,
+                               uint32_t* __restrict__ key) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        key[i] = suffix_key5(text, term, nbit, base + i, 0);
+}
+
 // ---------------------------------------------------------------------------
 // init / control
 // ---------------------------------------------------------------------------
@@ -485,7 +500,7 @@ __global__ void __launch_bounds__(kDigNt, SB_HIST_MINB) digit_hist_kernel(Lists 
         const bool kv = meta_kv(s.meta);
         const uint32_t* S = B.sa[buf];
         uint32_t* K = B.key[buf];
-        if (!kv && meta_iota(s.meta) && s.word == 0) {
+        if (!kv && meta_iota(s.meta) && s.word == 0 && !B.nbit) {
             // the block's first pass: key word 0 generated here from the packed
             // text (16 consecutive slots per thread, keys16) and written for the
             // scatter -- no separate key-generation pass
@@ -602,7 +617,8 @@ __global__ void __launch_bounds__(256) group_scan_kernel(const Group* __restrict
 __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
                                                          SegX* __restrict__ segx,
                                                          uint32_t* __restrict__ gtot,
-                                                         uint32_t* __restrict__ dbase) {
+                                                         uint32_t* __restrict__ dbase,
+                                                         uint32_t ksyms) {
     __shared__ uint32_t wsum[8];
     __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
     __shared__ int all_one;
@@ -640,7 +656,7 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
         __syncthreads();
         const uint32_t shift = meta_shift(s.meta);
         const uint32_t buf = meta_buf(s.meta);
-        const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < (uint32_t)kKeySyms);
+        const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < ksyms);
         uint32_t flag = 0;
         int cls = -1;
         Seg c;
@@ -816,7 +832,10 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
                     const uint32_t pk = lane == 0 ? carry : up;
                     carry = last;
                     const uint32_t sl = slot[it];
-                    const uint32_t b = (sl == 0 || (pk & 15u) == 0) ? 4u : (pk >> 30);
+                    uint32_t b;
+                    if (sl == 0 || (pk & 15u) == 0) b = 4u;
+                    else if (B.nbit) b = ((pk >> 28) & 7u) == 4u ? 5u : ((pk >> 28) & 7u);
+                    else b = pk >> 30;
                     slot[it] = sl | (b << kPayloadShift);
                 }
             } else {
@@ -880,7 +899,7 @@ constexpr uint32_t kTinyPerWarp = 32;  // list entries per warp, packed into sha
 // this word with 14 real symbols and `run` the first lane of their tie run.
 __device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint32_t grp,
                                                 uint32_t key, uint32_t rb, bool& tie,
-                                                uint32_t& run, uint32_t& x) {
+                                                uint32_t& run, uint32_t& x, uint32_t ksyms) {
     // x: a per-element value permuted along with the slot
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = lane < L;
@@ -909,7 +928,7 @@ __device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint3
     const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, hi, 1);
     const bool eqp = valid && lane > 0 && prv == hi;
     const bool eqn = valid && lane + 1 < L && nxt == hi;
-    tie = (eqp || eqn) && ((k2 & 15u) == (uint32_t)kKeySyms);
+    tie = (eqp || eqn) && ((k2 & 15u) == ksyms);
     const uint32_t starts = __ballot_sync(0xFFFFFFFFu, tie && !eqp);
     run = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
     return s2;
@@ -951,7 +970,7 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
                         bool tie;
                         uint32_t run;
                         uint32_t k1p = k1;
-                        r = warp_sort16(slot, lb, grp, key, rb, tie, run, k1p);
+                        r = warp_sort16(slot, lb, grp, key, rb, tie, run, k1p, B.ksyms);
                         // ties continue on word+1; word 1 comes from the carried
                         // key-1 words (permuted with the slots; the flag is the
                         // same for every lane of a segment)
@@ -1013,7 +1032,7 @@ __device__ __forceinline__ void warp_tail(const uint2* buf, const Seg& s, const 
             const uint32_t e = it * 32 + lane;
             const uint32_t k = buf[e].x;
             const bool st = e < L && (e == 0 || buf[e - 1].x != k) && e + 1 < L &&
-                            buf[e + 1].x == k && (k & 15u) == (uint32_t)kKeySyms;
+                            buf[e + 1].x == k && (k & 15u) == B.ksyms;
             uint32_t m = __ballot_sync(0xFFFFFFFFu, st);
             while (m) {
                 const uint32_t l = __ffs(m) - 1;
@@ -1162,7 +1181,7 @@ __global__ void __launch_bounds__(kWarpCta * 32, SB_BIT_MINB) bitonic_kernel(Lis
         for (int r = 0; r < NIT; ++r) {
             const uint32_t e = lane * NIT + r;
             const uint32_t nk = r + 1 < NIT ? k16[r + 1] : nxt0;
-            if (e + 1 < L && nk == k16[r] && (k16[r] & 15u) == (uint32_t)kKeySyms) eqn |= 1u << r;
+            if (e + 1 < L && nk == k16[r] && (k16[r] & 15u) == B.ksyms) eqn |= 1u << r;
         }
         const uint32_t lastn = __shfl_up_sync(0xFFFFFFFFu, eqn >> (NIT - 1), 1) & (lane > 0 ? 1u : 0u);
         const uint32_t eqp = ((eqn << 1) | lastn) & ((1u << NIT) - 1u);  // bit r: ties with e-1
@@ -1525,7 +1544,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
             B.saf[s.start + i] = slotA[i];
             const uint32_t k = keyA[i];
             const bool starts = (i == 0 || keyA[i - 1] != k) && i + 1 < len && keyA[i + 1] == k &&
-                                (k & 15u) == (uint32_t)kKeySyms;
+                                (k & 15u) == B.ksyms;
             if (starts) {
                 uint32_t L = 2;
                 while (i + L < len && keyA[i + L] == k) ++L;
@@ -1561,13 +1580,14 @@ using namespace sortk;
 cudaError_t sort_reserve(SortScratch& ws, uint32_t n_suf, const SortOpts& opts) {
     Profiler dummy;
     (void)dummy;
-    return sort_block(dummy, nullptr, ws, nullptr, nullptr, 0, n_suf, nullptr, nullptr, true, opts);
+    return sort_block(dummy, nullptr, ws, nullptr, nullptr, 0, n_suf, nullptr, nullptr, true, opts,
+                      nullptr);
 }
 
 cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const uint32_t* text,
                        const uint32_t* term, uint64_t slot_base, uint32_t n_suf,
                        uint32_t* d_sa_final, SortStats* st, bool reserve_only,
-                       const SortOpts& opts) {
+                       const SortOpts& opts, const uint32_t* nbit) {
     if (n_suf == 0) return cudaSuccess;
     const size_t n = n_suf;
     const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
@@ -1610,7 +1630,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         A.cnt = ctr;
         Bl.cnt = ctr + NCLASS;
     }
-    if (n >= opts.kw1_min) {
+    const bool kw1 = n >= opts.kw1_min && !nbit;  // sigma = 5: no carried key word 1
+    if (kw1) {
         uint32_t* kw1;
         SB_CHECK(ensure(ws.kw1, n + 16, &kw1));
         SB_CHECK(ensure(ws.kw1b, n + 16, &kw1));
@@ -1628,6 +1649,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.smask = sa_slot_mask(n_suf, opts.payload_limit);
     B.key1[0] = B.key1[1] = nullptr;
     B.n = n_suf;
+    B.nbit = nbit;
+    B.ksyms = nbit ? (uint32_t)kKeySyms5 : (uint32_t)kKeySyms;
 
     // (set on every call: cheap, per device, and safe from several host threads)
     constexpr size_t sm_m = local_smem<kCapM, kNtM>();
@@ -1646,7 +1669,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<4, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d1));
 
-    if (n >= opts.kw1_min) {
+    if (kw1) {
         // large blocks carry key word 1 with every element through the digit
         // passes (B.key1, position order): resolving a word-0 tie then reads
         // the element's own word-1 key, not two random text lookups.  Key
@@ -1661,10 +1684,15 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         B.key1[0] = k1a;
         B.key1[1] = k1b;
     }
-    if (n <= kCapM) {
+    if (n <= kCapM && !nbit) {
         SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
                   keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(
                       text, term, slot_base, n_suf, k0));
+        SB_CHECK(cudaGetLastError());
+    } else if (n <= kCapM) {
+        SB_LAUNCH(prof, s, "sort_keygen", 4.5 * n, n,
+                  keygen5_kernel<<<grid_for(n, 256, 148u * 16u), 256, 0, s>>>(
+                      text, term, nbit, slot_base, n_suf, k0));
         SB_CHECK(cudaGetLastError());
     }
     SB_LAUNCH(prof, s, "sort_init", n <= kCapM ? 4.0 * n : 0.0, n,
@@ -1744,7 +1772,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
             SB_CHECK(cudaGetLastError());
             SB_LAUNCH(prof, s, "digit_scan", 0, 0,
                       digit_scan_kernel<<<std::min<uint32_t>(cnt[LARGE], 148u * 8u), 256, 0, s>>>(
-                          in, out, segx, gtot, dbase));
+                          in, out, segx, gtot, dbase, B.ksyms));
             SB_CHECK(cudaGetLastError());
             if (B.key1[0]) {
                 SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
@@ -1802,6 +1830,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         if (st) st->replayed++;
     }
     std::vector<std::vector<uint32_t>> rec;
+    uint32_t extra = 0;  // host-driven rounds after a replay
     for (;;) {
         uint32_t any_in = 0, any_out = 0;
         for (int c = 0; c < NCLASS; ++c) {
@@ -1817,7 +1846,10 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
             continue;
         }
         if (!replayable) rec.emplace_back(h_cnt, h_cnt + NCLASS);
-        else if (st) st->after_replay++;
+        else {
+            if (st) st->after_replay++;
+            ++extra;
+        }
         SB_CHECK(run_round(h_cnt));
         SB_CHECK(read_back());
     }
@@ -1826,6 +1858,17 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         if (pat->rounds.empty()) {
             pat->n = n;
             pat->rounds = rec;
+            pat->misses = 0;
+        }
+    } else if (pat && replayable) {
+        // a stale pattern (blocks of another read-length mix): re-record it
+        // after two consecutive replays that needed extra host-driven rounds
+        std::lock_guard<std::mutex> lk(pat->mu);
+        pat->misses = extra > 1 ? pat->misses + 1 : 0;
+        if (pat->misses >= 2) {
+            pat->rounds.clear();
+            pat->n = 0;
+            pat->misses = 0;
         }
     }
     const uint64_t act_local = h_misc[M_ACTIVE];

@@ -6,7 +6,9 @@ independent per string); the slices are then assembled on every rank by one
 exchange -- an all-gather-v of the g slices.  The library calls back into
 ``make_allgather``'s function with the device buffer; the exchange itself is a
 sequence of NCCL broadcasts (one per source rank) through torch.distributed,
-queued on the library's stream.
+queued on the library's stream.  The production form is ``SetBWTE.set_comm``
+with ``nccl_comm(group)``: the library then issues the NCCL group itself, on
+its own stream, with no Python call per block.
 """
 from __future__ import annotations
 
@@ -42,11 +44,30 @@ def make_allgather(group=None):
     def _cb(buf_ptr: int, bytes_per_rank, world: int, stream_ptr: int):
         total = sum(bytes_per_rank)
         buf = torch.as_tensor(_CAI(buf_ptr, total), device="cuda")
-        # the library's stream is torch's current stream (bench sets it), so the
-        # collectives are ordered after ComputeRanks and before the gather.
-        allgather_slices(buf, bytes_per_rank, group)
+        # the slices are only QUEUED on the library's stream: issue the
+        # collectives on that same stream, so they run after ComputeRanks wrote
+        # this rank's slice and before the gather reads the others
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr)):
+            allgather_slices(buf, bytes_per_rank, group)
 
     return _cb
+
+
+def nccl_comm(group=None) -> int:
+    """Address of the ncclComm_t behind a torch.distributed NCCL group (the
+    default group if None), for SetBWTE.set_comm.  The communicator is created
+    eagerly if the group has not used it yet."""
+    g = group if group is not None else dist.group.WORLD
+    dev = torch.device("cuda", torch.cuda.current_device())
+    backend = g._get_backend(dev)
+    ptr = int(backend._comm_ptr())
+    if ptr == 0:
+        # lazily initialised communicator: one tiny collective creates it
+        t = torch.zeros(1, device=dev)
+        dist.all_reduce(t, group=g)
+        torch.cuda.synchronize(dev)
+        ptr = int(backend._comm_ptr())
+    return ptr
 
 
 def balanced_slices(slot_off, j0: int, j1: int, parts: int):

@@ -17,6 +17,8 @@ Recipes (shapes follow BASELINE.json configs):
                               bases: uniform start, 50 % reverse complement,
                               0.5 % substitutions -- overlapping reads give
                               deep LCPs like real sequencing sets.
+* ``uniform_n(m, L, p_n)`` -- as ``uniform`` over ACGT, each base replaced by N
+                              with probability p_n (sigma = 5).
 * ``random_set(...)``      -- small random sets for property tests (m <= 64,
                               |P| <= 50, empty and duplicate strings).
 * ``adversarial(kind)``    -- all-A, (AC)^k, many empty strings.
@@ -51,6 +53,14 @@ def to_strings(data, offsets):
 def uniform(m: int, L: int, seed: int = 1):
     rng = _rng(seed)
     data = ACGT[rng.integers(0, 4, size=m * L, dtype=np.uint8)]
+    offsets = np.arange(m + 1, dtype=np.uint64) * np.uint64(L)
+    return data, offsets
+
+
+def uniform_n(m: int, L: int, p_n: float = 0.01, seed: int = 1):
+    rng = _rng(seed)
+    data = ACGT[rng.integers(0, 4, size=m * L, dtype=np.uint8)]
+    data[rng.random(m * L) < p_n] = ord("N")
     offsets = np.arange(m + 1, dtype=np.uint64) * np.uint64(L)
     return data, offsets
 

@@ -44,6 +44,14 @@ def test_binding_loads_and_strerror(lib):
     L = binding.load_library()
     assert L.setbwte_strerror(0) == b"ok"
     assert L.setbwte_strerror(2) == b"invalid character"
+    assert b"NCCL" in L.setbwte_strerror(8)
+
+
+def test_set_comm_argument_checks_without_gpu(lib):
+    """setbwte_set_comm rejects a NULL handle before touching NCCL or CUDA."""
+    from paper_1410_0562_b200 import binding
+    L = binding.load_library()
+    assert L.setbwte_set_comm(None, None, 0, 1) == 1
 
 
 def test_create_without_gpu_fails_loudly(lib):
@@ -60,7 +68,7 @@ def test_create_rejects_bad_alphabets(lib):
     from paper_1410_0562_b200 import binding
     L = binding.load_library()
     h = ctypes.c_void_p()
-    assert L.setbwte_create(b"ACGTN", ctypes.byref(h)) == 6   # sigma > 4: unsupported
+    assert L.setbwte_create(b"ACGTNX", ctypes.byref(h)) == 6  # sigma > 5: unsupported
     assert L.setbwte_create(b"", ctypes.byref(h)) == 1
     assert L.setbwte_create(b"AA", ctypes.byref(h)) == 1
     assert L.setbwte_create(b"A$", ctypes.byref(h)) == 1
