@@ -55,7 +55,8 @@ STAGE_OF = {
     "sort_init": "sort", "sort_tiny": "sort", "sort_small": "sort", "sort_medium": "sort",
     "sort_warp": "sort", "sort_ctl": "sort",
     "sort_chunkify": "sort", "digit_hist": "sort", "digit_scan": "sort", "digit_scatter": "sort",
-    "compute_ranks": "rank", "slices": "rank", "gather": "gather", "insert": "insert",
+    "compute_ranks": "rank", "slices": "rank", "gather": "gather", "gather_part": "gather",
+    "gather_fetch": "gather", "insert": "insert",
     "sb_scan": "insert",
 }
 
@@ -77,7 +78,7 @@ def stage_fractions(kern: dict, stages: dict, peak_gbs: float, n_suf: int):
         return sum(v["bytes"] for k, v in kern.items() if k in names)
     out = {"timing": "serialised warm-up step (stage_ms_per_step)"}
     sort_names = [k for k in kern if k.startswith(("sort_", "digit_"))]
-    for st, names in (("sort", sort_names), ("gather", ["gather"]),
+    for st, names in (("sort", sort_names), ("gather", ["gather", "gather_part", "gather_fetch"]),
                       ("insert", ["insert", "sb_scan"]), ("pack", ["pack", "slot_offsets"]),
                       ("rank", ["compute_ranks"])):
         ms = stages.get(st, 0.0)

@@ -56,16 +56,21 @@ typedef enum {
     SETBWTE_E_OUT_OF_RANGE = 3,  /* rank position k > n */
     SETBWTE_E_NOMEM = 4,         /* device or pinned-host allocation failed */
     SETBWTE_E_CUDA = 5,          /* a CUDA runtime/kernel error (handle becomes sticky-failed) */
-    SETBWTE_E_UNSUPPORTED = 6,   /* e.g. sigma > 4 on the 2-bit path, block too large */
+    SETBWTE_E_UNSUPPORTED = 6,   /* e.g. sigma > 5, block too large, a sigma = 5 host tier */
     SETBWTE_E_STATE = 7,         /* handle previously failed, or call not valid now */
     SETBWTE_E_NCCL = 8           /* setbwte_set_comm: NCCL not loadable, or an NCCL call failed */
 } setbwte_status;
 
-/* Create an empty index.  alphabet: NUL-terminated, 1..4 distinct bytes in
- * increasing symbol order c_1 < ... < c_sigma (Sec.2), e.g. "ACGT";
- * '$' is reserved.  Matching is case-insensitive (reading R10).  sigma > 4 ->
- * SETBWTE_E_UNSUPPORTED (2-bit packed path).  Binds the current CUDA device
- * and creates a private non-blocking stream.  *out receives the handle. */
+/* Create an empty index.  alphabet: NUL-terminated, 1..5 distinct bytes in
+ * increasing symbol order c_1 < ... < c_sigma (Sec.2), e.g. "ACGT" or
+ * "ACGTN" (SPEC S:31's default alphabet); '$' is reserved.  Matching is
+ * case-insensitive (reading R10).  sigma <= 4 uses 2-bit symbols; sigma = 5
+ * adds a 1-bit plane for the fifth (largest) symbol to the packed text and to
+ * the rank dictionary -- with sigma = 5 the host tier,
+ * the sharded dictionary, insert_split and setbwte_merge are
+ * SETBWTE_E_UNSUPPORTED.  sigma > 5 -> SETBWTE_E_UNSUPPORTED.  Binds the
+ * current CUDA device and creates a private non-blocking stream.  *out
+ * receives the handle. */
 setbwte_status setbwte_create(const char* alphabet, setbwte_t* out);
 
 /* Release all device and host resources of h (NULL is a no-op). */
@@ -189,8 +194,6 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     Default 2^24.
  *   "profile"         1: time every kernel launch with CUDA events on the
  *                     handle's stream (reported by setbwte_stats); 0: off.
- *   "rank_ilp"        1 (default): one string per ComputeRanks thread; 2..4:
- *                     four strings per thread, their LF steps interleaved.
  *   "sort_lanes"      host threads (each with its own CUDA stream) running
  *                     ConstructSA of upcoming blocks ahead of the in-order
  *                     rank/insert stage (the stage pipeline of P:190-191):
@@ -223,13 +226,11 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     never (as for larger blocks: ComputeRanks records B_int
  *                     per slot instead).  Results are identical; the option
  *                     exists so both paths can be tested at small sizes.
- *   "kw1_min"         blocks of at least this many suffixes (default: none)
- *                     carry key word 1 with every element through the digit
- *                     passes (generated in one sequential pass), so resolving
- *                     a word-0 tie reads the element's own word-1 key instead
- *                     of two random text lookups.  Results identical; measured
- *                     slower on c3 (the wider scatter costs more than the
- *                     lookups it saves), hence off by default.
+ *   "gather_buckets"  how the g -> g_sa gather reads g: 1 (default) = in
+ *                     coalesced bucketed passes (L2-local g reads) when a
+ *                     block's g exceeds 96 MB, else one random read per
+ *                     suffix; 0 = always the random reads; 2 = always bucketed
+ *                     (test hook).  Results identical.
  *   "force_exchange"  1: (test hook) run the partitioned ComputeRanks and the
  *                     exchange step even with world == 1 (one slice; with a
  *                     communicator, one NCCL broadcast per exchange).

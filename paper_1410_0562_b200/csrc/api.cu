@@ -77,7 +77,7 @@ static void free_buf(DevBuf& b) { release(b); }
 
 std::vector<DevBuf*> SortScratch::bufs() {
     return {&sa0, &sa1, &k0, &k1, &segs_a, &segs_b, &small_a, &small_b, &chunks, &hist,
-            &ctr, &gtot, &groups, &kw1, &kw1b};
+            &ctr, &gtot, &groups};
 }
 
 void SortScratch::free_all() {
@@ -249,13 +249,12 @@ struct setbwte_s {
 
     // append scratch
     DevBuf in_bytes, in_off, text, term, nbit, slot_off, gfirst, bounds, err, small;
-    DevBuf saf, g, pos, bint, outbuf, bslot;
+    DevBuf saf, g, pos, bint, outbuf, bslot, gtmp;
     SortScratch sort[kMaxLanes];  // sort[0] also serves the inline (sort_lanes = 0) path
     Allocator user_alloc;         // setbwte_set_allocator (empty: cudaMalloc)
 
     // options
     uint64_t M = 1ull << 24;
-    int rank_ilp = 1;
     int sort_lanes = 3;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
     uint64_t lanes_checked_suf = 0;  // largest block the lane count was checked against free memory
     int lanes_checked_nl = 0;        // ... and the lane count that fitted
@@ -292,9 +291,10 @@ struct setbwte_s {
     std::vector<std::pair<uint64_t, void*>> ipc_open[kMaxShards];  // peer address -> opened mapping
     std::vector<void*> shard_retired;  // outgrown shard allocations (freed at destroy)
     Dict shard_dict = make_dict(nullptr);
-    SortOpts sopt;                           // options "sa_payload", "kw1_min"
+    SortOpts sopt;                           // option "sa_payload"
     SortPattern sort_pattern;                // recorded launch pattern (sopt.pattern)
     int g_width = 0;                         // option "g_width": 0 auto, 8 = always u64
+    int gather_mode = 0;                     // option "gather_buckets": 0 off, 1 auto, 2 forced
     setbwte_allgather_fn allgather = nullptr;
     void* allgather_ctx = nullptr;
     ncclComm_t nccl = nullptr;       // setbwte_set_comm: exchanges run in-library on NCCL
@@ -461,7 +461,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_dict(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
-                                          n_suf - (j1 - j0), g, gw, h->rank_ilp, bslot, bing, n5p));
+                                          n_suf - (j1 - j0), g, gw, bslot, bing, n5p));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
@@ -484,7 +484,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     const uint64_t steps = (slot_of[h->rank + 1] - slot_of[h->rank]) - (b - a);
     API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
                                       cur_dict(h), cur_sb(h), (const uint64_t*)h->d_C.p,
-                                      h->prepending ? 0 : h->m, steps, g, gw, h->rank_ilp, nullptr,
+                                      h->prepending ? 0 : h->m, steps, g, gw, nullptr,
                                       false, n5p));
     std::vector<uint64_t> bytes(P);
     for (int r = 0; r < P; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
@@ -767,9 +767,25 @@ setbwte_status rank_insert_stage(setbwte_t h, const Packed& pk, const BlockDesc&
     if (st != SETBWTE_OK) return st;
     // B_int := B(S_jk, SA_int), g_sa / pos and the superblock
     // slices of pos, fused
-    API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
-                               (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb, bslot,
-                               h->sopt.payload_limit, bing, pk.nbit));
+    const uint32_t gshift = gather_buckets_shift((uint32_t)n_suf, gw, h->gather_mode);
+    if (gshift) {
+        // g larger than L2: the bucketed gather (gather.cu)
+        uint8_t* gt;
+        API_CHECK(h, ensure(h->gtmp, gather_scratch_bytes((uint32_t)n_suf, gw), &gt));
+        GatherScratch ws;
+        ws.slot = reinterpret_cast<uint32_t*>(gt);
+        ws.gval = gt + ((4 * n_suf + 255) & ~255ull);
+        ws.rows = reinterpret_cast<uint32_t*>(gt + ((4 * n_suf + 255) & ~255ull) +
+                                              ((gw * n_suf + 255) & ~255ull));
+        API_CHECK(h, launch_gather_bucketed(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
+                                            (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb,
+                                            bslot, h->sopt.payload_limit, bing, pk.nbit, gshift,
+                                            ws));
+    } else {
+        API_CHECK(h, launch_gather(h->prof, h->stream, pk.text, pk.term, b.S0, saf, g,
+                                   (uint32_t)n_suf, pos, gw, bint, ib.sb_start, ib.nsb, bslot,
+                                   h->sopt.payload_limit, bing, pk.nbit));
+    }
     return insert_finish(h, ib, pos, gw, bint, n_suf, b.j1 - b.j0);
 }
 
@@ -1307,7 +1323,7 @@ static std::vector<DevBuf*> pooled_bufs(setbwte_t h) {
     std::vector<DevBuf*> v = {&h->d_code_of, &h->d_sym, &h->blk[0], &h->blk[1], &h->sb[0],
                               &h->sb[1], &h->d_C, &h->sb_tot, &h->in_bytes, &h->in_off, &h->text,
                               &h->term, &h->gfirst, &h->slot_off, &h->bounds, &h->err, &h->small,
-                              &h->saf, &h->g, &h->pos, &h->bslot, &h->bint, &h->outbuf,
+                              &h->saf, &h->g, &h->pos, &h->bslot, &h->bint, &h->outbuf, &h->gtmp,
                               &h->shard_ptrs, &h->stage_in, &h->stage_out, &h->nbit,
                               &h->nblk[0], &h->nblk[1], &h->nsb[0], &h->nsb[1], &h->ntot};
     for (SortScratch& ws : h->sort)
@@ -1721,9 +1737,6 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "sa_payload")) {
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->sopt.payload_limit = value ? kPayloadLimit : 0;
-    } else if (!strcmp(key, "kw1_min")) {
-        if (value == 0) return SETBWTE_E_INVALID_ARG;
-        h->sopt.kw1_min = value;
     } else if (!strcmp(key, "shard_dict")) {
         // 1: ranks share one address space; 2: separate processes (CUDA IPC)
         if (value > 2) return SETBWTE_E_INVALID_ARG;
@@ -1742,14 +1755,14 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
     } else if (!strcmp(key, "sort_lanes")) {
         if (value > (uint64_t)setbwte_s::kMaxLanes) return SETBWTE_E_INVALID_ARG;
         h->sort_lanes = (int)value;
+    } else if (!strcmp(key, "gather_buckets")) {
+        if (value > 2) return SETBWTE_E_INVALID_ARG;
+        h->gather_mode = (int)value;
     } else if (!strcmp(key, "force_exchange")) {
         // test hook: run the partitioned ComputeRanks + exchange path even
         // with world == 1 (one slice; with a communicator, one NCCL broadcast)
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->force_exchange = value != 0;
-    } else if (!strcmp(key, "rank_ilp")) {
-        if (value < 1 || value > 4) return SETBWTE_E_INVALID_ARG;
-        h->rank_ilp = (int)value;
     } else {
         return SETBWTE_E_INVALID_ARG;
     }

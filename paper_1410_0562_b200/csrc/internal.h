@@ -158,7 +158,6 @@ cudaError_t launch_slices_blocks(Profiler& prof, cudaStream_t s, const uint64_t*
 // sort.cu -- A1 ConstructSA (Sec.3).
 struct SortScratch {
     DevBuf sa0, sa1, k0, k1, segs_a, segs_b, small_a, small_b, chunks, hist, ctr, gtot, groups;
-    DevBuf kw1, kw1b;  // key word 1 in position order, ping-pong (large blocks only)
     void free_all();
     std::vector<DevBuf*> bufs();
 };
@@ -186,7 +185,7 @@ __host__ __device__ inline uint32_t sa_slot_mask(uint64_t n_suf, uint64_t limit 
     return sa_payload(n_suf, limit) ? (1u << kPayloadShift) - 1u : 0xFFFFFFFFu;
 }
 cudaError_t launch_strip_payload(cudaStream_t s, uint32_t* sa, uint32_t n, uint64_t limit);
-// per-handle sort options (setbwte_set_option "sa_payload", "kw1_min")
+// per-handle sort options (setbwte_set_option "sa_payload")
 // The launch pattern of one host-driven sort (per round: the segment count of
 // every size class), recorded once per handle from a block of >= 2^20
 // suffixes and replayed for blocks of about the same size without reading
@@ -207,7 +206,6 @@ struct SortPattern {
 };
 struct SortOpts {
     uint64_t payload_limit = kPayloadLimit;
-    uint64_t kw1_min = 1ull << 40;  // blocks from this size precompute key word 1 (off by default)
     SortPattern* pattern = nullptr;  // launch-pattern replay (null: every round host-driven)
 };
 
@@ -237,7 +235,7 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp, uint8_t* bslot = nullptr, bool bing = false,
+                                 int gw, uint8_t* bslot = nullptr, bool bing = false,
                                  const N5Dict* n5 = nullptr);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64).
 // Blocks without the SA payload get B_int from ComputeRanks: bslot (one byte
@@ -256,6 +254,25 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           uint64_t* sb_start = nullptr, uint64_t nsb = 0,
                           const uint8_t* bslot = nullptr, uint64_t payload_limit = kPayloadLimit,
                           bool bing = false, const uint32_t* nbit = nullptr);
+
+// gather.cu -- the g -> g_sa gather in bucketed passes (L2-local g reads).
+struct GatherScratch {
+    uint32_t* slot;  // n: SA slots partitioned by bucket
+    void* gval;      // n x gw: g of those slots
+    uint32_t* rows;  // 256 x tiles + 256: per-tile bucket offsets, bucket sizes
+};
+// scratch bytes for a block of n suffixes (GatherScratch carved from one buffer)
+size_t gather_scratch_bytes(uint32_t n, int gw);
+// log2 of the slots per bucket, or 0 = use the plain gather; mode 0 off,
+// 1 auto (g larger than L2), 2 forced (tests)
+uint32_t gather_buckets_shift(uint32_t n, int gw, int mode);
+cudaError_t launch_gather_bucketed(Profiler& prof, cudaStream_t s, const uint32_t* text,
+                                   const uint32_t* term, uint64_t slot_base, const uint32_t* sa,
+                                   const void* g, uint32_t n_suf, void* pos, int gw,
+                                   uint8_t* bint, uint64_t* sb_start, uint64_t nsb,
+                                   const uint8_t* bslot, uint64_t payload_limit, bool bing,
+                                   const uint32_t* nbit, uint32_t shift,
+                                   const GatherScratch& ws);
 
 // insert.cu -- A5 Insert + dictionary rebuild (Alg.1, Sec.5).
 cudaError_t launch_insert(Profiler& prof, cudaStream_t s, const Dict& in_blk, uint64_t n_in,

@@ -22,20 +22,27 @@
 namespace setbwte {
 
 template <class G>
-__device__ __forceinline__ void store4(G* dst, G a, G b, G c, G d);
+__device__ __forceinline__ void store4(G* dst, G a, G b, G c, G d, bool keep);
 template <>
 __device__ __forceinline__ void store4<uint32_t>(uint32_t* dst, uint32_t a, uint32_t b, uint32_t c,
-                                                 uint32_t d) {
-    // g is read back at random by the gather right after ComputeRanks: keep
-    // it in L2 (evict-last; measured +1 % on c2 over the default policy)
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst), "r"(a),
-                 "r"(b), "r"(c), "r"(d), "l"(pol));
+                                                 uint32_t d, bool keep) {
+    // g is read back at random by the gather right after ComputeRanks: when
+    // the block's g fits in L2 keep it there (evict-last; measured +1 % on
+    // c2).  A larger g must NOT be pinned: its evict-last lines would crowd
+    // out the bucketed gather's working set (gather.cu; measured 9 % L2 hits)
+    if (keep) {
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst), "r"(a),
+                     "r"(b), "r"(c), "r"(d), "l"(pol));
+    } else {
+        asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(a), "r"(b), "r"(c),
+                     "r"(d));
+    }
 }
 template <>
 __device__ __forceinline__ void store4<uint64_t>(uint64_t* dst, uint64_t a, uint64_t b, uint64_t c,
-                                                 uint64_t d) {
+                                                 uint64_t d, bool) {
     asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "l"(a), "l"(b), "l"(c),
                  "l"(d));
 }
@@ -54,7 +61,7 @@ __global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
     uint64_t j1, uint64_t slot_base, const D blk, const uint64_t* __restrict__ sb,
     const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g, uint8_t* __restrict__ bslot,
     bool bing, const uint32_t* __restrict__ nbit, const NBlk* __restrict__ nblk,
-    const uint64_t* __restrict__ nsb) {
+    const uint64_t* __restrict__ nsb, bool g_keep) {
     const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
     const uint64_t C4 = N5 ? Cd[4] : 0;
     for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
             const G a1 = (G)step(lp - 3);
             const G a0 = (G)step(lp - 4);
             lp -= 4;
-            store4<G>(g + lp, a0, a1, a2, a3);
+            store4<G>(g + lp, a0, a1, a2, a3, g_keep);
         }
         while (lp > l0) {
             --lp;
@@ -136,70 +143,19 @@ __global__ void __launch_bounds__(256, SB_RANK_MINB) compute_ranks_kernel(
     }
 }
 
-// ComputeRanks with K independent strings per thread, their LF steps
-// interleaved so K dictionary loads are in flight per thread.  For the host
-// tier: the dictionary is read zero-copy over PCIe, whose latency needs more
-// requests in flight than there are resident threads (one string each).
-template <class G, int K>
-__global__ void __launch_bounds__(256) compute_ranks_ilp_kernel(
-    const uint32_t* __restrict__ text, const uint64_t* __restrict__ slot_off, uint64_t j0,
-    uint64_t j1, uint64_t slot_base, const Dict blk, const uint64_t* __restrict__ sb,
-    const uint64_t* __restrict__ Cd, uint64_t m_ext, G* __restrict__ g) {
-    const uint64_t C0 = Cd[0], C1 = Cd[1], C2 = Cd[2], C3 = Cd[3];
-    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t jb = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; jb < j1;
-         jb += nthr * K) {
-        uint64_t i[K], lp[K], l0[K], wi[K];
-        uint32_t word[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint64_t j = jb + (uint64_t)k * nthr;
-            wi[k] = ~0ull;
-            word[k] = 0;
-            i[k] = m_ext;
-            if (j < j1) {
-                l0[k] = slot_off[j] - slot_base;
-                lp[k] = slot_off[j + 1] - 1 - slot_base;  // the terminator
-                g[lp[k]] = (G)m_ext;
-            } else {
-                l0[k] = lp[k] = 0;
-            }
-        }
-        for (;;) {
-            bool any = false;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                if (lp[k] > l0[k]) {
-                    any = true;
-                    const uint64_t q = --lp[k];
-                    const uint64_t p = q + slot_base;
-                    if ((p >> 4) != wi[k]) {
-                        wi[k] = p >> 4;
-                        word[k] = __ldg(text + wi[k]);
-                    }
-                    const uint32_t c = (word[k] >> (30 - 2 * (uint32_t)(p & 15))) & 3u;
-                    const uint64_t Cc = c == 0 ? C0 : c == 1 ? C1 : c == 2 ? C2 : C3;
-                    i[k] = Cc + (blk.P == 1 ? dict_rank(blk.ptr[0], sb, c, i[k])
-                                            : dict_rank(blk, sb, c, i[k]));
-                    g[q] = (G)i[k];
-                }
-            }
-            if (!any) break;
-        }
-    }
-}
-
 cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t* text,
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, int ilp, uint8_t* bslot, bool bing, const N5Dict* n5) {
+                                 int gw, uint8_t* bslot, bool bing, const N5Dict* n5) {
     if (j1 <= j0) return cudaSuccess;
     // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
     // superblock counter + g write + 0.25 B packed symbol; per string: 16 B
     // slot offsets + the terminator g.  Units = LF steps.
     const uint64_t nstr = j1 - j0;
     const double bytes = (40.25 + gw) * (double)n_steps + (16.0 + gw) * (double)nstr;
+    // keep g in L2 for the gather only while it fits (<= 96 MB; larger blocks use the bucketed gather)
+    const bool g_keep = (double)gw * (double)(n_steps + nstr) <= 96.0 * 1024 * 1024;
     if (n5) {
         // sigma = 5 (never sharded): the plain-array kernel with the N plane
         const unsigned grid = grid_for(nstr, 256, 1u << 20);
@@ -207,25 +163,12 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                       (compute_ranks_kernel<uint32_t, const Blk*, true><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
-                          (uint32_t*)g, bslot, false, n5->nbit, n5->nblk, n5->nsb)));
+                          (uint32_t*)g, bslot, false, n5->nbit, n5->nblk, n5->nsb, g_keep)));
         else
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                       (compute_ranks_kernel<uint64_t, const Blk*, true><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
-                          (uint64_t*)g, bslot, bing, n5->nbit, n5->nblk, n5->nsb)));
-        return cudaGetLastError();
-    }
-    if (ilp > 1 && !bslot && !bing) {
-        const unsigned gi = grid_for((nstr + 3) / 4, 256, 1u << 20);
-        if (gw == 4) {
-            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                      (compute_ranks_ilp_kernel<uint32_t, 4><<<gi, 256, 0, s>>>(
-                          text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g)));
-        } else {
-            SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
-                      (compute_ranks_ilp_kernel<uint64_t, 4><<<gi, 256, 0, s>>>(
-                          text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g)));
-        }
+                          (uint64_t*)g, bslot, bing, n5->nbit, n5->nblk, n5->nsb, g_keep)));
         return cudaGetLastError();
     }
     const unsigned grid = grid_for(nstr, 256, 1u << 20);
@@ -234,23 +177,23 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                       (compute_ranks_kernel<uint32_t, const Blk*, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
-                          (uint32_t*)g, bslot, false, nullptr, nullptr, nullptr)));
+                          (uint32_t*)g, bslot, false, nullptr, nullptr, nullptr, g_keep)));
         else
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                       (compute_ranks_kernel<uint32_t, Dict, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint32_t*)g,
-                          bslot, false, nullptr, nullptr, nullptr)));
+                          bslot, false, nullptr, nullptr, nullptr, g_keep)));
     } else {
         if (blk.P == 1)
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                       (compute_ranks_kernel<uint64_t, const Blk*, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk.ptr[0], sb, d_C, m_ext,
-                          (uint64_t*)g, bslot, bing, nullptr, nullptr, nullptr)));
+                          (uint64_t*)g, bslot, bing, nullptr, nullptr, nullptr, g_keep)));
         else
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
                       (compute_ranks_kernel<uint64_t, Dict, false><<<grid, 256, 0, s>>>(
                           text, slot_off, j0, j1, slot_base, blk, sb, d_C, m_ext, (uint64_t*)g,
-                          bslot, bing, nullptr, nullptr, nullptr)));
+                          bslot, bing, nullptr, nullptr, nullptr, g_keep)));
     }
     return cudaGetLastError();
 }

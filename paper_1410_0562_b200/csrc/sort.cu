@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "blockrank.cuh"
 #include "internal.h"
 
 namespace setbwte {
@@ -64,7 +65,9 @@ constexpr int kDigTile = kDigNt * kDigIpt;
 // BIT2..BIT16: 33..512 members whose unknown key bits fit in 16 (keys valid,
 // shift <= 8): one warp sorts 32*NIT packed (key bits, index) u32 values with a
 // register bitonic network.  SMALL: the other 33..512 segments (warp LSD radix).
-enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, NCLASS };
+// LOCALD: 513..4096 members with valid keys (one digit pass left in the word):
+// the whole digit pass of the segment in one CTA (local_digit_kernel).
+enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, LOCALD, NCLASS };
 // misc counters
 enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_N };
 
@@ -92,7 +95,6 @@ struct Bufs {
     const uint32_t* term;
     uint64_t base;
     uint32_t smask;  // slot bits of an SA entry (sa_slot_mask); ~0 without payload
-    uint32_t* key1[2];  // key word 1 in position order (large blocks), or null
     uint32_t n;         // suffixes of the block (debug bounds checks)
     const uint32_t* nbit;  // sigma = 5: code-4 plane of the text (common.cuh), else null
     uint32_t ksyms;        // symbols per key word: kKeySyms (14) or kKeySyms5 (9)
@@ -121,15 +123,9 @@ __device__ __forceinline__ uint32_t meta_shift(uint32_t m) { return m & 0xFF; }
 __device__ __forceinline__ uint32_t meta_buf(uint32_t m) { return (m >> 8) & 1; }
 __device__ __forceinline__ uint32_t meta_kv(uint32_t m) { return (m >> 9) & 1; }
 __device__ __forceinline__ uint32_t meta_iota(uint32_t m) { return (m >> 10) & 1; }
-// k1bad: the segment's elements were reordered without their key-1 words
-__device__ __forceinline__ uint32_t meta_k1bad(uint32_t m) { return (m >> 11) & 1; }
 __device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint32_t kv,
-                                              uint32_t iota = 0, uint32_t k1bad = 0) {
-    return shift | (buf << 8) | (kv << 9) | (iota << 10) | (k1bad << 11);
-}
-// key word 1 of the element at position pos of buffer buf, when carried
-__device__ __forceinline__ bool k1_ok(const Bufs& B, uint32_t meta) {
-    return B.key1[0] != nullptr && !meta_k1bad(meta);
+                                              uint32_t iota = 0) {
+    return shift | (buf << 8) | (kv << 9) | (iota << 10);
 }
 __host__ __device__ __forceinline__ int class_of(const Seg& c) {
     if (c.len <= kTiny) return TINY;
@@ -139,45 +135,14 @@ __host__ __device__ __forceinline__ int class_of(const Seg& c) {
         return SMALL;
     }
     // > 512 with valid keys: one more digit pass is cheaper than a CTA-wide
-    // sort (measured on c3's ~2048-member second-pass buckets)
-    if ((c.meta >> 9) & 1) return LARGE;
+    // sort (measured on c3's ~2048-member second-pass buckets); up to one
+    // tile it runs inside one CTA (no histogram / scan kernels)
+    if ((c.meta >> 9) & 1) return c.len <= kCapM ? LOCALD : LARGE;
     return c.len <= 1024 ? MED1K : c.len <= 2048 ? MED2K : c.len <= kCapM ? MEDIUM : LARGE;
 }
 __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
     const int k = class_of(c);
     out.seg[k][atomicAdd(out.cnt + k, 1u)] = c;
-}
-
-// Lanes of the warp holding the same NB-bit digit (a ballot per bit: short
-// fixed latency, unlike MATCH.ANY whose result latency serialised the ranking
-// loops -- ncu, profiles/).
-template <int NB>
-__device__ __forceinline__ uint32_t peers_of(uint32_t d) {
-    // per bit: test into a predicate, ballot it, replicate the lane's bit
-    // (selp), and fold  diff |= bal ^ rep  in one 3-input LOP3 (LUT 0xF6 =
-    // a | (b ^ c)); peers = lanes whose digit has no differing bit = ~diff
-    uint32_t diff = 0u;
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-        asm("{\n\t"
-            ".reg .pred p;\n\t"
-            ".reg .b32 t, bal, rep;\n\t"
-            "and.b32 t, %1, %2;\n\t"
-            "setp.ne.u32 p, t, 0;\n\t"
-            "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
-            "selp.b32 rep, 0xffffffff, 0, p;\n\t"
-            "lop3.b32 %0, %0, bal, rep, 0xF6;\n\t"
-            "}"
-            : "+r"(diff)
-            : "r"(d), "r"(1u << b));
-    }
-    return ~diff;
-}
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-    uint32_t m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -261,87 +226,6 @@ __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint3
         ++word;
     }
     return slot;
-}
-
-// ---------------------------------------------------------------------------
-// Block-level stable ranking of up to NT*IPT items by an 8-bit digit.
-// Item `it` of a thread is tile element warp*32*IPT + it*32 + lane; invalid
-// items carry digit 0x100.  On return dest[it] is the item's position in the
-// tile stably sorted by digit, dstart[d] the first position of digit d
-// (dstart[256] = number of valid items).  wcnt: NW*256 u32 of shared memory.
-// ---------------------------------------------------------------------------
-template <int NT, int IPT>
-__device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], uint32_t (&dest)[IPT],
-                                           uint32_t* wcnt, uint32_t* dstart, uint32_t* tmp) {
-    constexpr int NW = NT / 32;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t i = tid; i < NW * 256; i += NT) wcnt[i] = 0;
-    __syncthreads();
-    uint32_t* mine = wcnt + warp * 256;
-    // all MATCH.ANY first (independent, their latency overlaps), then the
-    // in-order per-warp counter updates: every lane reads its digit's counter
-    // (broadcast among peers), the lowest peer writes it back advanced.
-    // peers by ballots (MATCH.ANY measured slower here: MIO-pipe throughput);
-    // a full tile has no invalid items and needs only the 8 digit bits
-    uint32_t peers[IPT];
-    const bool full = __all_sync(0xFFFFFFFFu, dig[IPT - 1] < 256);
-#pragma unroll
-    for (int it = 0; it < IPT; ++it) peers[it] = full ? peers_of<8>(dig[it]) : peers_of<9>(dig[it]);
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-        const uint32_t d = dig[it];
-        const bool ok = d < 256;
-        const uint32_t b = ok ? mine[d] : 0u;
-        dest[it] = b + __popc(peers[it] & lt);
-        if (ok && (peers[it] & lt) == 0) mine[d] = b + __popc(peers[it]);
-        __syncwarp();
-    }
-    __syncthreads();
-    // per digit: prefix over the warps, then an exclusive scan over the 256
-    // digits; thread tid owns digits [tid*DPT, tid*DPT+DPT) (NT >= 256: DPT = 1)
-    constexpr int DPT = NT >= 256 ? 1 : 256 / NT;
-    constexpr int NACT = NT >= 256 ? 256 : NT;  // threads owning digits
-    uint32_t tot[DPT];
-    uint32_t local = 0;
-    if (tid < NACT) {
-#pragma unroll
-        for (int q = 0; q < DPT; ++q) {
-            const uint32_t d = tid * DPT + q;
-            uint32_t acc = 0;
-            for (int w = 0; w < NW; ++w) {
-                const uint32_t t = wcnt[w * 256 + d];
-                wcnt[w * 256 + d] = acc;
-                acc += t;
-            }
-            tot[q] = acc;
-            local += acc;
-        }
-    }
-    uint32_t incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-    }
-    if (lane == 31 && tid < NACT) tmp[warp] = incl;
-    __syncthreads();
-    if (tid < NACT) {
-        uint32_t run = incl - local;
-        for (uint32_t w = 0; w < warp; ++w) run += tmp[w];
-#pragma unroll
-        for (int q = 0; q < DPT; ++q) {
-            dstart[tid * DPT + q] = run;
-            run += tot[q];
-        }
-        if (tid == NACT - 1) dstart[256] = run;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-        const uint32_t d = dig[it];
-        if (d < 256) dest[it] += dstart[d] + mine[d];
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -565,8 +449,7 @@ __global__ void __launch_bounds__(kDigNt, SB_HIST_MINB) digit_hist_kernel(Lists 
                     key[u] = 0;
                     if (p < ch.end) {
                         const uint32_t sl = meta_iota(s.meta) ? p : __ldg(S + p);
-                        key[u] = (s.word == 1 && k1_ok(B, s.meta)) ? B.key1[buf][p]
-                                                                    : key_of(B, sl, s.word);
+                        key[u] = key_of(B, sl, s.word);
                         K[p] = key[u];
                     }
                 }
@@ -671,10 +554,10 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
                 c.len = total;
                 if (shift == 0) {
                     c.word = s.word + 1;
-                    c.meta = make_meta(24, cbuf, 0, ciota, meta_k1bad(s.meta));
+                    c.meta = make_meta(24, cbuf, 0, ciota);
                 } else {
                     c.word = s.word;
-                    c.meta = make_meta(shift - 8, cbuf, 1, ciota, meta_k1bad(s.meta));
+                    c.meta = make_meta(shift - 8, cbuf, 1, ciota);
                 }
                 cls = class_of(c);
                 local = atomicAdd(&ccount[cls], 1u);
@@ -710,9 +593,8 @@ struct Tile {
     uint32_t c, t0, end;  // chunk, first element, chunk end
 };
 
-// IPT items per thread (tile = kDigNt * IPT); K1: the segment data also
-// carries key word 1 (B.key1), moved with the key and the slot
-template <int IPT, bool K1>
+// IPT items per thread (tile = kDigNt * IPT)
+template <int IPT>
 __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     Lists in, const SegX* __restrict__ segx, const Chunk* __restrict__ chunks, const uint32_t* misc,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gtot,
@@ -724,9 +606,7 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
     uint2* s_kv = reinterpret_cast<uint2*>(wcnt + NW * 256);  // TILE (key, slot)
     uint32_t* s_ink = reinterpret_cast<uint32_t*>(s_kv + TILE);  // TILE: next tile's keys
     uint32_t* s_ins = s_ink + TILE;                              // TILE: next tile's slots
-    uint32_t* s_in1 = s_ins + TILE;                              // TILE (K1): next tile's word-1 keys
-    uint32_t* s_k1 = s_in1 + (K1 ? TILE : 0);                    // TILE (K1): staged word-1 keys
-    uint32_t* dstart = s_k1 + (K1 ? TILE : 0);                   // 257
+    uint32_t* dstart = s_ins + TILE;                             // 257
     uint32_t* run_base = dstart + 260;                        // 256
     uint32_t* off = run_base + 256;                           // 256: run_base - dstart
     uint32_t* tmp = off + 256;                                // 32
@@ -762,7 +642,6 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
         const uint32_t tn = min((uint32_t)TILE, t.end - t.t0);
         const uint32_t* K = B.key[buf] + t.t0;
         const uint32_t* S = B.sa[buf] + t.t0;
-        const uint32_t* K1s = K1 ? B.key1[buf] + t.t0 : nullptr;
         const bool iota = meta_iota(s.meta);
 #pragma unroll
         for (int it = 0; it < IPT; ++it) {
@@ -770,7 +649,6 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             if (e < tn) {
                 cp_async4(s_ink + e, K + e, pol_ef);
                 if (!iota) cp_async4(s_ins + e, S + e, pol_ef);
-                if (K1) cp_async4(s_in1 + e, K1s + e, pol_ef);
             }
         }
         cp_async_commit();
@@ -801,10 +679,9 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
         }
         uint32_t* S2 = B.sa[1 - buf];
         uint32_t* K2 = B.key[1 - buf];
-        uint32_t* K12 = K1 ? B.key1[1 - buf] : nullptr;
         const uint32_t t0 = cur.t0;
         const uint32_t tn = min((uint32_t)TILE, cur.end - t0);
-        uint32_t key[IPT], slot[IPT], dig[IPT], dest[IPT], k1v[K1 ? IPT : 1];
+        uint32_t key[IPT], slot[IPT], dig[IPT], dest[IPT];
         cp_async_wait_all();
 #pragma unroll
         for (int it = 0; it < IPT; ++it) {
@@ -812,7 +689,6 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
             const bool valid = e < tn;
             key[it] = valid ? s_ink[e] : 0u;
             slot[it] = valid ? (iota ? t0 + e : s_ins[e]) : 0u;
-            if (K1) k1v[K1 ? it : 0] = valid ? s_in1[e] : 0u;
             dig[it] = valid ? ((key[it] >> shift) & 0xFFu) : 0x100u;
         }
         if (iota && B.smask != 0xFFFFFFFFu) {
@@ -854,7 +730,6 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
         for (int it = 0; it < IPT; ++it)
             if (dig[it] < 256) {
                 s_kv[dest[it]] = make_uint2(key[it], slot[it]);
-                if (K1) s_k1[dest[it]] = k1v[K1 ? it : 0];
             }
         __syncthreads();
         // coalesced write-out: consecutive tile positions of one digit go to
@@ -871,21 +746,117 @@ __global__ void __launch_bounds__(kDigNt, 2) digit_scatter_kernel(
 #if SB_SCATTER_L2
                 S2[gp] = kv.y;
                 K2[gp] = kv.x;
-                if (K1) K12[gp] = s_k1[i];
 #else
                 __stcs(S2 + gp, kv.y);
                 __stcs(K2 + gp, kv.x);
-                if (K1) __stcs(K12 + gp, s_k1[i]);
 #endif
             }
         }
     }
 }
 
-template <int IPT, bool K1>
+template <int IPT>
 constexpr size_t scatter_smem() {
-    return (size_t)(kDigNt / 32) * 256 * 4 + (K1 ? 6 : 4) * (size_t)(kDigNt * IPT) * 4 + 260 * 4 +
+    return (size_t)(kDigNt / 32) * 256 * 4 + 4 * (size_t)(kDigNt * IPT) * 4 + 260 * 4 +
            2 * 256 * 4 + 32 * 4 + 256 + 16;
+}
+
+// ---------------------------------------------------------------------------
+// LOCALD: the digit pass of one segment of 513..4096 members with valid keys,
+// entirely in one CTA -- the segment is one tile, so the tile's stable ranks
+// ARE the segment's digit histogram and offsets: no chunk / histogram / scan
+// kernels, one read and one write of (key, slot).  Same outputs as the
+// LARGE path: resolved buckets (one member, or equal keys that end inside
+// the word) go to their final SA positions; the others become child
+// segments, keyed on the next digit (or the next word at shift 0).
+// ---------------------------------------------------------------------------
+constexpr int kLocNt = 512;
+constexpr int kLocIpt = 8;
+static_assert(kLocNt * kLocIpt == (int)kCapM, "one tile per LOCALD segment");
+
+constexpr size_t local_digit_smem() {
+    return (size_t)(kLocNt / 32) * 256 * 4 + 2 * (size_t)kCapM * 8 + 260 * 4 + 32 * 4 + 256 + 64;
+}
+
+__global__ void __launch_bounds__(kLocNt, 2) local_digit_kernel(Lists in, Lists out, Bufs B,
+                                                                 uint32_t* misc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);                   // NW*256
+    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + (kLocNt / 32) * 256);       // kCapM: sorted
+    uint2* s_in = s_kv + kCapM;                                               // kCapM: as loaded
+    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_in + kCapM);             // 257
+    uint32_t* tmp = dstart + 260;                                             // 32
+    uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);                      // 256
+    __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
+    const uint32_t n = in.cnt[LOCALD];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
+        const Seg s = in.seg[LOCALD][si];
+        const uint32_t shift = meta_shift(s.meta), buf = meta_buf(s.meta);
+        const bool iota = meta_iota(s.meta);
+        const uint32_t* S = B.sa[buf] + s.start;
+        const uint32_t* K = B.key[buf] + s.start;
+        // (key, slot) wait in shared memory while the digits are ranked
+        // (registers hold only digits and ranks: no spills at 2 CTAs/SM)
+        uint32_t dig[kLocIpt], dest[kLocIpt];
+#pragma unroll
+        for (int it = 0; it < kLocIpt; ++it) {
+            const uint32_t e = warp * (32 * kLocIpt) + it * 32 + lane;
+            const bool valid = e < s.len;
+            const uint32_t key = valid ? __ldcs(K + e) : 0u;
+            const uint32_t slot = valid ? (iota ? sa_entry(B, s.start + e) : __ldcs(S + e)) : 0u;
+            s_in[e] = make_uint2(key, slot);
+            dig[it] = valid ? ((key >> shift) & 0xFFu) : 0x100u;
+        }
+        if (tid < NCLASS) ccount[tid] = 0;
+        block_rank<kLocNt, kLocIpt>(dig, dest, wcnt, dstart, tmp);
+        // per digit: sieve decision and child segment (digit_scan's rules)
+        int cls = -1;
+        uint32_t local = 0;
+        Seg c;
+        if (tid < 256) {
+            const uint32_t d = tid;
+            const uint32_t total = dstart[d + 1] - dstart[d];
+            const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < B.ksyms);
+            fin[d] = resolved ? 1 : 0;
+            if (total > 0 && !resolved) {
+                c.start = s.start + dstart[d];
+                c.len = total;
+                if (shift == 0) {
+                    c.word = s.word + 1;
+                    c.meta = make_meta(24, 1u - buf, 0);
+                } else {
+                    c.word = s.word;
+                    c.meta = make_meta(shift - 8, 1u - buf, 1);
+                }
+                cls = class_of(c);
+                local = atomicAdd(&ccount[cls], 1u);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kLocIpt; ++it)
+            if (dig[it] < 256) s_kv[dest[it]] = s_in[warp * (32 * kLocIpt) + it * 32 + lane];
+        __syncthreads();
+        if (tid < NCLASS && ccount[tid]) cbase[tid] = atomicAdd(out.cnt + tid, ccount[tid]);
+        if (tid == 0) atomicAdd(misc + M_ACTIVE, s.len);
+        __syncthreads();
+        if (cls >= 0) out.seg[cls][cbase[cls] + local] = c;
+        // write-out in segment order: finished buckets to the final SA, the
+        // others (key, slot) into the other buffer
+        uint32_t* S2 = B.sa[1 - buf] + s.start;
+        uint32_t* K2 = B.key[1 - buf] + s.start;
+        for (uint32_t i = tid; i < s.len; i += kLocNt) {
+            const uint2 kv = s_kv[i];
+            if (fin[(kv.x >> shift) & 0xFFu]) {
+                SB_ASSERT(s.start + i < B.n);
+                __stcs(B.saf + s.start + i, kv.y);
+            } else {
+                S2[i] = kv.y;
+                K2[i] = kv.x;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -899,8 +870,7 @@ constexpr uint32_t kTinyPerWarp = 32;  // list entries per warp, packed into sha
 // this word with 14 real symbols and `run` the first lane of their tie run.
 __device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint32_t grp,
                                                 uint32_t key, uint32_t rb, bool& tie,
-                                                uint32_t& run, uint32_t& x, uint32_t ksyms) {
-    // x: a per-element value permuted along with the slot
+                                                uint32_t& run, uint32_t ksyms) {
     const uint32_t lane = threadIdx.x & 31;
     const bool valid = lane < L;
     const uint32_t rmask = (1u << rb) - 1u;
@@ -922,7 +892,6 @@ __device__ __forceinline__ uint32_t warp_sort16(uint32_t slot, uint32_t L, uint3
     const uint32_t src = v & 31u;
     const uint32_t s2 = __shfl_sync(0xFFFFFFFFu, slot, src);
     const uint32_t k2 = __shfl_sync(0xFFFFFFFFu, key, src);
-    x = __shfl_sync(0xFFFFFFFFu, x, src);
     const uint32_t hi = v >> 5;
     const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
     const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, hi, 1);
@@ -947,8 +916,9 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
         // pack consecutive segments into the 32 lanes; each lane remembers its
         // segment's output position, start word and key (a segment keeps its
         // lanes through the sort: the composite sorts by group first)
-        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0, rb = 0, k1 = 0;
-        bool mine = false, kv = false, fast = true, k1v = false;
+        uint32_t lb = 0, dst = 0, word = 0, key = 0, slot = 0, grp = 0, elems = 0, rb = 0;
+        uint32_t bf = 0;
+        bool mine = false, kv = false, fast = true;
         // all of the warp's list entries in one coalesced load (lane l holds
         // entry i0+l); the packing loop below broadcasts them with shuffles, so
         // it never waits on memory
@@ -965,17 +935,20 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
             }
             if (i == i1 || lb + sg.len > 32) {
                 if (lb) {
+                    // the packed group's members, all loads in flight at once
+                    // (per-segment loads serialised their latencies)
+                    if (mine) {
+                        slot = B.sa[bf][dst];
+                        key = kv ? B.key[bf][dst] : 0u;
+                    }
                     uint32_t r;
                     if (__all_sync(0xFFFFFFFFu, fast || lane >= lb)) {
                         bool tie;
                         uint32_t run;
-                        uint32_t k1p = k1;
-                        r = warp_sort16(slot, lb, grp, key, rb, tie, run, k1p, B.ksyms);
-                        // ties continue on word+1; word 1 comes from the carried
-                        // key-1 words (permuted with the slots; the flag is the
-                        // same for every lane of a segment)
+                        r = warp_sort16(slot, lb, grp, key, rb, tie, run, B.ksyms);
+                        // ties continue on word+1 (key words from the text)
                         if (__any_sync(0xFFFFFFFFu, tie))
-                            r = warp_finish(r, lb, word + 1, k1p, k1v && word == 0, B, run, tie);
+                            r = warp_finish(r, lb, word + 1, 0u, false, B, run, tie);
                     } else {
                         r = warp_finish(slot, lb, word, key, kv, B, grp);
                     }
@@ -989,19 +962,11 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
             }
             if (lane >= lb && lane < lb + sg.len) {
                 const uint32_t e = lane - lb;
-                const uint32_t bf = meta_buf(sg.meta);
+                bf = meta_buf(sg.meta);
                 mine = true;
                 dst = sg.start + e;
                 word = sg.word;
                 kv = meta_kv(sg.meta);
-                slot = B.sa[bf][dst];
-                key = kv ? B.key[bf][dst] : 0u;
-                k1v = k1_ok(B, sg.meta) && (sg.word == 0 || (sg.word == 1 && !kv));
-                k1 = k1v ? B.key1[bf][dst] : 0u;
-                if (sg.word == 1 && !kv && k1v) {
-                    key = k1;  // the word-1 key of a segment at word 1
-                    kv = true;
-                }
                 grp = lb;
                 rb = meta_shift(sg.meta) + 8;
                 fast = kv && meta_shift(sg.meta) <= 8;
@@ -1065,7 +1030,7 @@ __device__ __forceinline__ void warp_tail(const uint2* buf, const Seg& s, const 
                     lb += Lr;
                 } else {
                     for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = buf[rs + q].y;
-                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0, 0, 1)});
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0, 0)});
                 }
             }
         }
@@ -1227,19 +1192,14 @@ __global__ void __launch_bounds__(kWarpCta * 32, SB_BIT_MINB) bitonic_kernel(Lis
                     }
                     const uint32_t rs = tl[b] & 0xFFFFu;
                     for (uint32_t q = lane; q < Lr; q += 32) B.sa[bid][s.start + rs + q] = sl32[rs + q];
-                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0, 0, 1)});
+                    if (lane == 0) emit(out, Seg{s.start + rs, Lr, s.word + 1, make_meta(24, bid, 0, 0)});
                     b += Lr;
                     continue;
                 }
                 const uint32_t e = te & 0xFFFFu;
                 const uint32_t grp = 31u - __clz(starts & (0xFFFFFFFFu >> (31 - lane)));
                 uint32_t sl = lane < nb ? sl32[e] : 0u;
-                // word 1 from the carried key-1 words (the element's position
-                // before this sort: bits 16.. of its tie entry)
-                const bool k1 = s.word == 0 && k1_ok(B, s.meta);
-                const uint32_t kk =
-                    (k1 && lane < nb) ? B.key1[bid][s.start + ((te >> 16) & 0x7FFFu)] : 0u;
-                sl = warp_finish(sl, nb, s.word + 1, kk, k1, B, grp);
+                sl = warp_finish(sl, nb, s.word + 1, 0u, false, B, grp);
                 __syncwarp();
                 SB_ASSERT(lane >= nb || (e < L && s.start + e < B.n));
                 if (lane < nb) B.saf[s.start + e] = sl;
@@ -1278,9 +1238,7 @@ __global__ void __launch_bounds__(kWarpCta * 32) warp_sort_kernel(Lists in, List
             const uint32_t e = it * 32 + lane;
             if ((uint32_t)it < nit && e < L) {
                 slot[it] = S[s.start + e];
-                key[it] = kv ? B.key[bid][s.start + e]
-                             : (s.word == 1 && k1_ok(B, s.meta)) ? B.key1[bid][s.start + e]
-                                                                 : key_of(B, slot[it], s.word);
+                key[it] = kv ? B.key[bid][s.start + e] : key_of(B, slot[it], s.word);
             }
         }
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1476,9 +1434,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
         for (uint32_t i = tid; i < len; i += NT) {
             const uint32_t sl = S[s.start + i];
             slotA[i] = sl;
-            keyA[i] = kv ? B.key[buf][s.start + i]
-                         : (s.word == 1 && k1_ok(B, s.meta)) ? B.key1[buf][s.start + i]
-                                                             : key_of(B, sl, s.word);
+            keyA[i] = kv ? B.key[buf][s.start + i] : key_of(B, sl, s.word);
         }
         __syncthreads();
         const uint32_t top = kv ? meta_shift(s.meta) : 24u;
@@ -1561,7 +1517,7 @@ __global__ void __launch_bounds__(NT) local_kernel(Lists in, Lists out, int cls,
                 if (lane < rr.y) B.saf[s.start + rr.x + lane] = sl;
             } else {
                 for (uint32_t q = lane; q < rr.y; q += 32) S[s.start + rr.x + q] = slotA[rr.x + q];
-                if (lane == 0) emit(out, Seg{s.start + rr.x, rr.y, s.word + 1, make_meta(24, buf, 0, 0, 1)});
+                if (lane == 0) emit(out, Seg{s.start + rr.x, rr.y, s.word + 1, make_meta(24, buf, 0, 0)});
             }
         }
         __syncthreads();
@@ -1592,7 +1548,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     const size_t n = n_suf;
     const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
                                 n / 257 + 1, n / 33 + 1,   n / 513 + 1,  n / 1025 + 1,
-                                n / 2049 + 1, n / (kCapS + 1) + 1};  // LARGE: > 512 (kv)
+                                n / 2049 + 1, n / (kCapM + 1) + 2,   // LARGE: > 4096
+                                n / (kCapS + 1) + 1};                // LOCALD: 513..4096 (kv)
     const size_t max_large = cap[LARGE];
     const size_t max_chunks = n / kMinChunk + max_large + 1;
     uint32_t *sa0, *sa1, *k0, *k1, *hist, *ctr;
@@ -1630,12 +1587,6 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         A.cnt = ctr;
         Bl.cnt = ctr + NCLASS;
     }
-    const bool kw1 = n >= opts.kw1_min && !nbit;  // sigma = 5: no carried key word 1
-    if (kw1) {
-        uint32_t* kw1;
-        SB_CHECK(ensure(ws.kw1, n + 16, &kw1));
-        SB_CHECK(ensure(ws.kw1b, n + 16, &kw1));
-    }
     if (reserve_only) return cudaSuccess;
     Bufs B;
     B.sa[0] = sa0;
@@ -1647,7 +1598,6 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     B.term = term;
     B.base = slot_base;
     B.smask = sa_slot_mask(n_suf, opts.payload_limit);
-    B.key1[0] = B.key1[1] = nullptr;
     B.n = n_suf;
     B.nbit = nbit;
     B.ksyms = nbit ? (uint32_t)kKeySyms5 : (uint32_t)kKeySyms;
@@ -1660,30 +1610,15 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m1));
     SB_CHECK(cudaFuncSetAttribute(local_kernel<2048, 256>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m2));
-    constexpr size_t sm_d = scatter_smem<kDigIpt, false>();
-    constexpr size_t sm_d1 = scatter_smem<4, true>();
+    constexpr size_t sm_d = scatter_smem<kDigIpt>();
+    constexpr size_t sm_ld = local_digit_smem();
+    SB_CHECK(cudaFuncSetAttribute(local_digit_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ld));
     SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
-    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<kDigIpt, false>,
+    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<kDigIpt>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d));
-    SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<4, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_d1));
 
-    if (kw1) {
-        // large blocks carry key word 1 with every element through the digit
-        // passes (B.key1, position order): resolving a word-0 tie then reads
-        // the element's own word-1 key, not two random text lookups.  Key
-        // word 1 of slot i is key word 0 of slot i + 14.
-        uint32_t *k1a, *k1b;
-        SB_CHECK(ensure(ws.kw1, n + 16, &k1a));  // reserved by sort_reserve
-        SB_CHECK(ensure(ws.kw1b, n + 16, &k1b));
-        SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
-                  keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(
-                      text, term, slot_base + kKeySyms, n_suf, k1a));
-        SB_CHECK(cudaGetLastError());
-        B.key1[0] = k1a;
-        B.key1[1] = k1b;
-    }
     if (n <= kCapM && !nbit) {
         SB_LAUNCH(prof, s, "sort_keygen", 4.375 * n, n,
                   keygen_kernel<<<grid_for((n + 15) / 16, 256, 148u * 16u), 256, 0, s>>>(
@@ -1752,6 +1687,12 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                                                   sm_m2, s>>>(in, out, MED2K, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
+        if (cnt[LOCALD]) {
+            SB_LAUNCH(prof, s, "sort_local_digit", 0, 0,
+                      (local_digit_kernel<<<std::min<uint32_t>(cnt[LOCALD], 148u * 2u * 4u),
+                                            kLocNt, sm_ld, s>>>(in, out, B, misc)));
+            SB_CHECK(cudaGetLastError());
+        }
         if (cnt[MEDIUM]) {
             SB_LAUNCH(prof, s, "sort_medium", 0, 0,
                       (local_kernel<kCapM, kNtM><<<std::min<uint32_t>(cnt[MEDIUM], 148u * 3u),
@@ -1774,15 +1715,9 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                       digit_scan_kernel<<<std::min<uint32_t>(cnt[LARGE], 148u * 8u), 256, 0, s>>>(
                           in, out, segx, gtot, dbase, B.ksyms));
             SB_CHECK(cudaGetLastError());
-            if (B.key1[0]) {
-                SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
-                          (digit_scatter_kernel<4, true><<<g_dig, kDigNt, sm_d1, s>>>(
-                              in, segx, chunks, misc, hist, gtot, dbase, B)));
-            } else {
-                SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
-                          (digit_scatter_kernel<kDigIpt, false><<<g_dig, kDigNt, sm_d, s>>>(
-                              in, segx, chunks, misc, hist, gtot, dbase, B)));
-            }
+            SB_LAUNCH(prof, s, "digit_scatter", 0, 0,
+                      (digit_scatter_kernel<kDigIpt><<<g_dig, kDigNt, sm_d, s>>>(
+                          in, segx, chunks, misc, hist, gtot, dbase, B)));
             SB_CHECK(cudaGetLastError());
         }
         SB_LAUNCH(prof, s, "sort_ctl", 0, 0,

@@ -528,36 +528,32 @@ def test_c1_u64_g_without_payload(SetBWTE, c1):
 
 @pytest.mark.parametrize("payload", [0, 1])
 @pytest.mark.parametrize("kind", ["all_A", "AC_repeat", "staircase", "uniform"])
-def test_precomputed_word1_keys(SetBWTE, kind, payload):
-    """Blocks that precompute key word 1 (forced with kw1_min = 1) on
-    tie-heavy inputs; results must not change."""
+def test_tie_heavy_small_blocks(SetBWTE, kind, payload):
+    """Tie-heavy inputs in small blocks (many key words per suffix), with and
+    without the SA payload."""
     if kind == "uniform":
         d, o = synth.random_set(15000, max_m=64, max_len=80)
     else:
         d, o = synth.adversarial(kind, 40, 70)
     idx = SetBWTE(A, block_suffixes=500)
-    idx.set_option("kw1_min", 1)
     idx.set_option("sa_payload", payload)
     idx.append(d, o)
     assert idx.bwt() == oracle.bwt(A, d, o)
 
 
-def test_genome_precomputed_word1_keys(SetBWTE):
+def test_genome_one_block(SetBWTE):
     d, o = synth.genome_sampled(3000, 120, 60000, seed=5)
     idx = SetBWTE(A, block_suffixes=90000)
-    idx.set_option("kw1_min", 1)
     idx.append(d, o)
     assert idx.bwt() == oracle.bwt(A, d, o, threads=None)
 
 
 @pytest.mark.parametrize("seed", range(12))
-def test_random_sets_carried_word1(SetBWTE, seed):
-    """Key word 1 carried through the digit passes (kw1_min = 1) on random
-    sets with small blocks, both SA layouts and g widths."""
+def test_random_sets_small_blocks(SetBWTE, seed):
+    """Random sets with small blocks, both SA layouts and g widths."""
     d, o = synth.random_set(16000 + seed, max_m=64, max_len=90, alphabet=["ACGT", "AC", "A"][seed % 3])
     rng = np.random.default_rng(seed)
     idx = SetBWTE(A, block_suffixes=int(rng.integers(40, 3000)))
-    idx.set_option("kw1_min", 1)
     idx.set_option("sa_payload", seed % 2)
     if seed % 4 == 3:
         idx.set_option("g_width", 8)
@@ -565,24 +561,26 @@ def test_random_sets_carried_word1(SetBWTE, seed):
     assert idx.bwt() == oracle.bwt(A, d, o)
 
 
-def test_c1_carried_word1(SetBWTE, c1):
+def test_c1_one_and_four_blocks(SetBWTE, c1):
     d, o, want = c1
     for M in (25250, 101000):
         idx = SetBWTE(A, block_suffixes=M)
-        idx.set_option("kw1_min", 1)
         idx.append(d, o)
         assert idx.bwt() == want
 
 
 @pytest.mark.parametrize("budget", [1 << 40, 1])
 @pytest.mark.parametrize("seed", range(4))
-def test_rank_ilp(SetBWTE, seed, budget):
-    """ComputeRanks with 4 interleaved strings per thread (rank_ilp), HBM and
-    host-tier dictionaries."""
+def test_random_sets_hbm_and_host_tier(SetBWTE, seed, budget):
+    """Random sets, HBM and host-tier dictionaries (options rank_ilp / kw1_min
+    are retired: they must be rejected)."""
     d, o = synth.random_set(17000 + seed, max_m=64, max_len=70)
     rng = np.random.default_rng(seed)
     idx = SetBWTE(A, block_suffixes=int(rng.integers(30, 600)))
-    idx.set_option("rank_ilp", 4)
+    from paper_1410_0562_b200 import SetBWTEError
+    for key in ("rank_ilp", "kw1_min"):
+        with pytest.raises(SetBWTEError):
+            idx.set_option(key, 4)
     idx.set_option("hbm_budget_bytes", budget)
     if seed % 2:
         idx.set_option("g_width", 8)
@@ -733,3 +731,47 @@ def test_invalid_char_into_empty_index(SetBWTE, lanes, device):
     with pytest.raises(SetBWTEError):
         idx.append(bad, o)
     assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+# --- bucketed gather (gather.cu): forced at small sizes, every B_int source ----
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("opts", [dict(), dict(g_width=8), dict(sa_payload=0),
+                                  dict(sa_payload=0, g_width=8)])
+def test_bucketed_gather_random_sets(SetBWTE, seed, opts):
+    d, o = synth.random_set(24000 + seed, max_m=64, max_len=60)
+    want = oracle.bwt(A, d, o)
+    idx = SetBWTE(A, block_suffixes=int(np.random.default_rng(seed).integers(50, 3000)))
+    idx.set_option("gather_buckets", 2)
+    for k, v in opts.items():
+        idx.set_option(k, v)
+    m = len(o) - 1
+    oo = np.asarray(o, dtype=np.uint64)
+    idx.append(d[: int(oo[m // 2])], oo[: m // 2 + 1])
+    idx.append(d[int(oo[m // 2]):], oo[m // 2:] - oo[m // 2])
+    assert idx.bwt() == want
+
+
+@pytest.mark.parametrize("M", [25250, 1 << 20])
+def test_bucketed_gather_c1_and_scaled(SetBWTE, c1, M):
+    d, o, want = c1
+    idx = build(SetBWTE, d, o, M=M)
+    ref = idx.bwt()
+    idx2 = SetBWTE(A, block_suffixes=M)
+    idx2.set_option("gather_buckets", 2)
+    idx2.append(d, o)
+    assert idx2.bwt() == want == ref
+
+
+def test_bucketed_gather_multi_tile_blocks(SetBWTE):
+    """300k reads, blocks of 2^23 suffixes: thousands of 4096-position tiles
+    and 8+ buckets per block, forced."""
+    d, o = synth.uniform(300_000, 100, seed=11)
+    want = oracle.bwt(A, d, o, threads=None)
+    for gw in (0, 8):
+        idx = SetBWTE(A, block_suffixes=1 << 23)
+        idx.set_option("gather_buckets", 2)
+        if gw:
+            idx.set_option("g_width", 8)
+        idx.append(d, o)
+        assert idx.bwt() == want

@@ -1,9 +1,16 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times: the whole BWT against the oracle where the oracle finishes in seconds
-(c2), otherwise sampled outputs the oracle computes one by one (the SA
-position of a suffix, gives B at that position by Eq.(1)) plus
-properties that hold at any size (B[0..m) = last symbols, m terminators,
-LF inversion recovers reads)."""
+times.  c3, c4 and c5: the WHOLE BWT against the oracle's, through the
+oracle-written digests of tests/golden/<cfg>_bwt_digest.json
+(tools/make_golden_digests.py: the bucketed one-shot oracle, BLAKE2b-128 of
+the full ASCII BWT, per-bucket digests and exact 4 KB windows) -- a byte
+compare in all but name.  Also sampled outputs the oracle computes one by one
+(the SA position of a suffix, gives B at that position by Eq.(1)) and
+properties that hold at any size (B[0..m) = last symbols, m terminators, LF
+inversion recovers reads)."""
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -12,6 +19,26 @@ import synth
 
 pytestmark = pytest.mark.gpu
 A = "ACGT"
+
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _digest_checks(B: bytes, cfg: str):
+    """The whole BWT against the oracle's digest, windows and bucket digests."""
+    gd = json.load(open(os.path.join(GOLD, "%s_bwt_digest.json" % cfg)))
+    assert len(B) == gd["n"]
+    mv = memoryview(B)
+    for w in gd["windows"]:
+        s = w["start"]
+        assert bytes(mv[s:s + len(w["bytes"])]) == w["bytes"].encode(), ("window", s)
+    bad = [b["bucket"] for b in gd["buckets"]
+           if hashlib.blake2b(mv[b["start"]:b["start"] + b["len"]], digest_size=16).hexdigest()
+           != b["blake2b_128"]]
+    assert not bad, ("buckets differ", bad[:10])
+    h = hashlib.blake2b(digest_size=16)
+    h.update(mv)
+    assert h.hexdigest() == gd["digest"]["hex"]
 
 
 def _sampled_checks(idx, data, offsets, n_samples, seed):
@@ -61,6 +88,7 @@ def test_c3_full_sampled():
     idx = SetBWTE(A, block_suffixes=1 << 27)
     idx.append(d, o)
     assert idx.stats()["blocks"] == 16
+    _digest_checks(idx.bwt(), "c3")
     _sampled_checks(idx, d, o, n_samples=4, seed=3)
 
 
@@ -95,6 +123,7 @@ def test_c4_full_sampled():
     idx = SetBWTE(A, block_suffixes=1 << 30)
     idx.append(d, o)
     assert idx.stats()["blocks"] >= 5
+    _digest_checks(idx.bwt(), "c4")
     _sampled_checks(idx, d, o, n_samples=2, seed=5)
 
 
@@ -115,4 +144,5 @@ def test_c5_full_sampled():
     o = np.concatenate([np.asarray(bo, dtype=np.uint64),
                         np.asarray(ao[1:], dtype=np.uint64) + np.uint64(bo[-1])])
     del bd, ad
+    _digest_checks(idx.bwt(), "c5")
     _sampled_checks(idx, d, o, n_samples=2, seed=6)
