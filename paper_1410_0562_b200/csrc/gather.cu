@@ -25,6 +25,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
+#include <stdio.h>
 
 #include "blockrank.cuh"
 #include "internal.h"
@@ -132,14 +134,15 @@ __device__ __forceinline__ void gb_tile(const uint32_t* __restrict__ sa, uint32_
     __syncthreads();
 }
 
-template <int NB>
+template <int NB, class G>
 __global__ void __launch_bounds__(kGbNt) gb_part_kernel(const uint32_t* __restrict__ sa,
                                                         uint32_t smask, uint32_t n,
                                                         uint32_t shift, uint32_t nb,
                                                         uint32_t ntiles,
                                                         const uint32_t* __restrict__ row,
                                                         const uint32_t* __restrict__ tot,
-                                                        uint32_t* __restrict__ out) {
+                                                        uint32_t* __restrict__ out,
+                                                        G* __restrict__ kpos) {
     __shared__ uint32_t wcnt[(kGbNt / 32) * 256];
     __shared__ uint32_t dstart[260], tmp[32], off[256];
     __shared__ uint32_t s_slot[kGbTile];
@@ -147,9 +150,15 @@ __global__ void __launch_bounds__(kGbNt) gb_part_kernel(const uint32_t* __restri
         uint32_t e[kGbIpt], dig[kGbIpt], dest[kGbIpt];
         gb_tile<NB>(sa, smask, n, shift, nb, ntiles, row, tot, t, e, dig, dest, wcnt, dstart, tmp,
                     off);
+        // every element's place k in the partition, in SA order: the final
+        // pass reads g_sa[i] back from there without ranking again
+        const uint32_t t0 = t * kGbTile;
 #pragma unroll
         for (int it = 0; it < kGbIpt; ++it)
-            if (dig[it] < (1u << NB)) s_slot[dest[it]] = e[it] & smask;
+            if (dig[it] < (1u << NB)) {
+                s_slot[dest[it]] = e[it] & smask;
+                __stcs(kpos + t0 + item_index(threadIdx.x, it), (G)(off[dig[it]] + dest[it]));
+            }
         __syncthreads();
         // coalesced write-out: a bucket's members of the tile are one run
         const uint32_t tn = min(kGbTile, n - t * kGbTile);
@@ -161,106 +170,77 @@ __global__ void __launch_bounds__(kGbNt) gb_part_kernel(const uint32_t* __restri
     }
 }
 
-// tmp2[k] = g[slot[k]] in k order (the g reads stay inside one bucket's slice)
+// tmp2[k] = g[slot[k]] in k order (the g reads stay inside one bucket's
+// slice).  ONE wave of CTAs (148 x 8 resident) walking k with the grid
+// stride: every CTA is at about the same k, so the reads at any moment fall
+// in one or two buckets.  (A 4x-unrolled version with 2 waves of CTAs read
+// 12.4 GB of DRAM per c3 block instead of 1.1 GB: its concurrent reads
+// spanned the whole array -- ncu, profiles/.)
 template <class G>
-__global__ void gb_fetch_kernel(const uint32_t* __restrict__ slot, const G* __restrict__ g,
-                                uint32_t n, G* __restrict__ out) {
-    const uint32_t stride = gridDim.x * blockDim.x;
-    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    for (; k + 3 * stride < n; k += 4 * stride) {
-        uint32_t s[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s[u] = __ldcs(slot + k + u * stride);
-        G v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldg(g + s[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) __stcs(out + k + u * stride, v[u]);
-    }
-    for (; k < n; k += stride) __stcs(out + k, __ldg(g + __ldcs(slot + k)));
+__global__ void __launch_bounds__(256) gb_fetch_kernel(const uint32_t* __restrict__ slot,
+                                                       const G* __restrict__ g, uint32_t n,
+                                                       G* __restrict__ out) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        __stcs(out + k, __ldg(g + __ldcs(slot + k)));
 }
 
-// pos, B_int and sb_start from the fetched g values (the tail of gather_kernel)
-template <int NB, class G>
-__global__ void __launch_bounds__(kGbNt) gb_final_kernel(
-    const uint32_t* __restrict__ sa, uint32_t smask, uint32_t n, uint32_t shift, uint32_t nb,
-    uint32_t ntiles, const uint32_t* __restrict__ row, const uint32_t* __restrict__ tot,
-    const G* __restrict__ gv_b, const G* __restrict__ g, G* __restrict__ pos,
-    uint8_t* __restrict__ bint, uint64_t* __restrict__ sb_start, uint64_t nsb,
-    const uint8_t* __restrict__ bslot, bool bing, const uint32_t* __restrict__ text,
-    const uint32_t* __restrict__ term, const uint32_t* __restrict__ nbit, uint64_t slot_base) {
-    __shared__ uint32_t wcnt[(kGbNt / 32) * 256];
-    __shared__ uint32_t dstart[260], tmp[32], off[256];
-    __shared__ uint64_t wlast[kGbNt / 32];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        uint32_t e[kGbIpt], dig[kGbIpt], dest[kGbIpt];
-        gb_tile<NB>(sa, smask, n, shift, nb, ntiles, row, tot, t, e, dig, dest, wcnt, dstart, tmp,
-                    off);
-        const uint32_t t0 = t * kGbTile;
-        uint64_t pv[kGbIpt];
-#pragma unroll
-        for (int it = 0; it < kGbIpt; ++it) {
-            const uint32_t i = t0 + item_index(threadIdx.x, it);
-            pv[it] = 0;
-            if (i < n) {
-                uint64_t gvv = (uint64_t)__ldcs(gv_b + off[dig[it]] + dest[it]);
-                const uint8_t bg = (uint8_t)(gvv >> 56);
-                if (bing) gvv &= (1ull << 56) - 1ull;
-                pv[it] = gvv + i;
-                __stcs(pos + i, (G)pv[it]);
-                const uint32_t sl = e[it] & smask;
-                uint8_t b;
-                if (bing) {
-                    b = bg;
-                } else if (smask != 0xFFFFFFFFu) {
-                    b = (uint8_t)(e[it] >> kPayloadShift);
-                } else if (bslot) {
-                    b = __ldg(bslot + sl);
-                } else {
-                    const uint64_t p = slot_base + sl;
-                    if (sl == 0 || term_bit(term, p - 1)) b = 4;
-                    else if (nbit && term_bit(nbit, p - 1)) b = 5;
-                    else b = (uint8_t)text_sym(text, p - 1);
-                }
-                if (b == 5) b = 12;  // code 4 of sigma = 5: '$' flag + N flag
-                __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
+// pos, B_int and sb_start from the fetched g values (the tail of gather_kernel):
+// pos[i] holds the element's place k in the partition (gb_part_kernel), so
+// g_sa[i] = gval[k] -- a streaming pass, no ranking.
+template <class G>
+__global__ void __launch_bounds__(256) gb_final_kernel(
+    const uint32_t* __restrict__ sa, uint32_t smask, uint32_t n, const G* __restrict__ gv_b,
+    const G* __restrict__ g, G* __restrict__ pos, uint8_t* __restrict__ bint,
+    uint64_t* __restrict__ sb_start, uint64_t nsb, const uint8_t* __restrict__ bslot, bool bing,
+    const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
+    const uint32_t* __restrict__ nbit, uint64_t slot_base) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t iters = (n + stride - 1) / stride;  // warp-uniform trip count
+    for (uint64_t itr = 0; itr < iters; ++itr) {
+        const uint64_t i = itr * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        const bool v = i < n;
+        uint64_t pv = 0;
+        if (v) {
+            const uint32_t e = __ldcs(sa + i);
+            const uint64_t k = (uint64_t)__ldcs(pos + i);
+            uint64_t gvv = (uint64_t)__ldcs(gv_b + k);
+            const uint8_t bg = (uint8_t)(gvv >> 56);
+            if (bing) gvv &= (1ull << 56) - 1ull;
+            pv = gvv + i;
+            __stcs(pos + i, (G)pv);
+            const uint32_t sl = e & smask;
+            uint8_t b;
+            if (bing) {
+                b = bg;
+            } else if (smask != 0xFFFFFFFFu) {
+                b = (uint8_t)(e >> kPayloadShift);
+            } else if (bslot) {
+                b = __ldg(bslot + sl);
+            } else {
+                const uint64_t p = slot_base + sl;
+                if (sl == 0 || term_bit(term, p - 1)) b = 4;
+                else if (nbit && term_bit(nbit, p - 1)) b = 5;
+                else b = (uint8_t)text_sym(text, p - 1);
             }
+            if (b == 5) b = 12;  // code 4 of sigma = 5: '$' flag + N flag
+            __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
         }
         if (sb_start) {
-            // predecessor of every item: the previous lane, lane 31 of the
-            // previous item, the previous warp's last item, or (tile start)
-            // the element before the tile, fetched directly
-            if (lane == 31) wlast[warp] = pv[kGbIpt - 1];
-            __syncthreads();
-            uint64_t carry;
-            if (warp > 0) {
-                carry = wlast[warp - 1];
-            } else {
-                carry = 0;
-                if (t0 > 0) {
-                    const uint32_t sl1 = sa[t0 - 1] & smask;
+            uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
+            if (v) {
+                if (lane == 0 && i > 0) {
+                    const uint32_t sl1 = sa[i - 1] & smask;
                     uint64_t g1 = (uint64_t)__ldg(g + sl1);
                     if (bing) g1 &= (1ull << 56) - 1ull;
-                    carry = g1 + (t0 - 1);
+                    prev = g1 + (i - 1);
                 }
+                const uint64_t cur = pv >> kSbShift;
+                const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
+                for (uint64_t s = first; s <= cur && s <= nsb; ++s) sb_start[s] = i;
+                if (i + 1 == n)
+                    for (uint64_t s = cur + 1; s <= nsb; ++s) sb_start[s] = n;
             }
-#pragma unroll
-            for (int it = 0; it < kGbIpt; ++it) {
-                const uint32_t i = t0 + item_index(threadIdx.x, it);
-                const uint64_t up = __shfl_up_sync(0xFFFFFFFFu, pv[it], 1);
-                const uint64_t l31 = __shfl_sync(0xFFFFFFFFu, pv[it], 31);
-                const uint64_t prev = lane == 0 ? carry : up;
-                carry = l31;
-                if (i < n) {
-                    const uint64_t cur = pv[it] >> kSbShift;
-                    const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
-                    for (uint64_t s = first; s <= cur && s <= nsb; ++s) sb_start[s] = i;
-                    if (i + 1 == n)
-                        for (uint64_t s = cur + 1; s <= nsb; ++s) sb_start[s] = n;
-                }
-            }
-            __syncthreads();
         }
     }
 }
@@ -283,18 +263,28 @@ cudaError_t run_bucketed(Profiler& prof, cudaStream_t s, const uint32_t* sa, uin
               (gb_rows_kernel<<<nb, 1024, 0, s>>>(ws.rows, ntiles, tot)));
     SB_CHECK(cudaGetLastError());
     SB_LAUNCH(prof, s, "gather_part", 0, 0,
-              (gb_part_kernel<NB><<<grid_t, kGbNt, 0, s>>>(sa, smask, n, shift, nb, ntiles, ws.rows,
-                                                           tot, ws.slot)));
+              (gb_part_kernel<NB, G><<<grid_t, kGbNt, 0, s>>>(sa, smask, n, shift, nb, ntiles,
+                                                              ws.rows, tot, ws.slot, pos)));
     SB_CHECK(cudaGetLastError());
+    if (getenv("SETBWTE_GB_CHECK")) {
+        // debug: is the partition bucket-ordered?
+        SB_CHECK(cudaStreamSynchronize(s));
+        std::vector<uint32_t> hs(n);
+        SB_CHECK(cudaMemcpy(hs.data(), ws.slot, 4ull * n, cudaMemcpyDeviceToHost));
+        uint64_t inv = 0, maxs = 0;
+        for (uint32_t k = 1; k < n; ++k) inv += (hs[k] >> shift) < (hs[k - 1] >> shift);
+        for (uint32_t k = 0; k < n; ++k) maxs = std::max<uint64_t>(maxs, hs[k]);
+        fprintf(stderr, "[gb] n=%u shift=%u nb=%u inversions=%llu max_slot=%llu first=%u,%u,%u\n", n,
+                shift, nb, (unsigned long long)inv, (unsigned long long)maxs, hs[0], hs[1], hs[2]);
+    }
     G* gv_b = reinterpret_cast<G*>(ws.gval);
     SB_LAUNCH(prof, s, "gather_fetch", 0, 0,
-              (gb_fetch_kernel<G><<<grid_for(n, 256, 148u * 16u), 256, 0, s>>>(ws.slot, g, n,
-                                                                               gv_b)));
+              (gb_fetch_kernel<G><<<148u * 8u, 256, 0, s>>>(ws.slot, g, n, gv_b)));
     SB_CHECK(cudaGetLastError());
     SB_LAUNCH(prof, s, "gather", bytes, n,
-              (gb_final_kernel<NB, G><<<grid_t, kGbNt, 0, s>>>(
-                  sa, smask, n, shift, nb, ntiles, ws.rows, tot, gv_b, g, pos, bint, sb_start, nsb,
-                  bslot, bing, text, term, nbit, slot_base)));
+              (gb_final_kernel<G><<<grid_for(n, 256, 148u * 8u), 256, 0, s>>>(
+                  sa, smask, n, gv_b, g, pos, bint, sb_start, nsb, bslot, bing, text, term, nbit,
+                  slot_base)));
     return cudaGetLastError();
 }
 
@@ -331,13 +321,13 @@ cudaError_t launch_gather_bucketed(Profiler& prof, cudaStream_t s, const uint32_
     const uint32_t smask = sa_slot_mask(n_suf, payload_limit);
     const uint32_t nb = (uint32_t)(((uint64_t)(n_suf - 1) >> shift) + 1);
     const double bytes = (5.375 + 2.0 * gw) * n_suf;
-    if (nb <= 16) {
+    if (nb <= 32) {
         if (gw == 4)
-            return run_bucketed<4, uint32_t>(prof, s, sa, smask, n_suf, shift, nb,
+            return run_bucketed<5, uint32_t>(prof, s, sa, smask, n_suf, shift, nb,
                                              (const uint32_t*)g, (uint32_t*)pos, bint, sb_start,
                                              nsb, bslot, false, text, term, nbit, slot_base, ws,
                                              bytes);
-        return run_bucketed<4, uint64_t>(prof, s, sa, smask, n_suf, shift, nb, (const uint64_t*)g,
+        return run_bucketed<5, uint64_t>(prof, s, sa, smask, n_suf, shift, nb, (const uint64_t*)g,
                                          (uint64_t*)pos, bint, sb_start, nsb, bslot, bing, text,
                                          term, nbit, slot_base, ws, bytes);
     }

@@ -69,7 +69,8 @@ constexpr int kDigTile = kDigNt * kDigIpt;
 // the whole digit pass of the segment in one CTA (local_digit_kernel).
 enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, LOCALD, NCLASS };
 // misc counters
-enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_N };
+enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_ACTIVE_LOC,
+       M_N };
 
 struct Seg {
     uint32_t start, len, word, meta;  // meta: shift | buf<<8 | keys_valid<<9 | iota<<10
@@ -762,104 +763,6 @@ constexpr size_t scatter_smem() {
 }
 
 // ---------------------------------------------------------------------------
-// LOCALD: the digit pass of one segment of 513..4096 members with valid keys,
-// entirely in one CTA -- the segment is one tile, so the tile's stable ranks
-// ARE the segment's digit histogram and offsets: no chunk / histogram / scan
-// kernels, one read and one write of (key, slot).  Same outputs as the
-// LARGE path: resolved buckets (one member, or equal keys that end inside
-// the word) go to their final SA positions; the others become child
-// segments, keyed on the next digit (or the next word at shift 0).
-// ---------------------------------------------------------------------------
-constexpr int kLocNt = 512;
-constexpr int kLocIpt = 8;
-static_assert(kLocNt * kLocIpt == (int)kCapM, "one tile per LOCALD segment");
-
-constexpr size_t local_digit_smem() {
-    return (size_t)(kLocNt / 32) * 256 * 4 + 2 * (size_t)kCapM * 8 + 260 * 4 + 32 * 4 + 256 + 64;
-}
-
-__global__ void __launch_bounds__(kLocNt, 2) local_digit_kernel(Lists in, Lists out, Bufs B,
-                                                                 uint32_t* misc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);                   // NW*256
-    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + (kLocNt / 32) * 256);       // kCapM: sorted
-    uint2* s_in = s_kv + kCapM;                                               // kCapM: as loaded
-    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_in + kCapM);             // 257
-    uint32_t* tmp = dstart + 260;                                             // 32
-    uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);                      // 256
-    __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
-    const uint32_t n = in.cnt[LOCALD];
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
-        const Seg s = in.seg[LOCALD][si];
-        const uint32_t shift = meta_shift(s.meta), buf = meta_buf(s.meta);
-        const bool iota = meta_iota(s.meta);
-        const uint32_t* S = B.sa[buf] + s.start;
-        const uint32_t* K = B.key[buf] + s.start;
-        // (key, slot) wait in shared memory while the digits are ranked
-        // (registers hold only digits and ranks: no spills at 2 CTAs/SM)
-        uint32_t dig[kLocIpt], dest[kLocIpt];
-#pragma unroll
-        for (int it = 0; it < kLocIpt; ++it) {
-            const uint32_t e = warp * (32 * kLocIpt) + it * 32 + lane;
-            const bool valid = e < s.len;
-            const uint32_t key = valid ? __ldcs(K + e) : 0u;
-            const uint32_t slot = valid ? (iota ? sa_entry(B, s.start + e) : __ldcs(S + e)) : 0u;
-            s_in[e] = make_uint2(key, slot);
-            dig[it] = valid ? ((key >> shift) & 0xFFu) : 0x100u;
-        }
-        if (tid < NCLASS) ccount[tid] = 0;
-        block_rank<kLocNt, kLocIpt>(dig, dest, wcnt, dstart, tmp);
-        // per digit: sieve decision and child segment (digit_scan's rules)
-        int cls = -1;
-        uint32_t local = 0;
-        Seg c;
-        if (tid < 256) {
-            const uint32_t d = tid;
-            const uint32_t total = dstart[d + 1] - dstart[d];
-            const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < B.ksyms);
-            fin[d] = resolved ? 1 : 0;
-            if (total > 0 && !resolved) {
-                c.start = s.start + dstart[d];
-                c.len = total;
-                if (shift == 0) {
-                    c.word = s.word + 1;
-                    c.meta = make_meta(24, 1u - buf, 0);
-                } else {
-                    c.word = s.word;
-                    c.meta = make_meta(shift - 8, 1u - buf, 1);
-                }
-                cls = class_of(c);
-                local = atomicAdd(&ccount[cls], 1u);
-            }
-        }
-#pragma unroll
-        for (int it = 0; it < kLocIpt; ++it)
-            if (dig[it] < 256) s_kv[dest[it]] = s_in[warp * (32 * kLocIpt) + it * 32 + lane];
-        __syncthreads();
-        if (tid < NCLASS && ccount[tid]) cbase[tid] = atomicAdd(out.cnt + tid, ccount[tid]);
-        if (tid == 0) atomicAdd(misc + M_ACTIVE, s.len);
-        __syncthreads();
-        if (cls >= 0) out.seg[cls][cbase[cls] + local] = c;
-        // write-out in segment order: finished buckets to the final SA, the
-        // others (key, slot) into the other buffer
-        uint32_t* S2 = B.sa[1 - buf] + s.start;
-        uint32_t* K2 = B.key[1 - buf] + s.start;
-        for (uint32_t i = tid; i < s.len; i += kLocNt) {
-            const uint2 kv = s_kv[i];
-            if (fin[(kv.x >> shift) & 0xFFu]) {
-                SB_ASSERT(s.start + i < B.n);
-                __stcs(B.saf + s.start + i, kv.y);
-            } else {
-                S2[i] = kv.y;
-                K2[i] = kv.x;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // TINY: one warp per segment
 // ---------------------------------------------------------------------------
 constexpr uint32_t kTinyPerWarp = 32;  // list entries per warp, packed into shared calls
@@ -977,6 +880,156 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
         if (lane == 0) atomicAdd(misc + M_ELEMS_T, elems);
     }
 }
+
+// ---------------------------------------------------------------------------
+// LOCALD: the digit pass of one segment of 513..4096 members with valid keys,
+// entirely in one CTA -- the segment is one tile, so the tile's stable ranks
+// ARE the segment's digit histogram and offsets: no chunk / histogram / scan
+// kernels, one read and one write of (key, slot).  Same outputs as the
+// LARGE path: resolved buckets (one member, or equal keys that end inside
+// the word) go to their final SA positions; buckets of 2..32 members are
+// finished right here by the warps, as the TINY class would (a register sort
+// of their remaining key bits, ties continued on the next words); the
+// others become child segments, keyed on the next digit (or the next word
+// at shift 0).
+// ---------------------------------------------------------------------------
+constexpr int kLocNt = 512;
+constexpr int kLocIpt = 8;
+static_assert(kLocNt * kLocIpt == (int)kCapM, "one tile per LOCALD segment");
+
+constexpr size_t local_digit_smem() {
+    return (size_t)(kLocNt / 32) * 256 * 4 + 2 * (size_t)kCapM * 8 + 260 * 4 + 32 * 4 + 256 + 64;
+}
+
+__global__ void __launch_bounds__(kLocNt, 2) local_digit_kernel(Lists in, Lists out, Bufs B,
+                                                                 uint32_t* misc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);                   // NW*256
+    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + (kLocNt / 32) * 256);       // kCapM: sorted
+    uint2* s_in = s_kv + kCapM;                                               // kCapM: as loaded
+    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_in + kCapM);             // 257
+    uint32_t* tmp = dstart + 260;                                             // 32
+    uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);                      // 256
+    __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
+    const uint32_t n = in.cnt[LOCALD];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
+        const Seg s = in.seg[LOCALD][si];
+        const uint32_t shift = meta_shift(s.meta), buf = meta_buf(s.meta);
+        const bool iota = meta_iota(s.meta);
+        const uint32_t* S = B.sa[buf] + s.start;
+        const uint32_t* K = B.key[buf] + s.start;
+        // (key, slot) wait in shared memory while the digits are ranked
+        // (registers hold only digits and ranks: no spills at 2 CTAs/SM)
+        uint32_t dig[kLocIpt], dest[kLocIpt];
+#pragma unroll
+        for (int it = 0; it < kLocIpt; ++it) {
+            const uint32_t e = warp * (32 * kLocIpt) + it * 32 + lane;
+            const bool valid = e < s.len;
+            const uint32_t key = valid ? __ldcs(K + e) : 0u;
+            const uint32_t slot = valid ? (iota ? sa_entry(B, s.start + e) : __ldcs(S + e)) : 0u;
+            s_in[e] = make_uint2(key, slot);
+            dig[it] = valid ? ((key >> shift) & 0xFFu) : 0x100u;
+        }
+        if (tid < NCLASS) ccount[tid] = 0;
+        block_rank<kLocNt, kLocIpt>(dig, dest, wcnt, dstart, tmp);
+        // per digit: sieve decision and child segment (digit_scan's rules)
+        int cls = -1;
+        uint32_t local = 0;
+        Seg c;
+        if (tid < 256) {
+            const uint32_t d = tid;
+            const uint32_t total = dstart[d + 1] - dstart[d];
+            const bool resolved = (total == 1) || (shift == 0 && (d & 15u) < B.ksyms);
+            // 2..32 members, remaining key bits <= 16 (or the next word):
+            // finished in this CTA below (fin = 2)
+            const bool here = !resolved && total >= 2 && total <= 32 && shift <= 16;
+            fin[d] = resolved ? 1 : here ? 2 : 0;
+            if (total > 0 && !resolved && !here) {
+                c.start = s.start + dstart[d];
+                c.len = total;
+                if (shift == 0) {
+                    c.word = s.word + 1;
+                    c.meta = make_meta(24, 1u - buf, 0);
+                } else {
+                    c.word = s.word;
+                    c.meta = make_meta(shift - 8, 1u - buf, 1);
+                }
+                cls = class_of(c);
+                local = atomicAdd(&ccount[cls], 1u);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kLocIpt; ++it)
+            if (dig[it] < 256) s_kv[dest[it]] = s_in[warp * (32 * kLocIpt) + it * 32 + lane];
+        __syncthreads();
+        if (tid < NCLASS && ccount[tid]) cbase[tid] = atomicAdd(out.cnt + tid, ccount[tid]);
+        if (tid == 0) {
+            atomicAdd(misc + M_ACTIVE, s.len);
+            atomicAdd(misc + M_ACTIVE_LOC, s.len);
+        }
+        __syncthreads();
+        if (cls >= 0) out.seg[cls][cbase[cls] + local] = c;
+        // the small buckets: warp w takes digits [16w, 16w+16) in order and
+        // packs consecutive buckets into its 32 lanes (tiny_kernel's scheme)
+        {
+            uint32_t lb = 0, dstp = 0, slot = 0, key = 0, grp = 0;
+            bool mine = false;
+            for (uint32_t q = 0; q <= 16; ++q) {
+                const uint32_t d = warp * 16 + q;
+                const uint32_t tot = (q < 16 && fin[d] == 2) ? dstart[d + 1] - dstart[d] : 0u;
+                if (q == 16 || lb + tot > 32) {
+                    if (lb) {
+                        uint32_t r;
+                        if (shift > 0) {
+                            // the child's unknown key bits: [0, shift)
+                            bool tie;
+                            uint32_t run;
+                            r = warp_sort16(slot, lb, grp, key, shift, tie, run, B.ksyms);
+                            if (__any_sync(0xFFFFFFFFu, tie))
+                                r = warp_finish(r, lb, s.word + 1, 0u, false, B, run, tie);
+                        } else {
+                            r = warp_finish(slot, lb, s.word + 1, 0u, false, B, grp);
+                        }
+                        SB_ASSERT(!mine || s.start + dstp < B.n);
+                        if (mine) B.saf[s.start + dstp] = r;
+                    }
+                    lb = 0;
+                    mine = false;
+                    if (q == 16) break;
+                }
+                if (tot) {
+                    if (lane >= lb && lane < lb + tot) {
+                        dstp = dstart[d] + (lane - lb);
+                        const uint2 kv = s_kv[dstp];
+                        key = kv.x;
+                        slot = kv.y;
+                        grp = lb;
+                        mine = true;
+                    }
+                    lb += tot;
+                }
+            }
+        }
+        // write-out in segment order: finished buckets to the final SA, the
+        // child segments' (key, slot) into the other buffer
+        uint32_t* S2 = B.sa[1 - buf] + s.start;
+        uint32_t* K2 = B.key[1 - buf] + s.start;
+        for (uint32_t i = tid; i < s.len; i += kLocNt) {
+            const uint2 kv = s_kv[i];
+            const uint8_t f = fin[(kv.x >> shift) & 0xFFu];
+            if (f == 1) {
+                SB_ASSERT(s.start + i < B.n);
+                __stcs(B.saf + s.start + i, kv.y);
+            } else if (f == 0) {
+                S2[i] = kv.y;
+                K2[i] = kv.x;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 
 // ---------------------------------------------------------------------------
 // Common tail of the warp sorts: buf[0..L) holds the segment's (key word,
@@ -1688,6 +1741,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
             SB_CHECK(cudaGetLastError());
         }
         if (cnt[LOCALD]) {
+            // algorithmic bytes: the digit pass's read + write of (key, slot)
+            // per member (16 B, added with the round's active count below)
             SB_LAUNCH(prof, s, "sort_local_digit", 0, 0,
                       (local_digit_kernel<<<std::min<uint32_t>(cnt[LOCALD], 148u * 2u * 4u),
                                             kLocNt, sm_ld, s>>>(in, out, B, misc)));
@@ -1811,8 +1866,10 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     // algorithmic bytes: a digit pass reads/writes the
     // (slot, key) pair -- histogram 8 B, scatter 16 B per active element; the
     // local sorts read (slot, key) and write the final SA entry (12 B/element).
-    prof.add_bytes("digit_hist", 8.0 * act_local, act_local);
-    prof.add_bytes("digit_scatter", 16.0 * act_local, act_local);
+    const uint64_t act_loc = h_misc[M_ACTIVE_LOC];
+    prof.add_bytes("digit_hist", 8.0 * (act_local - act_loc), act_local - act_loc);
+    prof.add_bytes("digit_scatter", 16.0 * (act_local - act_loc), act_local - act_loc);
+    prof.add_bytes("sort_local_digit", 16.0 * act_loc, act_loc);
     prof.add_bytes("sort_tiny", 12.0 * h_misc[M_ELEMS_T], h_misc[M_ELEMS_T]);
     prof.add_bytes("sort_small", 12.0 * h_misc[M_ELEMS_S], h_misc[M_ELEMS_S]);
     prof.add_bytes("sort_medium", 12.0 * h_misc[M_ELEMS_M], h_misc[M_ELEMS_M]);
