@@ -91,7 +91,9 @@ def load_library(path: str = LIB_PATH):
         "setbwte_last_error": ([vp, _u64p, _u8p], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
-        f = getattr(lib, name)
+        f = getattr(lib, name, None)
+        if f is None:  # an older library build (A/B variants): the call is unavailable
+            continue
         f.argtypes = args
         f.restype = res
     _lib = lib

@@ -16,6 +16,7 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <sys/mman.h>
 
 #include "internal.h"
 #include "setbwte.h"
@@ -264,9 +265,13 @@ struct setbwte_s {
     // host memory (zero-copy for ComputeRanks / queries), rewritten in place
     // by Insert through HBM staging, top superblock range first
     bool host_tier = false;
-    Blk* hdict = nullptr;       // host pointer
+    Blk* hdict = nullptr;       // host pointer (mmap'd, registered mapped + portable)
     Blk* hdict_dev = nullptr;   // device alias
     uint64_t hdict_cap = 0;     // capacity in Blks
+    size_t hdict_bytes = 0;     // bytes mapped
+    // the host Insert's read-ahead pipeline: staging H2D / write-back D2H
+    cudaStream_t tier_in = nullptr, tier_out = nullptr;
+    cudaEvent_t ev_staged[2] = {}, ev_merged[2] = {}, ev_written[2] = {};
     DevBuf stage_in, stage_out;
     std::vector<uint64_t> h_sb_start;
 
@@ -505,21 +510,57 @@ struct BlockDesc {
 // Pinned mapped host buffer for the dictionary with >= nblk Blks, keeping
 // the first keep_blks of the current content.  Capacity grows 1.5x, so the
 // host memory stays <= 1.5 x 4 bits/symbol = 6 bits = 3 n log(sigma) for
-// sigma = 4.
+// sigma = 4 -- at EVERY instant: the buffer is an anonymous
+// mapping that grows with mremap (the kernel moves the page mappings; no
+// second buffer and no copy), registered with CUDA as mapped memory.
+static void host_dict_free(setbwte_t h) {
+    if (!h->hdict) return;
+    cudaHostUnregister(h->hdict);
+    munmap(h->hdict, h->hdict_bytes);
+    h->hdict = nullptr;
+    h->hdict_dev = nullptr;
+    h->hdict_cap = 0;
+    h->hdict_bytes = 0;
+}
+
 setbwte_status host_reserve(setbwte_t h, uint64_t nblk, const Blk* src, bool src_dev,
                             uint64_t keep_blks) {
     const uint64_t cap = std::max<uint64_t>(nblk + nblk / 2, 1024);
+    const size_t bytes = ((size_t)cap * sizeof(Blk) + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
+    // nothing may read the old mapping while it moves
+    API_CHECK(h, cudaDeviceSynchronize());
     void* p = nullptr;
-    API_CHECK(h, cudaHostAlloc(&p, cap * sizeof(Blk), cudaHostAllocMapped | cudaHostAllocPortable));
+    if (h->hdict && !src_dev) {
+        // grow in place (keep_blks of the old content travel with the pages)
+        API_CHECK(h, cudaHostUnregister(h->hdict));
+        p = mremap(h->hdict, h->hdict_bytes, bytes, MREMAP_MAYMOVE);
+        if (p == MAP_FAILED) {
+            // the old mapping is intact: register it again and report
+            cudaHostRegister(h->hdict, h->hdict_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+            return SETBWTE_E_NOMEM;
+        }
+    } else {
+        host_dict_free(h);
+        p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) return SETBWTE_E_NOMEM;
+    }
+    h->hdict = (Blk*)p;
+    h->hdict_bytes = bytes;
+    madvise(p, bytes, MADV_HUGEPAGE);
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        munmap(p, bytes);
+        h->hdict = nullptr;
+        h->hdict_bytes = 0;
+        h->hdict_cap = 0;
+        return from_cuda(h, e);
+    }
     void* pd = nullptr;
     API_CHECK(h, cudaHostGetDevicePointer(&pd, p, 0));
-    if (keep_blks)
-        API_CHECK(h, cudaMemcpyAsync(p, src, keep_blks * sizeof(Blk),
-                                     src_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost,
+    if (keep_blks && src_dev)
+        API_CHECK(h, cudaMemcpyAsync(p, src, keep_blks * sizeof(Blk), cudaMemcpyDeviceToHost,
                                      h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
-    if (h->hdict) API_CHECK(h, cudaFreeHost(h->hdict));
-    h->hdict = (Blk*)p;
     h->hdict_dev = (Blk*)pd;
     h->hdict_cap = cap;
     return SETBWTE_OK;
@@ -528,9 +569,12 @@ setbwte_status host_reserve(setbwte_t h, uint64_t nblk, const Blk* src, bool src
 // Insert with B_ext in host memory: output superblocks in chunks from the top
 // down; each chunk's external input range is staged into HBM, merged, and
 // written back in place.  A chunk writes [O0, O1) and reads external symbols
-// below O1 only, which no later (lower) chunk has written yet, and every
-// higher chunk's inputs lie at or above O1's chunk boundary -- so one stream
-// in top-down order is safe without extra copies.
+// [E0, E1) with E1 <= O1 = the first output symbol of the chunk above it
+// (an output index is never below its input index), so no write-back of a
+// higher chunk touches an input symbol of a lower one.  So the staging H2D of the next (lower)
+// chunk runs while this chunk merges and writes back: a read-ahead pipeline
+// on three streams with double-buffered staging (the one extra Blk a stage
+// reads past E1 only feeds bits the merge never uses).
 setbwte_status host_insert(setbwte_t h, const void* pos, int gw, const uint8_t* bint,
                            uint64_t n_suf, uint64_t* osb, uint64_t* tot, uint64_t* sb_start,
                            uint64_t m_new) {
@@ -546,27 +590,50 @@ setbwte_status host_insert(setbwte_t h, const void* pos, int gw, const uint8_t* 
     API_CHECK(h, cudaStreamSynchronize(h->stream));
     constexpr uint64_t CS = 1024;  // superblocks per chunk (2^26 symbols, 32 MB of Blks)
     Blk *sin, *sout;
-    API_CHECK(h, ensure(h->stage_in, CS * kBlkPerSb + 8, &sin));
-    API_CHECK(h, ensure(h->stage_out, CS * kBlkPerSb + 8, &sout));
+    // two staging buffers of each kind
+    API_CHECK(h, ensure(h->stage_in, 2 * (CS * kBlkPerSb + 8), &sin));
+    API_CHECK(h, ensure(h->stage_out, 2 * (CS * kBlkPerSb + 8), &sout));
     const uint64_t nin_blk = n_in ? (n_in >> 6) + 1 : 0;
-    for (int64_t c = (int64_t)((nsb - 1) / CS); c >= 0; --c) {
+    // the pipeline starts after everything queued on the main stream
+    API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
+    API_CHECK(h, cudaStreamWaitEvent(h->tier_in, h->ev_start, 0));
+    API_CHECK(h, cudaStreamWaitEvent(h->tier_out, h->ev_start, 0));
+    int q = 0;
+    for (int64_t c = (int64_t)((nsb - 1) / CS); c >= 0; --c, ++q) {
+        const int b = q & 1;
+        Blk* si = sin + b * (CS * kBlkPerSb + 8);
+        Blk* so = sout + b * (CS * kBlkPerSb + 8);
         const uint64_t sa = (uint64_t)c * CS, sbe = std::min(nsb, sa + CS);
         const uint64_t O0 = sa << kSbShift, Oe = std::min(sbe << kSbShift, n_out);
         const uint64_t E0 = O0 - h->h_sb_start[sa];
         const uint64_t E1 = std::min(n_in, Oe - h->h_sb_start[sbe]);
         uint64_t bE0 = 0, bE1 = 0;
+        // stage the chunk's input once the merge two chunks back released si
+        if (q >= 2) API_CHECK(h, cudaStreamWaitEvent(h->tier_in, h->ev_merged[b], 0));
         if (E1 > E0) {
             bE0 = E0 >> 6;
             bE1 = std::min(((E1 - 1) >> 6) + 2, nin_blk);
-            API_CHECK(h, cudaMemcpyAsync(sin, h->hdict + bE0, (bE1 - bE0) * sizeof(Blk),
-                                         cudaMemcpyHostToDevice, h->stream));
+            API_CHECK(h, cudaMemcpyAsync(si, h->hdict + bE0, (bE1 - bE0) * sizeof(Blk),
+                                         cudaMemcpyHostToDevice, h->tier_in));
         }
-        API_CHECK(h, launch_insert_range(h->prof, h->stream, make_dict(sin - bE0), n_in, pos, gw, bint, n_suf,
-                                         sout - (sa << (kSbShift - 6)), tot, sb_start, sa, sbe));
+        API_CHECK(h, cudaEventRecord(h->ev_staged[b], h->tier_in));
+        // merge once staged and once the write-back two chunks back released so
+        API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_staged[b], 0));
+        if (q >= 2) API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_written[b], 0));
+        API_CHECK(h, launch_insert_range(h->prof, h->stream, make_dict(si - bE0), n_in, pos, gw,
+                                         bint, n_suf, so - (sa << (kSbShift - 6)), tot, sb_start,
+                                         sa, sbe));
+        API_CHECK(h, cudaEventRecord(h->ev_merged[b], h->stream));
+        // write back
         const uint64_t b0 = sa << (kSbShift - 6), b1 = std::min(sbe << (kSbShift - 6), nblk);
-        API_CHECK(h, cudaMemcpyAsync(h->hdict + b0, sout, (b1 - b0) * sizeof(Blk),
-                                     cudaMemcpyDeviceToHost, h->stream));
+        API_CHECK(h, cudaStreamWaitEvent(h->tier_out, h->ev_merged[b], 0));
+        API_CHECK(h, cudaMemcpyAsync(h->hdict + b0, so, (b1 - b0) * sizeof(Blk),
+                                     cudaMemcpyDeviceToHost, h->tier_out));
+        API_CHECK(h, cudaEventRecord(h->ev_written[b], h->tier_out));
     }
+    // the main stream joins the write-backs (later kernels read the host dictionary)
+    API_CHECK(h, cudaEventRecord(h->ev_start, h->tier_out));
+    API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
     API_CHECK(h, launch_sb_scan(h->prof, h->stream, tot, nsb, osb, m_new, (uint64_t*)h->d_C.p));
     return SETBWTE_OK;
 }
@@ -1364,6 +1431,13 @@ setbwte_status setbwte_create(const char* alphabet, setbwte_t* out) {
             e = cudaStreamCreateWithPriority(&h->lane_stream[l], cudaStreamNonBlocking, prio_high);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->tier_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->tier_out, cudaStreamNonBlocking);
+    for (int b = 0; b < 2; ++b) {
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_staged[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_merged[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_written[b], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->derr_host, sizeof(DevErr), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
     for (int l = 0; l < setbwte_s::kMaxLanes; ++l) {
@@ -1404,7 +1478,16 @@ void setbwte_destroy(setbwte_t h) {
     for (DevBuf* b : pooled_bufs(h)) free_buf(*b);
     free_buf(h->shard_buf[0]);
     free_buf(h->shard_buf[1]);
-    if (h->hdict) cudaFreeHost(h->hdict);
+    if (h->tier_in) cudaStreamSynchronize(h->tier_in);
+    if (h->tier_out) cudaStreamSynchronize(h->tier_out);
+    host_dict_free(h);
+    for (int b = 0; b < 2; ++b) {
+        if (h->ev_staged[b]) cudaEventDestroy(h->ev_staged[b]);
+        if (h->ev_merged[b]) cudaEventDestroy(h->ev_merged[b]);
+        if (h->ev_written[b]) cudaEventDestroy(h->ev_written[b]);
+    }
+    if (h->tier_in) cudaStreamDestroy(h->tier_in);
+    if (h->tier_out) cudaStreamDestroy(h->tier_out);
     for (cudaStream_t ls : h->lane_stream)
         if (ls) cudaStreamSynchronize(ls);
     if (h->ev_start) cudaEventDestroy(h->ev_start);

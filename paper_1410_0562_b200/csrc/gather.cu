@@ -171,11 +171,12 @@ __global__ void __launch_bounds__(kGbNt) gb_part_kernel(const uint32_t* __restri
 }
 
 // tmp2[k] = g[slot[k]] in k order (the g reads stay inside one bucket's
-// slice).  ONE wave of CTAs (148 x 8 resident) walking k with the grid
-// stride: every CTA is at about the same k, so the reads at any moment fall
-// in one or two buckets.  (A 4x-unrolled version with 2 waves of CTAs read
-// 12.4 GB of DRAM per c3 block instead of 1.1 GB: its concurrent reads
-// spanned the whole array -- ncu, profiles/.)
+// slice).  ONE wave of CTAs (148 x 8 resident), one element per thread per
+// step, walking k with the grid stride.  Measured (ncu, c3 block, 2^27
+// suffixes): this form reads 1.1 GB of DRAM at 61 % L2 hits; a 4x-unrolled
+// grid-stride form with two waves of CTAs read 12.4 GB, and 4 loads per
+// thread inside per-CTA chunks of 1024 read 11.3 GB -- more loads in flight
+// per thread defeat the L2 reuse on this part.
 template <class G>
 __global__ void __launch_bounds__(256) gb_fetch_kernel(const uint32_t* __restrict__ slot,
                                                        const G* __restrict__ g, uint32_t n,
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) gb_final_kernel(
         if (v) {
             const uint32_t e = __ldcs(sa + i);
             const uint64_t k = (uint64_t)__ldcs(pos + i);
-            uint64_t gvv = (uint64_t)__ldcs(gv_b + k);
+            uint64_t gvv = (uint64_t)__ldg(gv_b + k);  // evict-normal: neighbours reuse the sector
             const uint8_t bg = (uint8_t)(gvv >> 56);
             if (bing) gvv &= (1ull << 56) - 1ull;
             pv = gvv + i;

@@ -65,9 +65,10 @@ constexpr int kDigTile = kDigNt * kDigIpt;
 // BIT2..BIT16: 33..512 members whose unknown key bits fit in 16 (keys valid,
 // shift <= 8): one warp sorts 32*NIT packed (key bits, index) u32 values with a
 // register bitonic network.  SMALL: the other 33..512 segments (warp LSD radix).
-// LOCALD: 513..4096 members with valid keys (one digit pass left in the word):
-// the whole digit pass of the segment in one CTA (local_digit_kernel).
-enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, LOCALD, NCLASS };
+// LOCALD2 / LOCALD: 513..2048 / 2049..4096 members with valid keys: the
+// whole digit pass of the segment in one CTA (local_digit_kernel<256 / 512>).
+enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, LOCALD, LOCALD2,
+       NCLASS };
 // misc counters
 enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_ACTIVE_LOC,
        M_N };
@@ -138,7 +139,7 @@ __host__ __device__ __forceinline__ int class_of(const Seg& c) {
     // > 512 with valid keys: one more digit pass is cheaper than a CTA-wide
     // sort (measured on c3's ~2048-member second-pass buckets); up to one
     // tile it runs inside one CTA (no histogram / scan kernels)
-    if ((c.meta >> 9) & 1) return c.len <= kCapM ? LOCALD : LARGE;
+    if ((c.meta >> 9) & 1) return c.len <= 2048 ? LOCALD2 : c.len <= kCapM ? LOCALD : LARGE;
     return c.len <= 1024 ? MED1K : c.len <= 2048 ? MED2K : c.len <= kCapM ? MEDIUM : LARGE;
 }
 __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
@@ -893,28 +894,35 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
 // others become child segments, keyed on the next digit (or the next word
 // at shift 0).
 // ---------------------------------------------------------------------------
-constexpr int kLocNt = 512;
 constexpr int kLocIpt = 8;
-static_assert(kLocNt * kLocIpt == (int)kCapM, "one tile per LOCALD segment");
 
+template <int NT>
 constexpr size_t local_digit_smem() {
-    return (size_t)(kLocNt / 32) * 256 * 4 + 2 * (size_t)kCapM * 8 + 260 * 4 + 32 * 4 + 256 + 64;
+    return (size_t)(NT / 32) * 256 * 4 + 2 * (size_t)(NT * kLocIpt) * 8 + 260 * 4 + 32 * 4 + 256 +
+           64;
 }
 
-__global__ void __launch_bounds__(kLocNt, 2) local_digit_kernel(Lists in, Lists out, Bufs B,
-                                                                 uint32_t* misc) {
+// NT = 512: LOCALD (tile 4096); NT = 256: LOCALD2 (tile 2048)
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Lists out, Bufs B,
+                                                                   uint32_t* misc) {
+    constexpr int kLocNt = NT;
+    constexpr uint32_t kTileL = NT * kLocIpt;
+    constexpr int NWL = NT / 32;
+    constexpr int DPW = 256 / NWL;  // digits per warp in the small-bucket finish (16 or 32)
+    constexpr int CLS = NT == 512 ? LOCALD : LOCALD2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem_raw);                   // NW*256
-    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + (kLocNt / 32) * 256);       // kCapM: sorted
-    uint2* s_in = s_kv + kCapM;                                               // kCapM: as loaded
-    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_in + kCapM);             // 257
+    uint2* s_kv = reinterpret_cast<uint2*>(wcnt + (kLocNt / 32) * 256);       // tile: sorted
+    uint2* s_in = s_kv + kTileL;                                              // tile: as loaded
+    uint32_t* dstart = reinterpret_cast<uint32_t*>(s_in + kTileL);            // 257
     uint32_t* tmp = dstart + 260;                                             // 32
     uint8_t* fin = reinterpret_cast<uint8_t*>(tmp + 32);                      // 256
     __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
-    const uint32_t n = in.cnt[LOCALD];
+    const uint32_t n = in.cnt[CLS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
-        const Seg s = in.seg[LOCALD][si];
+        const Seg s = in.seg[CLS][si];
         const uint32_t shift = meta_shift(s.meta), buf = meta_buf(s.meta);
         const bool iota = meta_iota(s.meta);
         const uint32_t* S = B.sa[buf] + s.start;
@@ -970,15 +978,23 @@ __global__ void __launch_bounds__(kLocNt, 2) local_digit_kernel(Lists in, Lists 
         }
         __syncthreads();
         if (cls >= 0) out.seg[cls][cbase[cls] + local] = c;
-        // the small buckets: warp w takes digits [16w, 16w+16) in order and
-        // packs consecutive buckets into its 32 lanes (tiny_kernel's scheme)
+        // the small buckets: warp w takes digits [DPW*w, DPW*w + DPW) in
+        // order and packs consecutive buckets into its 32 lanes (tiny_kernel's
+        // scheme); lane q holds digit q's size and start, broadcast by shuffles
         {
+            uint32_t my_tot = 0, my_start = 0;
+            if (lane < (uint32_t)DPW) {
+                const uint32_t d = warp * DPW + lane;
+                my_start = dstart[d];
+                my_tot = fin[d] == 2 ? dstart[d + 1] - my_start : 0u;
+            }
+            uint32_t todo = __ballot_sync(0xFFFFFFFFu, my_tot != 0);
             uint32_t lb = 0, dstp = 0, slot = 0, key = 0, grp = 0;
             bool mine = false;
-            for (uint32_t q = 0; q <= 16; ++q) {
-                const uint32_t d = warp * 16 + q;
-                const uint32_t tot = (q < 16 && fin[d] == 2) ? dstart[d + 1] - dstart[d] : 0u;
-                if (q == 16 || lb + tot > 32) {
+            while (true) {
+                const uint32_t q = todo ? (uint32_t)(__ffs(todo) - 1) : 32u;
+                const uint32_t tot = q < 32 ? __shfl_sync(0xFFFFFFFFu, my_tot, q) : 0u;
+                if (q == 32 || lb + tot > 32) {
                     if (lb) {
                         uint32_t r;
                         if (shift > 0) {
@@ -996,19 +1012,19 @@ __global__ void __launch_bounds__(kLocNt, 2) local_digit_kernel(Lists in, Lists 
                     }
                     lb = 0;
                     mine = false;
-                    if (q == 16) break;
+                    if (q == 32) break;
                 }
-                if (tot) {
-                    if (lane >= lb && lane < lb + tot) {
-                        dstp = dstart[d] + (lane - lb);
-                        const uint2 kv = s_kv[dstp];
-                        key = kv.x;
-                        slot = kv.y;
-                        grp = lb;
-                        mine = true;
-                    }
-                    lb += tot;
+                const uint32_t st0 = __shfl_sync(0xFFFFFFFFu, my_start, q);
+                if (lane >= lb && lane < lb + tot) {
+                    dstp = st0 + (lane - lb);
+                    const uint2 kv = s_kv[dstp];
+                    key = kv.x;
+                    slot = kv.y;
+                    grp = lb;
+                    mine = true;
                 }
+                lb += tot;
+                todo &= todo - 1;
             }
         }
         // write-out in segment order: finished buckets to the final SA, the
@@ -1602,7 +1618,8 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
                                 n / 257 + 1, n / 33 + 1,   n / 513 + 1,  n / 1025 + 1,
                                 n / 2049 + 1, n / (kCapM + 1) + 2,   // LARGE: > 4096
-                                n / (kCapS + 1) + 1};                // LOCALD: 513..4096 (kv)
+                                n / 2049 + 1,                        // LOCALD: 2049..4096 (kv)
+                                n / (kCapS + 1) + 1};                // LOCALD2: 513..2048 (kv)
     const size_t max_large = cap[LARGE];
     const size_t max_chunks = n / kMinChunk + max_large + 1;
     uint32_t *sa0, *sa1, *k0, *k1, *hist, *ctr;
@@ -1664,9 +1681,12 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     SB_CHECK(cudaFuncSetAttribute(local_kernel<2048, 256>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m2));
     constexpr size_t sm_d = scatter_smem<kDigIpt>();
-    constexpr size_t sm_ld = local_digit_smem();
-    SB_CHECK(cudaFuncSetAttribute(local_digit_kernel,
+    constexpr size_t sm_ld = local_digit_smem<512>();
+    constexpr size_t sm_ld2 = local_digit_smem<256>();
+    SB_CHECK(cudaFuncSetAttribute(local_digit_kernel<512>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ld));
+    SB_CHECK(cudaFuncSetAttribute(local_digit_kernel<256>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ld2));
     SB_CHECK(cudaFuncSetAttribute(local_kernel<kCapM, kNtM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
     SB_CHECK(cudaFuncSetAttribute(digit_scatter_kernel<kDigIpt>,
@@ -1740,12 +1760,18 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                                                   sm_m2, s>>>(in, out, MED2K, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
+        // algorithmic bytes: the digit pass's read + write of (key, slot) per
+        // member (16 B, added with the round's active count below)
         if (cnt[LOCALD]) {
-            // algorithmic bytes: the digit pass's read + write of (key, slot)
-            // per member (16 B, added with the round's active count below)
             SB_LAUNCH(prof, s, "sort_local_digit", 0, 0,
-                      (local_digit_kernel<<<std::min<uint32_t>(cnt[LOCALD], 148u * 2u * 4u),
-                                            kLocNt, sm_ld, s>>>(in, out, B, misc)));
+                      (local_digit_kernel<512><<<std::min<uint32_t>(cnt[LOCALD], 148u * 2u * 4u),
+                                                 512, sm_ld, s>>>(in, out, B, misc)));
+            SB_CHECK(cudaGetLastError());
+        }
+        if (cnt[LOCALD2]) {
+            SB_LAUNCH(prof, s, "sort_local_digit", 0, 0,
+                      (local_digit_kernel<256><<<std::min<uint32_t>(cnt[LOCALD2], 148u * 4u * 4u),
+                                                 256, sm_ld2, s>>>(in, out, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
         if (cnt[MEDIUM]) {

@@ -323,7 +323,28 @@ def test_host_tier_multichunk(SetBWTE):
     idx = SetBWTE(A, block_suffixes=1 << 24)
     idx.set_option("hbm_budget_bytes", 1 << 20)
     idx.append(d, o)
-    assert idx.stats()["host_tier"] == 1
+    st = idx.stats()
+    assert st["host_tier"] == 1
+    assert idx.bwt() == want
+    # <= 3 n log(sigma) bits of system memory = 0.75 B/symbol for
+    # sigma = 4 (1.5x growth of 4 bits/symbol), +2 MB mapping granularity
+    assert st["host_dict_bytes"] <= 0.75 * st["n"] + (4 << 20)
+
+
+def test_host_tier_growth_keeps_content_and_bound(SetBWTE):
+    """Many appends into a host-tier index: the pinned dictionary grows in
+    place (mremap) several times, pipelined multi-chunk Inserts each time."""
+    d, o = synth.uniform(900_000, 100, seed=22)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 22)
+    idx.set_option("host_tier", 1)
+    m = len(o) - 1
+    oo = np.asarray(o, dtype=np.uint64)
+    cuts = [0, 1000, 20_000, 100_000, 300_000, m]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        idx.append(d[int(oo[a]):int(oo[b])], oo[a:b + 1] - oo[a])
+        st = idx.stats()
+        assert st["host_dict_bytes"] <= 0.75 * st["n"] + (4 << 20)
     assert idx.bwt() == want
 
 

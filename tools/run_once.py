@@ -17,6 +17,7 @@ ap.add_argument("--M", type=int, default=1 << 24)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--genome", type=int, default=0)
 ap.add_argument("--var", action="store_true", help="c4-style read lengths U[1000, 10000]")
+ap.add_argument("--option", action="append", default=[], help="library option key=value")
 a = ap.parse_args()
 if a.var:
     d, o = synth.uniform_var(a.reads, 1000, 10000, seed=1)
@@ -27,6 +28,9 @@ else:
 dd = torch.from_numpy(d).cuda()
 do = torch.from_numpy(o.view(np.int64)).cuda()
 idx = SetBWTE("ACGT", block_suffixes=a.M)
+for kv in a.option:
+    k, v = kv.split("=", 1)
+    idx.set_option(k, int(v))
 for _ in range(a.repeat):
     idx.clear()
     idx.append_device(dd, do)
