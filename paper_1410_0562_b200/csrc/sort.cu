@@ -921,22 +921,40 @@ __global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Li
     __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
     const uint32_t n = in.cnt[CLS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    // the next segment's (key, slot) are fetched into s_in with cp.async
+    // while this one is finished (each thread copies exactly the elements it
+    // reads back: no barrier needed for the copies themselves)
+    auto prefetch = [&](uint32_t si2) {
+        if (si2 >= n) return;
+        const Seg s2 = in.seg[CLS][si2];
+        const uint32_t b2 = meta_buf(s2.meta);
+        const bool io2 = meta_iota(s2.meta);
+#pragma unroll
+        for (int it = 0; it < kLocIpt; ++it) {
+            const uint32_t e = warp * (32 * kLocIpt) + it * 32 + lane;
+            if (e < s2.len) {
+                cp_async4(&s_in[e].x, B.key[b2] + s2.start + e, pol);
+                if (io2) s_in[e].y = sa_entry(B, s2.start + e);
+                else cp_async4(&s_in[e].y, B.sa[b2] + s2.start + e, pol);
+            }
+        }
+        cp_async_commit();
+    };
+    prefetch(blockIdx.x);
     for (uint32_t si = blockIdx.x; si < n; si += gridDim.x) {
         const Seg s = in.seg[CLS][si];
         const uint32_t shift = meta_shift(s.meta), buf = meta_buf(s.meta);
-        const bool iota = meta_iota(s.meta);
-        const uint32_t* S = B.sa[buf] + s.start;
-        const uint32_t* K = B.key[buf] + s.start;
         // (key, slot) wait in shared memory while the digits are ranked
         // (registers hold only digits and ranks: no spills at 2 CTAs/SM)
         uint32_t dig[kLocIpt], dest[kLocIpt];
+        cp_async_wait_all();
 #pragma unroll
         for (int it = 0; it < kLocIpt; ++it) {
             const uint32_t e = warp * (32 * kLocIpt) + it * 32 + lane;
             const bool valid = e < s.len;
-            const uint32_t key = valid ? __ldcs(K + e) : 0u;
-            const uint32_t slot = valid ? (iota ? sa_entry(B, s.start + e) : __ldcs(S + e)) : 0u;
-            s_in[e] = make_uint2(key, slot);
+            const uint32_t key = valid ? s_in[e].x : 0u;
             dig[it] = valid ? ((key >> shift) & 0xFFu) : 0x100u;
         }
         if (tid < NCLASS) ccount[tid] = 0;
@@ -971,6 +989,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Li
         for (int it = 0; it < kLocIpt; ++it)
             if (dig[it] < 256) s_kv[dest[it]] = s_in[warp * (32 * kLocIpt) + it * 32 + lane];
         __syncthreads();
+        prefetch(si + gridDim.x);  // s_in is free again
         if (tid < NCLASS && ccount[tid]) cbase[tid] = atomicAdd(out.cnt + tid, ccount[tid]);
         if (tid == 0) {
             atomicAdd(misc + M_ACTIVE, s.len);

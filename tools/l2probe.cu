@@ -28,6 +28,16 @@ __global__ void fetch_chunk(const uint32_t* __restrict__ slot, const uint32_t* _
 int main(int argc, char** argv) {
     const uint32_t n = 1u << 27;
     const int shift = argc > 1 ? atoi(argv[1]) : 23;
+    if (argc > 2) {
+        cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[2]));
+        size_t v = 0;
+        cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+        printf("set L2 fetch granularity %s -> %zu (%s)\n", argv[2], v, cudaGetErrorString(e));
+    } else {
+        size_t v = 0;
+        cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+        printf("default L2 fetch granularity %zu\n", v);
+    }
     std::vector<uint32_t> h(n);
     std::mt19937_64 rng(1);
     for (uint32_t i = 0; i < n; ++i) h[i] = (uint32_t)(rng() % n);
