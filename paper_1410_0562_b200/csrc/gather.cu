@@ -321,7 +321,9 @@ cudaError_t launch_gather_bucketed(Profiler& prof, cudaStream_t s, const uint32_
                                    const GatherScratch& ws) {
     const uint32_t smask = sa_slot_mask(n_suf, payload_limit);
     const uint32_t nb = (uint32_t)(((uint64_t)(n_suf - 1) >> shift) + 1);
-    const double bytes = (5.375 + 2.0 * gw) * n_suf;
+    // the plain gather's algorithmic bytes (ranks.cu launch_gather): the
+    // random g read counted as one 32-byte sector (g here exceeds L2)
+    const double bytes = (5.375 + 32.0 + gw) * n_suf;
     if (nb <= 32) {
         if (gw == 4)
             return run_bucketed<5, uint32_t>(prof, s, sa, smask, n_suf, shift, nb,

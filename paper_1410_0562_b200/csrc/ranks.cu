@@ -268,8 +268,12 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
                           uint64_t* sb_start, uint64_t nsb, const uint8_t* bslot,
                           uint64_t payload_limit, bool bing, const uint32_t* nbit) {
     const uint32_t smask = sa_slot_mask(n_suf, payload_limit);
-    // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol + term bit)
-    const double bytes = (5.375 + 2.0 * gw) * n_suf;
+    // bytes per suffix: 4 (SA) + gw (g) + gw (pos) + 1 (B_int) + 0.375 (symbol
+    // + term bit); when g does not fit in L2 (> 96 MB) the random g read is
+    // one 32-byte sector ("44 B at 32 B-sector granularity if
+    // g misses L2"; the same convention as ComputeRanks' Blk reads)
+    const bool g_l2 = (double)gw * n_suf <= 96.0 * 1024 * 1024;
+    const double bytes = (5.375 + (g_l2 ? (double)gw : 32.0) + gw) * n_suf;
     const unsigned grid = grid_for(n_suf, 256, 148u * 64u);
     if (gw == 4) {
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,

@@ -71,7 +71,7 @@ enum { TINY = 0, BIT2, BIT4, BIT8, BIT16, SMALL, MED1K, MED2K, MEDIUM, LARGE, LO
        NCLASS };
 // misc counters
 enum { M_CHUNKS = 0, M_ACTIVE, M_ELEMS_T, M_ELEMS_S, M_ELEMS_M, M_ELEMS_B, M_GROUPS, M_ACTIVE_LOC,
-       M_N };
+       M_LOOKUPS, M_N };
 
 struct Seg {
     uint32_t start, len, word, meta;  // meta: shift | buf<<8 | keys_valid<<9 | iota<<10
@@ -152,9 +152,12 @@ __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
 // in slot order).  Sorts by key word `word`, then word+1, ... until no ties
 // remain, entirely in registers.  Returns the lane's slot in final order.
 // ---------------------------------------------------------------------------
+// nlook (optional): accumulates (in a register) the key-word lookups
+// (random text reads) made.
 __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint32_t word,
                                                 uint32_t key0, bool have_key, const Bufs& B,
-                                                uint32_t group0 = 0, bool active0 = true) {
+                                                uint32_t group0 = 0, bool active0 = true,
+                                                uint32_t* nlook = nullptr) {
     // Several independent runs may be packed into one call: lanes [g, g+len)
     // of each run carry group0 = g (its first lane); runs never mix.  A lane
     // that is not active (or not valid) is a group of its own.
@@ -165,6 +168,7 @@ __device__ __forceinline__ uint32_t warp_finish(uint32_t slot, uint32_t L, uint3
     for (;;) {
         uint32_t key = 0;
         if (active) key = have_key ? key0 : key_of(B, slot, word);
+        if (nlook && !have_key && active) ++*nlook;
         have_key = false;
         // group extents: [group, gend)
         const uint32_t starts = __ballot_sync(0xFFFFFFFFu, group == lane);
@@ -921,6 +925,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Li
     __shared__ uint32_t ccount[NCLASS], cbase[NCLASS];
     const uint32_t n = in.cnt[CLS];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t nlook = 0;  // this thread's key-word lookups (algorithmic-byte count)
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     // the next segment's (key, slot) are fetched into s_in with cp.async
@@ -1022,9 +1027,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Li
                             uint32_t run;
                             r = warp_sort16(slot, lb, grp, key, shift, tie, run, B.ksyms);
                             if (__any_sync(0xFFFFFFFFu, tie))
-                                r = warp_finish(r, lb, s.word + 1, 0u, false, B, run, tie);
+                                r = warp_finish(r, lb, s.word + 1, 0u, false, B, run, tie,
+                                                &nlook);
                         } else {
-                            r = warp_finish(slot, lb, s.word + 1, 0u, false, B, grp);
+                            r = warp_finish(slot, lb, s.word + 1, 0u, false, B, grp, true,
+                                            &nlook);
                         }
                         SB_ASSERT(!mine || s.start + dstp < B.n);
                         if (mine) B.saf[s.start + dstp] = r;
@@ -1063,6 +1070,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Li
         }
         __syncthreads();
     }
+    // one atomic per warp for the lookup count
+    uint32_t w = nlook;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xFFFFFFFFu, w, o);
+    if (lane == 0 && w) atomicAdd(misc + M_LOOKUPS, w);
 }
 
 
@@ -1914,7 +1926,10 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     const uint64_t act_loc = h_misc[M_ACTIVE_LOC];
     prof.add_bytes("digit_hist", 8.0 * (act_local - act_loc), act_local - act_loc);
     prof.add_bytes("digit_scatter", 16.0 * (act_local - act_loc), act_local - act_loc);
-    prof.add_bytes("sort_local_digit", 16.0 * act_loc, act_loc);
+    // + the key-word lookups of the in-place finish: two random 32-byte
+    // sectors each (a text word pair and a terminator word pair), counted at
+    // sector granularity like ComputeRanks' Blk reads
+    prof.add_bytes("sort_local_digit", 16.0 * act_loc + 64.0 * h_misc[M_LOOKUPS], act_loc);
     prof.add_bytes("sort_tiny", 12.0 * h_misc[M_ELEMS_T], h_misc[M_ELEMS_T]);
     prof.add_bytes("sort_small", 12.0 * h_misc[M_ELEMS_S], h_misc[M_ELEMS_S]);
     prof.add_bytes("sort_medium", 12.0 * h_misc[M_ELEMS_M], h_misc[M_ELEMS_M]);
