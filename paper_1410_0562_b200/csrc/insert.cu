@@ -13,6 +13,10 @@
 // writes the u16 in-superblock counters ("sampled relative counters")
 // and its superblock totals; a second kernel scans the totals into the u64
 // superblock counters ("global counters") and C (Lemma 1).
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "internal.h"
 
 namespace setbwte {
@@ -386,7 +390,9 @@ cudaError_t launch_insert_range(Profiler& prof, cudaStream_t s, const Dict& in_b
     const double frac = (double)nsb_r / (double)((n_out >> kSbShift) + 1);
     const double dsym = n5 ? 0.75 : 0.5;
     const double bytes = frac * (dsym * (double)n_in + dsym * (double)n_out + (gw + 1.0) * (double)n_ins);
-    const unsigned grid = (unsigned)(nsb_r < 148u * 64u ? nsb_r : 148u * 64u);
+    unsigned grid = (unsigned)(nsb_r < 148u * 64u ? nsb_r : 148u * 64u);
+    if (const char* e = getenv("SETBWTE_INSERT_GRID"))
+        grid = std::min<unsigned>(grid, (unsigned)atoi(e));
     if (n5)  // sigma = 5: one plain array (no shards, no host tier)
         SB_CHECK((launch_insert_kernel<const Blk*, true>(prof, s, in_blk.ptr[0], n_in, pos, gw, bint,
                                                          n_ins, out_blk, n_out, sb_tot, sb_start,

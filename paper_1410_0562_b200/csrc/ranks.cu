@@ -17,6 +17,10 @@
 // g and pos are stored as u32 while the index stays below 2^32 symbols and as
 // u64 beyond (G = uint32_t / uint64_t): the narrower g of one block is small
 // enough to stay L2-resident between ComputeRanks and the gather.
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "internal.h"
 
 namespace setbwte {
@@ -171,7 +175,12 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                           (uint64_t*)g, bslot, bing, n5->nbit, n5->nblk, n5->nsb, g_keep)));
         return cudaGetLastError();
     }
-    const unsigned grid = grid_for(nstr, 256, 1u << 20);
+    // ONE wave of 3 CTAs per SM walking the strings with the grid stride:
+    // as fast alone as 5 resident CTAs/SM (the walk is DRAM-bound), and it
+    // leaves SM slots to the sort lanes' kernels running beside it (c3 step
+    // 197.5 -> 188.7 ms, alternated runs)
+    unsigned grid = grid_for(nstr, 256, 148u * 3u);
+    if (const char* e = getenv("SETBWTE_RANK_GRID")) grid = std::min<unsigned>(grid_for(nstr, 256, 1u << 20), (unsigned)atoi(e));
     if (gw == 4) {
         if (blk.P == 1)
             SB_LAUNCH(prof, s, "compute_ranks", bytes, n_steps,
@@ -274,7 +283,8 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
     // g misses L2"; the same convention as ComputeRanks' Blk reads)
     const bool g_l2 = (double)gw * n_suf <= 96.0 * 1024 * 1024;
     const double bytes = (5.375 + (g_l2 ? (double)gw : 32.0) + gw) * n_suf;
-    const unsigned grid = grid_for(n_suf, 256, 148u * 64u);
+    unsigned grid = grid_for(n_suf, 256, 148u * 64u);
+    if (const char* e = getenv("SETBWTE_GATHER_GRID")) grid = std::min<unsigned>(grid, (unsigned)atoi(e));
     if (gw == 4) {
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
                   gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
