@@ -210,7 +210,10 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
 // Fused A2 + A4 (+ the superblock slices Insert needs): pos[i], B_int[i], and
 // sb_start[s] = first i with pos[i] >= s * 2^16 (the "vectorised binary
 // search" of P:158 as one pass: every superblock boundary has one writer).
-template <class G>
+// U consecutive runs of blockDim elements per CTA iteration: U independent
+// random g reads in flight per thread (so fewer threads keep as many reads
+// in flight); a warp's lanes always hold 32 consecutive positions.
+template <class G, int U>
 __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t* __restrict__ term,
                               uint64_t slot_base, const uint32_t* __restrict__ sa,
                               const G* __restrict__ g, uint32_t n_suf, G* __restrict__ pos,
@@ -218,54 +221,67 @@ __global__ void gather_kernel(const uint32_t* __restrict__ text, const uint32_t*
                               uint64_t nsb, const uint8_t* __restrict__ bslot, bool bing,
                               uint32_t smask, const uint32_t* __restrict__ nbit) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t iters = (n_suf + stride - 1) / stride;  // warp-uniform trip count
-    for (uint64_t it = 0; it < iters; ++it) {
-        const uint64_t i = it * stride + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-        const bool v = i < n_suf;
-        uint64_t pv = 0;
-        if (v) {
+    const uint64_t per = (uint64_t)U * blockDim.x;
+    for (uint64_t base = blockIdx.x * per; base < n_suf; base += (uint64_t)gridDim.x * per) {
+        uint32_t e[U];
+        uint64_t gvv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + (uint64_t)u * blockDim.x + threadIdx.x;
             // streaming (evict-first) SA / pos / B_int accesses leave L2 to g
-            const uint32_t e = __ldcs(sa + i);
-            const uint32_t sl = e & smask;
-            SB_ASSERT(sl < n_suf);
-            uint64_t gv = g ? (uint64_t)__ldg(g + sl) : 0ull;
-            const uint8_t bg = (uint8_t)(gv >> 56);
-            if (bing) gv &= (1ull << 56) - 1ull;
-            pv = gv + i;
-            __stcs(pos + i, (G)pv);
-            uint8_t b;
-            if (bing) {
-                b = bg;  // B_int stored in g's top byte by ComputeRanks
-            } else if (smask != 0xFFFFFFFFu) {
-                b = (uint8_t)(e >> kPayloadShift);  // B_int carried by the SA entry
-            } else if (bslot) {
-                b = __ldg(bslot + sl);  // recorded by ComputeRanks
-            } else {
-                const uint64_t p = slot_base + sl;
-                if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
-                else if (nbit && term_bit(nbit, p - 1)) b = 5;
-                else b = (uint8_t)text_sym(text, p - 1);
-            }
-            // B_int byte: code bits 0-1, '$' flag 4; code 4 of sigma = 5 (carried
-            // as 5) is stored like '$' plus the N flag 8 (common.cuh NBlk)
-            if (b == 5) b = 12;
-            __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
+            e[u] = i < n_suf ? __ldcs(sa + i) : 0u;
         }
-        if (sb_start) {
-            uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + (uint64_t)u * blockDim.x + threadIdx.x;
+            SB_ASSERT(i >= n_suf || (e[u] & smask) < n_suf);
+            gvv[u] = (i < n_suf && g) ? (uint64_t)__ldg(g + (e[u] & smask)) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + (uint64_t)u * blockDim.x + threadIdx.x;
+            const bool v = i < n_suf;
+            uint64_t pv = 0;
             if (v) {
-                if (lane == 0 && i > 0) {
-                    const uint32_t sl1 = sa[i - 1] & smask;
-                    uint64_t g1 = g ? (uint64_t)__ldg(g + sl1) : 0ull;
-                    if (bing) g1 &= (1ull << 56) - 1ull;
-                    prev = g1 + (i - 1);
+                const uint32_t sl = e[u] & smask;
+                uint64_t gv = gvv[u];
+                const uint8_t bg = (uint8_t)(gv >> 56);
+                if (bing) gv &= (1ull << 56) - 1ull;
+                pv = gv + i;
+                __stcs(pos + i, (G)pv);
+                uint8_t b;
+                if (bing) {
+                    b = bg;  // B_int stored in g's top byte by ComputeRanks
+                } else if (smask != 0xFFFFFFFFu) {
+                    b = (uint8_t)(e[u] >> kPayloadShift);  // B_int carried by the SA entry
+                } else if (bslot) {
+                    b = __ldg(bslot + sl);  // recorded by ComputeRanks
+                } else {
+                    const uint64_t p = slot_base + sl;
+                    if (sl == 0 || term_bit(term, p - 1)) b = 4;  // '$': suffix starts a string
+                    else if (nbit && term_bit(nbit, p - 1)) b = 5;
+                    else b = (uint8_t)text_sym(text, p - 1);
                 }
-                const uint64_t cur = pv >> kSbShift;
-                const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
-                for (uint64_t s = first; s <= cur && s <= nsb; ++s) sb_start[s] = i;
-                if (i + 1 == n_suf)
-                    for (uint64_t s = cur + 1; s <= nsb; ++s) sb_start[s] = n_suf;
+                // B_int byte: code bits 0-1, '$' flag 4; code 4 of sigma = 5
+                // (carried as 5) is stored like '$' plus the N flag 8 (NBlk)
+                if (b == 5) b = 12;
+                __stcs(reinterpret_cast<signed char*>(bint) + i, (signed char)b);
+            }
+            if (sb_start) {
+                uint64_t prev = __shfl_up_sync(0xFFFFFFFFu, pv, 1);
+                if (v) {
+                    if (lane == 0 && i > 0) {
+                        const uint32_t sl1 = sa[i - 1] & smask;
+                        uint64_t g1 = g ? (uint64_t)__ldg(g + sl1) : 0ull;
+                        if (bing) g1 &= (1ull << 56) - 1ull;
+                        prev = g1 + (i - 1);
+                    }
+                    const uint64_t cur = pv >> kSbShift;
+                    const uint64_t first = i > 0 ? (prev >> kSbShift) + 1 : 0;
+                    for (uint64_t s = first; s <= cur && s <= nsb; ++s) sb_start[s] = i;
+                    if (i + 1 == n_suf)
+                        for (uint64_t s = cur + 1; s <= nsb; ++s) sb_start[s] = n_suf;
+                }
             }
         }
     }
@@ -283,19 +299,19 @@ cudaError_t launch_gather(Profiler& prof, cudaStream_t s, const uint32_t* text,
     // g misses L2"; the same convention as ComputeRanks' Blk reads)
     const bool g_l2 = (double)gw * n_suf <= 96.0 * 1024 * 1024;
     const double bytes = (5.375 + (g_l2 ? (double)gw : 32.0) + gw) * n_suf;
-    unsigned grid = grid_for(n_suf, 256, 148u * 64u);
-    if (const char* e = getenv("SETBWTE_GATHER_GRID")) grid = std::min<unsigned>(grid, (unsigned)atoi(e));
-    if (gw == 4) {
+    // (U = 2 or 4 reads in flight per thread with a 2-8x smaller grid measured
+    // slower on c3: 45-48 vs 42.3 ms)
+    const unsigned grid = grid_for(n_suf, 256, 148u * 64u);
+    if (gw == 4)
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
-                  gather_kernel<uint32_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
-                                                               (const uint32_t*)g, n_suf,
-                                                               (uint32_t*)pos, bint, sb_start, nsb, bslot, false, smask, nbit));
-    } else {
+                  (gather_kernel<uint32_t, 1><<<grid, 256, 0, s>>>(
+                      text, term, slot_base, sa, (const uint32_t*)g, n_suf, (uint32_t*)pos, bint,
+                      sb_start, nsb, bslot, false, smask, nbit)));
+    else
         SB_LAUNCH(prof, s, "gather", bytes, n_suf,
-                  gather_kernel<uint64_t><<<grid, 256, 0, s>>>(text, term, slot_base, sa,
-                                                               (const uint64_t*)g, n_suf,
-                                                               (uint64_t*)pos, bint, sb_start, nsb, bslot, bing, smask, nbit));
-    }
+                  (gather_kernel<uint64_t, 1><<<grid, 256, 0, s>>>(
+                      text, term, slot_base, sa, (const uint64_t*)g, n_suf, (uint64_t*)pos, bint,
+                      sb_start, nsb, bslot, bing, smask, nbit)));
     return cudaGetLastError();
 }
 

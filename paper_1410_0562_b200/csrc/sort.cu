@@ -27,6 +27,8 @@
 //
 // Ties are only ever broken by slot order, which every pass preserves
 // (stable), so the result is the unique SA of the block (reading R15).
+#include <stdlib.h>
+
 #include <algorithm>
 #include <cstring>
 
@@ -1793,6 +1795,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         }
         // algorithmic bytes: the digit pass's read + write of (key, slot) per
         // member (16 B, added with the round's active count below)
+        static const unsigned g_loc2 = getenv("SETBWTE_LOC_GRID") ? (unsigned)atoi(getenv("SETBWTE_LOC_GRID")) : 148u * 4u * 4u;
         if (cnt[LOCALD]) {
             SB_LAUNCH(prof, s, "sort_local_digit", 0, 0,
                       (local_digit_kernel<512><<<std::min<uint32_t>(cnt[LOCALD], 148u * 2u * 4u),
@@ -1801,7 +1804,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         }
         if (cnt[LOCALD2]) {
             SB_LAUNCH(prof, s, "sort_local_digit", 0, 0,
-                      (local_digit_kernel<256><<<std::min<uint32_t>(cnt[LOCALD2], 148u * 4u * 4u),
+                      (local_digit_kernel<256><<<std::min<uint32_t>(cnt[LOCALD2], g_loc2),
                                                  256, sm_ld2, s>>>(in, out, B, misc)));
             SB_CHECK(cudaGetLastError());
         }
@@ -1816,7 +1819,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
                       chunkify_kernel<<<grid_for((uint64_t)cnt[LARGE] * 32, 128), 128, 0, s>>>(
                           in, segx, chunks, groups, misc));
             SB_CHECK(cudaGetLastError());
-            const unsigned g_dig = 148u * 8u;
+            static const unsigned g_dig = getenv("SETBWTE_DIG_GRID") ? (unsigned)atoi(getenv("SETBWTE_DIG_GRID")) : 148u * 8u;
             SB_LAUNCH(prof, s, "digit_hist", 0, 0,
                       digit_hist_kernel<<<g_dig, kDigNt, 0, s>>>(in, chunks, misc, B, hist));
             SB_CHECK(cudaGetLastError());

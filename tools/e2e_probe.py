@@ -1,4 +1,4 @@
-"""Where the end-to-end c2 step's time goes (GPU box): wall-clock of
+"""Where the end-to-end step's time goes (python tools/e2e_probe.py [c2|c3]) (GPU box): wall-clock of
 append_device / append from pinned host / bwt into pinned host / bwt_device."""
 import sys
 import time
@@ -10,7 +10,8 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_1410_0562_b200 import SetBWTE  # noqa: E402
 
-data, offsets = bench.gen("c2")
+WL = sys.argv[1] if len(sys.argv) > 1 else "c2"
+data, offsets = bench.gen(WL)
 m = len(offsets) - 1
 dev = torch.device("cuda:0")
 d_data = torch.from_numpy(data).to(dev)
@@ -18,12 +19,12 @@ d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
 pin_data = torch.from_numpy(data).pin_memory()
 pin_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
 np_data, np_off = pin_data.numpy(), pin_off.numpy().view(np.uint64)
-idx = SetBWTE("ACGT", block_suffixes=1 << 24)
+idx = SetBWTE("ACGT", block_suffixes=bench.WORKLOADS[WL][2])
 pin_out = torch.empty(int(offsets[-1]) + m, dtype=torch.uint8).pin_memory()
 d_out = torch.empty_like(pin_out, device=dev)
 
 
-def t(f, reps=12):
+def t(f, reps=4 if WL != "c2" else 12):
     out = []
     for _ in range(reps):
         idx.clear()
@@ -63,7 +64,7 @@ def tb(f, reps=6):
 
 print("bwt pinned host    ", tb(lambda: idx.bwt(pin_out)))
 print("bwt device         ", tb(lambda: idx.bwt_device(d_out)))
-print("torch H2D 108MB    ", tb(lambda: (d_data.copy_(pin_data, non_blocking=True), d_off.copy_(pin_off, non_blocking=True))))
-print("torch D2H 101MB    ", tb(lambda: pin_out.copy_(d_out, non_blocking=True)))
+print("torch H2D inputs   ", tb(lambda: (d_data.copy_(pin_data, non_blocking=True), d_off.copy_(pin_off, non_blocking=True))))
+print("torch D2H BWT      ", tb(lambda: pin_out.copy_(d_out, non_blocking=True)))
 import os
 print("cpus", os.cpu_count(), "load", os.getloadavg())
