@@ -796,3 +796,21 @@ def test_bucketed_gather_multi_tile_blocks(SetBWTE):
             idx.set_option("g_width", 8)
         idx.append(d, o)
         assert idx.bwt() == want
+
+
+def test_third_level_counting_path(SetBWTE):
+    """One block of 40 M suffixes (400k x 100 bp, M = 2^26): after two 8-bit
+    digit passes the segments hold ~600 members with 16 key bits left -- the
+    one-CTA pass's 11-bit counting placement (sort.cu FAST PATH), whose
+    in-bucket order is restored by original position.  Whole BWT vs the
+    oracle, plus a genome-sampled set whose deep ties take the stable path."""
+    d, o = synth.uniform(400_000, 100, seed=31)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 26)
+    idx.append(d, o)
+    assert idx.bwt() == want
+    d, o = synth.genome_sampled(400_000, 100, 8_000_000, seed=32)
+    want = oracle.bwt(A, d, o, threads=None)
+    idx = SetBWTE(A, block_suffixes=1 << 26)
+    idx.append(d, o)
+    assert idx.bwt() == want
