@@ -408,6 +408,12 @@ inline N5Dict cur_n5(setbwte_t h, const uint32_t* nbit = nullptr) {
 // The current B_ext Blks as a (possibly sharded) Dict.
 inline Dict cur_dict(setbwte_t h) { return h->sharded ? h->shard_dict : make_dict(cur_blk(h)); }
 
+// B_ext's dictionary (4 bits/symbol) larger than ~half the L2: ComputeRanks'
+// LF walk is DRAM-bound rather than L2-latency-bound.
+// (Not the host tier: its zero-copy walk is PCIe-latency-bound and wants every
+// read in flight it can get.)
+inline bool dict_beyond_l2(setbwte_t h) { return !h->host_tier && (h->n >> 1) > (64ull << 20); }
+
 // True when the running appends split ComputeRanks across ranks.
 inline bool partitioned(setbwte_t h) { return h->world > 1 || h->force_exchange; }
 
@@ -466,7 +472,8 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
         API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, j0, j1,
                                           slot_base, cur_dict(h), cur_sb(h),
                                           (const uint64_t*)h->d_C.p, h->prepending ? 0 : h->m,
-                                          n_suf - (j1 - j0), g, gw, bslot, bing, n5p));
+                                          n_suf - (j1 - j0), g, gw, bslot, bing, n5p,
+                                          dict_beyond_l2(h)));
         return SETBWTE_OK;
     }
     // data-parallel over strings: balanced slices by suffix count
@@ -490,7 +497,7 @@ setbwte_status compute_ranks_for(setbwte_t h, const Packed& pk, uint64_t j0, uin
     API_CHECK(h, launch_compute_ranks(h->prof, h->stream, pk.text, pk.slot_off, a, b, slot_base,
                                       cur_dict(h), cur_sb(h), (const uint64_t*)h->d_C.p,
                                       h->prepending ? 0 : h->m, steps, g, gw, nullptr,
-                                      false, n5p));
+                                      false, n5p, dict_beyond_l2(h)));
     std::vector<uint64_t> bytes(P);
     for (int r = 0; r < P; ++r) bytes[r] = (uint64_t)gw * (slot_of[r + 1] - slot_of[r]);
     return exchange(h, g, bytes.data());
@@ -1204,7 +1211,13 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
     // host input: the bytes start travelling now, in chunks, while the
     // offsets are checked and the blocks partitioned (they do not depend on
     // either); each block's packing waits for the chunks covering it
-    const uint64_t chunk = std::max<uint64_t>(16ull << 20, (n_bytes + 7) / 8);
+    // chunks of n/32, between 16 and 64 MB: the first block starts after its
+    // first chunk (~1 ms at PCIe speed) instead of after 1/8 of the input
+    static const uint64_t max_chunk =
+        getenv("SETBWTE_H2D_CHUNK_MB") ? (uint64_t)atoll(getenv("SETBWTE_H2D_CHUNK_MB")) << 20
+                                       : 64ull << 20;
+    const uint64_t chunk =
+        std::max<uint64_t>(16ull << 20, std::min<uint64_t>(max_chunk, (n_bytes + 31) / 32));
     const uint64_t n_chunks = host_bytes && n_bytes ? (n_bytes + chunk - 1) / chunk : 0;
     if (n_chunks) {
         while (h->ev_chunk.size() < n_chunks) {

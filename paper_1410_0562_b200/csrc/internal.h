@@ -236,7 +236,7 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
                                  int gw, uint8_t* bslot = nullptr, bool bing = false,
-                                 const N5Dict* n5 = nullptr);
+                                 const N5Dict* n5 = nullptr, bool one_wave = false);
 // g / pos element width gw = 4 (u32, index < 2^32 symbols) or 8 (u64).
 // Blocks without the SA payload get B_int from ComputeRanks: bslot (one byte
 // per slot) with u32 g, or bing = the top byte of each u64 g.

@@ -151,7 +151,8 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                                  const uint64_t* slot_off, uint64_t j0, uint64_t j1,
                                  uint64_t slot_base, const Dict& blk, const uint64_t* sb,
                                  const uint64_t* d_C, uint64_t m_ext, uint64_t n_steps, void* g,
-                                 int gw, uint8_t* bslot, bool bing, const N5Dict* n5) {
+                                 int gw, uint8_t* bslot, bool bing, const N5Dict* n5,
+                                 bool one_wave) {
     if (j1 <= j0) return cudaSuccess;
     // algorithmic bytes per LF step (= base): one 32 B Blk sector + one 8 B
     // superblock counter + g write + 0.25 B packed symbol; per string: 16 B
@@ -175,11 +176,12 @@ cudaError_t launch_compute_ranks(Profiler& prof, cudaStream_t s, const uint32_t*
                           (uint64_t*)g, bslot, bing, n5->nbit, n5->nblk, n5->nsb, g_keep)));
         return cudaGetLastError();
     }
-    // ONE wave of 3 CTAs per SM walking the strings with the grid stride:
-    // as fast alone as 5 resident CTAs/SM (the walk is DRAM-bound), and it
-    // leaves SM slots to the sort lanes' kernels running beside it (c3 step
-    // 197.5 -> 188.7 ms, alternated runs)
-    unsigned grid = grid_for(nstr, 256, 148u * 3u);
+    // one_wave (a dictionary larger than L2): ONE wave of 3 CTAs per SM
+    // walking the strings with the grid stride -- as fast alone as 5 resident
+    // CTAs/SM (the walk is DRAM-bound), and it leaves SM slots to the sort
+    // lanes' kernels beside it (c3 step 197.5 -> 188.7 ms, alternated runs).
+    // An L2-resident dictionary (c2) is latency-bound: every CTA it can get.
+    unsigned grid = grid_for(nstr, 256, one_wave ? 148u * 3u : 1u << 20);
     if (const char* e = getenv("SETBWTE_RANK_GRID")) grid = std::min<unsigned>(grid_for(nstr, 256, 1u << 20), (unsigned)atoi(e));
     if (gw == 4) {
         if (blk.P == 1)

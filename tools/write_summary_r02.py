@@ -20,13 +20,16 @@ N_C3 = 134217789  # suffixes of a full c3 block (2^27 + the last string)
 
 # tools/make_profiles_r02.sh's ncu --set full captures (tools/prof_c3.sh order)
 CAPTURES = [("sort_local_digit", "local_digit_kernel<256> of block 0 (its third digit level, "
-             "~2048-member segments)", 16.0 * N_C3),
-            ("gather", "block 8", (5.375 + 8.0) * N_C3),
+             "~2048-member segments; DRAM bytes as captured)", None),
+            ("gather", "block 8", (5.375 + 32.0 + 4.0) * N_C3),  # g read as one 32 B sector
             ("compute_ranks", "block 8", None),
             ("digit_scatter", "second 8-bit pass of block 0", 16.0 * N_C3),
             ("insert", "block 10", None),
             ("digit_hist", "second pass of block 0", 8.0 * N_C3),
             ("pack", "block 5", 1.375 * N_C3)]
+
+
+KEEP_REPORTS = (0, 1, 2)  # local_digit, gather, compute_ranks
 
 
 def sh(cmd):
@@ -81,7 +84,7 @@ def main():
         tab = sh([sys.executable, os.path.join(ROOT, "tools", "summarize_launches.py"), lc])
         md += ["## Per-kernel share of one c3 step (ncu launch list of `bench.py --steps 2 --warmup 3 "
                "--no-cpu-baseline`; cold-cache, serialised)", "",
-               "Raw list: `profiles/%s_launches.csv`." % (r + "_launches"), "", tab, ""]
+               "Raw list: `profiles/%s_launches.csv`." % r, "", tab, ""]
     md += ["## ncu --set full, one launch each (c3, `tools/prof_c3.sh`)", "", "```"]
     traffic = {}
     tpath = os.path.join(PROF, "traffic.json")
@@ -92,8 +95,8 @@ def main():
         if not os.path.exists(rep):
             continue
         md.append(brief(rep).rstrip())
-        dst = os.path.join(PROF, "%s_full_%d.ncu-rep" % (r, i))
-        shutil.copy(rep, dst)
+        if i in KEEP_REPORTS:  # the largest reports stay in gpurun_out/ only
+            shutil.copy(rep, os.path.join(PROF, "%s_full_%d.ncu-rep" % (r, i)))
         dram, t = dram_bytes(rep)
         if dram:
             ent = {"dram_bytes_per_launch": dram, "launch": "c3 %s, ncu --set full %s_full_%d" % (
