@@ -141,23 +141,31 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
         const uint64_t i_lo = sb_start[sbi], i_hi = sb_start[sbi + 1];
         const bool staged = i_hi - i_lo <= kStage;
         // pass 1 (coalesced): inserted symbols per output word, staged entries;
-        // four independent loads in flight per thread
-        for (uint64_t i0 = i_lo + tid; i0 < i_hi; i0 += 4 * kInsNt) {
+        // four independent loads in flight per thread while four whole rounds
+        // of the CTA remain, then one element per round (a late c3 block has
+        // ~4400 per superblock: unconditional 4-wide rounds wasted half the
+        // issue slots on predicated-off elements)
+        uint64_t i0 = i_lo + tid;
+        for (; i0 + 3ull * kInsNt < i_hi; i0 += 4 * kInsNt) {
             uint32_t rel[4], bb[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint64_t i = i0 + (uint64_t)u * kInsNt;
-                rel[u] = i < i_hi ? (uint32_t)((uint64_t)__ldg(pos + i) - o0) : 0u;
-                bb[u] = (i < i_hi && staged) ? (uint32_t)__ldg(bint + i) : 0u;
+                rel[u] = (uint32_t)((uint64_t)__ldg(pos + i) - o0);
+                bb[u] = staged ? (uint32_t)__ldg(bint + i) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint64_t i = i0 + (uint64_t)u * kInsNt;
-                if (i < i_hi) {
-                    atomicAdd(&wcnt[rel[u] >> 6], 1u);
-                    if (staged) ent[i - i_lo] = (uint16_t)((rel[u] & 63u) | (bb[u] << 6));
-                }
+                atomicAdd(&wcnt[rel[u] >> 6], 1u);
+                if (staged) ent[i - i_lo] = (uint16_t)((rel[u] & 63u) | (bb[u] << 6));
             }
+        }
+        for (; i0 < i_hi; i0 += kInsNt) {
+            const uint32_t rel = (uint32_t)((uint64_t)__ldg(pos + i0) - o0);
+            const uint32_t bb = staged ? (uint32_t)__ldg(bint + i0) : 0u;
+            atomicAdd(&wcnt[rel >> 6], 1u);
+            if (staged) ent[i0 - i_lo] = (uint16_t)((rel & 63u) | (bb << 6));
         }
         __syncthreads();
         // exclusive scan over the 1024 words (two-level)
