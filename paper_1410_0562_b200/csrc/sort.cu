@@ -90,6 +90,7 @@ struct Group {
 struct Lists {
     Seg* seg[NCLASS];
     uint32_t* cnt;  // NCLASS counters
+    uint32_t local;  // 513..4096-member segments with valid keys take the one-CTA pass
 };
 struct Bufs {
     uint32_t* sa[2];
@@ -131,7 +132,7 @@ __device__ __forceinline__ uint32_t make_meta(uint32_t shift, uint32_t buf, uint
                                               uint32_t iota = 0) {
     return shift | (buf << 8) | (kv << 9) | (iota << 10);
 }
-__host__ __device__ __forceinline__ int class_of(const Seg& c) {
+__host__ __device__ __forceinline__ int class_of(const Seg& c, uint32_t local = 1) {
     if (c.len <= kTiny) return TINY;
     if (c.len <= kCapS) {
         if (((c.meta >> 9) & 1) && (c.meta & 0xFF) <= 8)
@@ -141,11 +142,12 @@ __host__ __device__ __forceinline__ int class_of(const Seg& c) {
     // > 512 with valid keys: one more digit pass is cheaper than a CTA-wide
     // sort (measured on c3's ~2048-member second-pass buckets); up to one
     // tile it runs inside one CTA (no histogram / scan kernels)
-    if ((c.meta >> 9) & 1) return c.len <= 2048 ? LOCALD2 : c.len <= kCapM ? LOCALD : LARGE;
+    if ((c.meta >> 9) & 1)
+        return !local ? LARGE : c.len <= 2048 ? LOCALD2 : c.len <= kCapM ? LOCALD : LARGE;
     return c.len <= 1024 ? MED1K : c.len <= 2048 ? MED2K : c.len <= kCapM ? MEDIUM : LARGE;
 }
 __device__ __forceinline__ void emit(const Lists& out, const Seg& c) {
-    const int k = class_of(c);
+    const int k = class_of(c, out.local);
     out.seg[k][atomicAdd(out.cnt + k, 1u)] = c;
 }
 
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(256) digit_scan_kernel(Lists in, Lists out,
                     c.word = s.word;
                     c.meta = make_meta(shift - 8, cbuf, 1, ciota);
                 }
-                cls = class_of(c);
+                cls = class_of(c, out.local);
                 local = atomicAdd(&ccount[cls], 1u);
                 if (all_one) segx[si].skip = 1;
             }
@@ -988,7 +990,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Li
                     c.word = s.word;
                     c.meta = make_meta(shift - 8, 1u - buf, 1);
                 }
-                cls = class_of(c);
+                cls = class_of(c, out.local);
                 local = atomicAdd(&ccount[cls], 1u);
             }
         }
@@ -1689,6 +1691,11 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
         }
         A.cnt = ctr;
         Bl.cnt = ctr + NCLASS;
+        // the one-CTA digit pass pays on large blocks (c3: the ~2048-member
+        // third level); smaller blocks (c2) keep the global digit passes
+        static const uint64_t local_min =
+            getenv("SETBWTE_LOCAL_MIN") ? (uint64_t)atoll(getenv("SETBWTE_LOCAL_MIN")) : (1ull << 25);
+        A.local = Bl.local = (uint64_t)n >= local_min ? 1u : 0u;
     }
     if (reserve_only) return cudaSuccess;
     Bufs B;
@@ -1740,7 +1747,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
               init_kernel<<<n <= kCapM ? grid_for(n, 256) : 1u, 256, 0, s>>>(sa0, d_sa_final, n_suf, A, Bl, misc, B));
     SB_CHECK(cudaGetLastError());
     uint32_t h_cnt[NCLASS] = {0}, h_oth[NCLASS] = {0};  // counts of in / out
-    if (n > 1) h_cnt[class_of(Seg{0u, (uint32_t)n, 0u, 24u | (1u << 9)})] = 1;
+    if (n > 1) h_cnt[class_of(Seg{0u, (uint32_t)n, 0u, 24u | (1u << 9)}, A.local)] = 1;
     Lists in = A, out = Bl;
     uint32_t prev_active = 0;
     uint32_t h_misc[M_N] = {0};
