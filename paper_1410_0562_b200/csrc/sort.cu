@@ -1652,7 +1652,7 @@ cudaError_t sort_block(Profiler& prof, cudaStream_t s, SortScratch& ws, const ui
     const size_t n = n_suf;
     const size_t cap[NCLASS] = {n / 2 + 1,   n / 33 + 1,   n / 65 + 1,   n / 129 + 1,
                                 n / 257 + 1, n / 33 + 1,   n / 513 + 1,  n / 1025 + 1,
-                                n / 2049 + 1, n / (kCapM + 1) + 2,   // LARGE: > 4096
+                                n / 2049 + 1, n / (kCapS + 1) + 1,   // LARGE: > 512 (kv, small blocks)
                                 n / 2049 + 1,                        // LOCALD: 2049..4096 (kv)
                                 n / (kCapS + 1) + 1};                // LOCALD2: 513..2048 (kv)
     const size_t max_large = cap[LARGE];

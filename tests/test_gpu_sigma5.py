@@ -165,3 +165,24 @@ def test_unsupported_combinations(SetBWTE):
     with pytest.raises(SetBWTEError) as e:
         idx.merge(other)
     assert e.value.name == "E_UNSUPPORTED"
+
+
+@pytest.mark.slow
+def test_c2_size_with_n(SetBWTE):
+    """c2's shape (1M x 100 bp, M = 2^24, K = 7) with 1 % N: every pass of
+    the sort on 3-bit key words at full block size, whole BWT vs the oracle."""
+    d, o = synth.uniform_n(1_000_000, 100, p_n=0.01, seed=3)
+    want = oracle.bwt(A5, d, o, threads=None)
+    idx = build(SetBWTE, d, o, M=1 << 24)
+    assert idx.stats()["blocks"] == 7
+    assert idx.bwt() == want
+
+
+def test_large_block_with_n(SetBWTE):
+    """A 35 M-suffix block with N ranked into a 25 M-symbol index (blocks of
+    >= 2^25 suffixes take the one-CTA digit pass for their ~500-member third
+    level)."""
+    d, o = synth.uniform_n(600_000, 100, p_n=0.02, seed=4)
+    want = oracle.bwt(A5, d, o, threads=None)
+    # the second append (350k reads, 35 M suffixes) is one large block
+    assert build(SetBWTE, d, o, M=1 << 26, splits=[250_000]).bwt() == want
