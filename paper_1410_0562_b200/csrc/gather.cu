@@ -25,8 +25,6 @@
 #include <stdlib.h>
 
 #include <algorithm>
-#include <vector>
-#include <stdio.h>
 
 #include "blockrank.cuh"
 #include "internal.h"
@@ -267,17 +265,6 @@ cudaError_t run_bucketed(Profiler& prof, cudaStream_t s, const uint32_t* sa, uin
               (gb_part_kernel<NB, G><<<grid_t, kGbNt, 0, s>>>(sa, smask, n, shift, nb, ntiles,
                                                               ws.rows, tot, ws.slot, pos)));
     SB_CHECK(cudaGetLastError());
-    if (getenv("SETBWTE_GB_CHECK")) {
-        // debug: is the partition bucket-ordered?
-        SB_CHECK(cudaStreamSynchronize(s));
-        std::vector<uint32_t> hs(n);
-        SB_CHECK(cudaMemcpy(hs.data(), ws.slot, 4ull * n, cudaMemcpyDeviceToHost));
-        uint64_t inv = 0, maxs = 0;
-        for (uint32_t k = 1; k < n; ++k) inv += (hs[k] >> shift) < (hs[k - 1] >> shift);
-        for (uint32_t k = 0; k < n; ++k) maxs = std::max<uint64_t>(maxs, hs[k]);
-        fprintf(stderr, "[gb] n=%u shift=%u nb=%u inversions=%llu max_slot=%llu first=%u,%u,%u\n", n,
-                shift, nb, (unsigned long long)inv, (unsigned long long)maxs, hs[0], hs[1], hs[2]);
-    }
     G* gv_b = reinterpret_cast<G*>(ws.gval);
     SB_LAUNCH(prof, s, "gather_fetch", 0, 0,
               (gb_fetch_kernel<G><<<148u * 8u, 256, 0, s>>>(ws.slot, g, n, gv_b)));
@@ -307,7 +294,6 @@ uint32_t gather_buckets_shift(uint32_t n, int gw, int mode) {
     int shift = gw == 4 ? 23 : 22;
     if (mode == 2) shift = std::max(0, lg - 3);
     shift = std::max(shift, lg - 8);  // <= 256 buckets
-    if (const char* e = getenv("SETBWTE_GB_SHIFT")) shift = std::max(atoi(e), lg - 8);  // experiments
     if (((uint64_t)(n - 1) >> shift) == 0) return 0;  // one bucket: nothing to gain
     return (uint32_t)shift;
 }
