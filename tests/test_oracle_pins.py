@@ -342,3 +342,39 @@ def test_bucketed_matches_oracle_on_reads():
     d, o = synth.uniform(3000, 100, seed=5)
     got, _, _ = _bucketed(A, d, o, 3, 50_000, threads=4)
     assert got == oracle.bwt(A, d, o, threads=4)
+
+
+# --- the golden full-size digests (tools/make_golden_digests.py) ---------------
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_golden_digest_files_are_consistent(cfg):
+    """Self-consistency of the oracle-written digest files: bucket ranges tile
+    [0, n), the symbol counts add up to n with exactly m terminators, the
+    windows lie inside B and agree with the bucket layout's length."""
+    gd = json.load(open(os.path.join(GOLD, "%s_bwt_digest.json" % cfg)))
+    n, m = gd["n"], gd["m"]
+    pos = 0
+    for b in gd["buckets"]:
+        assert b["start"] == pos and b["len"] > 0
+        pos += b["len"]
+    assert pos == n
+    cnt = gd["symbol_counts"]
+    assert sum(cnt.values()) == n and cnt["$"] == m
+    for w in gd["windows"]:
+        assert 0 <= w["start"] and w["start"] + len(w["bytes"]) <= n
+        assert set(w["bytes"]) <= set("$ACGT")
+
+
+def test_golden_c3_digest_against_the_input():
+    """The c3 digest against properties of the INPUT (no oracle call): the
+    BWT's symbol multiset is the input's plus m terminators, and B[0..4096) --
+    the rows of $_0..$_4095 -- are the last symbols of strings 0..4095
+    (SURVEY 8(c) invariants)."""
+    gd = json.load(open(os.path.join(GOLD, "c3_bwt_digest.json")))
+    d, o = synth.uniform(20_000_000, 100, seed=1)
+    assert gd["m"] == len(o) - 1 and gd["n"] == int(o[-1]) + len(o) - 1
+    for c in "ACGT":
+        assert gd["symbol_counts"][c] == int(np.count_nonzero(d == ord(c)))
+    w0 = next(w for w in gd["windows"] if w["start"] == 0)["bytes"].encode()
+    last = d[(o[1:len(w0) + 1] - 1).astype(np.int64)].tobytes()
+    assert w0 == last
