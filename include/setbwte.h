@@ -226,11 +226,12 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *                     never (as for larger blocks: ComputeRanks records B_int
  *                     per slot instead).  Results are identical; the option
  *                     exists so both paths can be tested at small sizes.
- *   "gather_buckets"  how the g -> g_sa gather reads g: 1 (default) = in
+ *   "gather_buckets"  how the g -> g_sa gather (Alg.1) reads g:
+ *                     0 (default) = one random read per suffix; 1 = in
  *                     coalesced bucketed passes (L2-local g reads) when a
- *                     block's g exceeds 96 MB, else one random read per
- *                     suffix; 0 = always the random reads; 2 = always bucketed
- *                     (test hook).  Results identical.
+ *                     block's g exceeds 96 MB; 2 = always bucketed (test
+ *                     hook).  Results identical; the bucketed form moves less
+ *                     DRAM but measured slower end to end.
  *   "force_exchange"  1: (test hook) run the partitioned ComputeRanks and the
  *                     exchange step even with world == 1 (one slice; with a
  *                     communicator, one NCCL broadcast per exchange).
