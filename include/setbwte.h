@@ -66,9 +66,10 @@ typedef enum {
  * "ACGTN" (SPEC S:31's default alphabet); '$' is reserved.  Matching is
  * case-insensitive (reading R10).  sigma <= 4 uses 2-bit symbols; sigma = 5
  * adds a 1-bit plane for the fifth (largest) symbol to the packed text and to
- * the rank dictionary -- with sigma = 5 the host tier,
- * the sharded dictionary, insert_split and setbwte_merge are
- * SETBWTE_E_UNSUPPORTED.  sigma > 5 -> SETBWTE_E_UNSUPPORTED.  Binds the
+ * the rank dictionary -- with sigma = 5 the host tier
+ * (also a dictionary outgrowing hbm_budget_bytes), the sharded dictionary and
+ * setbwte_merge are SETBWTE_E_UNSUPPORTED, and option insert_split falls back
+ * to the replicated Insert.  sigma > 5 -> SETBWTE_E_UNSUPPORTED.  Binds the
  * current CUDA device and creates a private non-blocking stream.  *out
  * receives the handle. */
 setbwte_status setbwte_create(const char* alphabet, setbwte_t* out);
