@@ -312,7 +312,8 @@ setbwte_status setbwte_set_comm(setbwte_t h, void* nccl_comm, int rank, int worl
 setbwte_status setbwte_set_allocator(setbwte_t h, void* (*alloc)(size_t bytes, void* ctx),
                                      void (*free_)(void* ptr, void* ctx), void* ctx);
 
-/* Per-stage statistics of the last append as a NUL-terminated JSON object
+/* Per-stage statistics of the last append (or setbwte_compute_ranks) as a
+ * NUL-terminated JSON object
  * written into HOST buffer out (cap bytes); *n receives the length needed
  * (including NUL).  out == NULL -> size query.  Includes per-kernel launch
  * counts, and (when "profile" is on) per-kernel CUDA-event time and

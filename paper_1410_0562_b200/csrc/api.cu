@@ -1787,6 +1787,7 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
     API_CHECK(h, ensure(h->in_off, m + 1, &dof));
     if (nb) API_CHECK(h, cudaMemcpyAsync(db, strings, nb, cudaMemcpyHostToDevice, h->stream));
     API_CHECK(h, cudaMemcpyAsync(dof, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    h->prof.reset();  // setbwte_stats reports this call's kernels
     PackOut po;
     setbwte_status st = pack_input(h, db, dof, m, &po);
     if (st != SETBWTE_OK) return st;
@@ -1796,6 +1797,8 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
     if (st != SETBWTE_OK) return st;
     API_CHECK(h, cudaMemcpyAsync(g_out, g, n_suf * 8, cudaMemcpyDeviceToHost, h->stream));
     API_CHECK(h, cudaStreamSynchronize(h->stream));
+    API_CHECK(h, h->prof.resolve());
+    build_stats(h);
     return SETBWTE_OK;
 }
 
