@@ -1292,14 +1292,17 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
                                      cudaMemcpyDeviceToHost, h->stream));
         API_CHECK(h, cudaStreamSynchronize(h->stream));
     }
-    // packing, block by block on the pack ("copy") stream, each after its chunks
+    // packing, block by block on the pack ("copy") stream, each after its chunks;
+    // with sort_lanes = 0 (no pipelining: the profiled step) on the main stream,
+    // so every launch is timed alone
+    cudaStream_t ps = h->sort_lanes == 0 ? h->stream : h->copy_stream;
     while (h->ev_packed.size() < K) {
         cudaEvent_t ev;
         API_CHECK(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         h->ev_packed.push_back(ev);
     }
     API_CHECK(h, cudaEventRecord(h->ev_start, h->stream));
-    API_CHECK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_start, 0));
+    API_CHECK(h, cudaStreamWaitEvent(ps, h->ev_start, 0));
     uint64_t waited = 0;  // chunks the pack stream already waits for
     for (uint64_t k = 0; k < K; ++k) {
         if (n_chunks) {
@@ -1308,18 +1311,18 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
             const uint64_t last = std::min(n_bytes, host_off[blocks[k].j1] + 2048);
             const uint64_t need = std::min(n_chunks, (last + chunk - 1) / chunk);
             for (; waited < need; ++waited)
-                API_CHECK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_chunk[waited], 0));
+                API_CHECK(h, cudaStreamWaitEvent(ps, h->ev_chunk[waited], 0));
         }
         const uint64_t g0 = k == 0 ? 0 : blocks[k].S0 >> 5;
         const uint64_t g1 = k + 1 < K ? blocks[k + 1].S0 >> 5 : n_groups;
-        API_CHECK(h, launch_pack_range(h->prof, h->copy_stream, d_bytes, m, n_bytes,
+        API_CHECK(h, launch_pack_range(h->prof, ps, d_bytes, m, n_bytes,
                                        (const uint8_t*)h->d_code_of.p, pk, g0, g1, &derr->err_pos));
-        API_CHECK(h, cudaEventRecord(h->ev_packed[k], h->copy_stream));
+        API_CHECK(h, cudaEventRecord(h->ev_packed[k], ps));
     }
     API_CHECK(h, cudaMemcpyAsync(h->derr_host, derr, sizeof(DevErr), cudaMemcpyDeviceToHost,
-                                 h->copy_stream));
+                                 ps));
     auto validate = [&]() -> setbwte_status {
-        cudaError_t e = cudaStreamSynchronize(h->copy_stream);
+        cudaError_t e = cudaStreamSynchronize(ps);
         if (e != cudaSuccess) return from_cuda(h, e);
         const uint64_t ep = h->derr_host->err_pos;
         if (ep == ~0ull) return SETBWTE_OK;
@@ -1363,7 +1366,7 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
         }
     }
     // the main stream joins the copy stream (the bytes buffer is reused later)
-    API_CHECK(h, cudaEventRecord(h->ev_start, h->copy_stream));
+    API_CHECK(h, cudaEventRecord(h->ev_start, ps));
     API_CHECK(h, cudaStreamWaitEvent(h->stream, h->ev_start, 0));
     if (st != SETBWTE_OK) return st;
     {

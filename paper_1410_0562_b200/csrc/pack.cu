@@ -11,9 +11,11 @@
 namespace setbwte {
 
 // slot_off[j] = offsets[j] + j; flags non-CSR offsets; gfirst[g] = the string
-// owning slot 32g (each string writes the groups that start inside it).
+// owning slot 32g (each string writes the groups that start inside it); the
+// terminator bitmap gets string j's last slot (term must be zero on entry).
 __global__ void slot_off_kernel(const uint64_t* __restrict__ off, uint64_t m, uint64_t n_bytes,
-                                uint64_t* __restrict__ slot_off, uint32_t* __restrict__ gfirst,
+                                uint64_t n_slots, uint64_t* __restrict__ slot_off,
+                                uint32_t* __restrict__ gfirst, uint32_t* __restrict__ term,
                                 int* __restrict__ bad) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= m;
          j += (uint64_t)gridDim.x * blockDim.x) {
@@ -29,23 +31,27 @@ __global__ void slot_off_kernel(const uint64_t* __restrict__ off, uint64_t m, ui
             }
             const uint64_t a = o + j, e = o1 + j + 1;  // slots [a, e)
             for (uint64_t g = (a + 31) >> 5; (g << 5) < e; ++g) gfirst[g] = (uint32_t)j;
+            if (e - 1 < n_slots) atomicOr(term + ((e - 1) >> 5), 1u << (31 - ((e - 1) & 31)));
         }
     }
 }
 
 // One warp per 1024 slots (32 groups of 32): the warp stages the <= 1024
-// ASCII bytes of its slots in shared memory with 16-byte loads, then each lane
-// packs one group: two text words + one terminator word.
+// ASCII bytes of its slots in shared memory with 16-byte loads, then packs
+// the groups one after the other, one slot per lane: a slot's string (hence
+// its byte position, slot minus the terminators before it) comes from the
+// terminator bitmap, and the group's two text words are two warp OR
+// reductions (lane q keeps group q's words for one coalesced store).
 constexpr int kPackWarps = 8;
 __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
-    const uint8_t* __restrict__ bytes, uint64_t n_bytes, const uint64_t* __restrict__ slot_off,
-    const uint32_t* __restrict__ gfirst, uint64_t m, uint64_t n_slots,
-    const uint8_t* __restrict__ code_of_g, uint32_t* __restrict__ text, uint32_t* __restrict__ term,
-    uint32_t* __restrict__ nbit, unsigned long long* __restrict__ err_pos, uint64_t g_begin,
-    uint64_t g_end) {
+    const uint8_t* __restrict__ bytes, uint64_t n_bytes, const uint32_t* __restrict__ gfirst,
+    uint64_t m, uint64_t n_slots, const uint8_t* __restrict__ code_of_g,
+    uint32_t* __restrict__ text, const uint32_t* __restrict__ term, uint32_t* __restrict__ nbit,
+    unsigned long long* __restrict__ err_pos, uint64_t g_begin, uint64_t g_end) {
     // nbit (sigma = 5): code 4 is stored as 2-bit code 0 plus a set nbit bit
     const uint32_t maxc = nbit ? 4u : 3u;
-    __shared__ __align__(16) uint8_t sbuf[kPackWarps][1024 + 80];
+    constexpr uint32_t kWin = 1024 + 80;
+    __shared__ __align__(16) uint8_t sbuf[kPackWarps][kWin];
     __shared__ uint8_t code_of[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) code_of[i] = code_of_g[i];
     __syncthreads();
@@ -56,11 +62,19 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
          wbase < (g_end << 5); wbase += nw << 10) {
         const uint64_t g = (wbase >> 5) + lane;
         const bool gv = g < g_end;
-        uint64_t j = gv ? min((uint64_t)gfirst[g], m - 1) : 0;
-        const uint64_t j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
+        const uint32_t tw = gv ? term[g] : 0u;
+        // terminators before this lane's group, within the warp's 1024 slots
+        uint32_t rel = __popc(tw);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, rel, d);
+            if (lane >= (uint32_t)d) rel += y;
+        }
+        rel -= __popc(tw);
+        const uint64_t j0 = min((uint64_t)gfirst[wbase >> 5], m - 1);
         const uint64_t bp_first = wbase - min(j0, wbase);
         const uint64_t al = bp_first & ~15ull;
-        for (uint32_t k = lane; k < (1024 + 80) / 16; k += 32) {
+        for (uint32_t k = lane; k < kWin / 16; k += 32) {
             const uint64_t a = al + 16ull * k;
             if (a + 16 <= n_bytes) {
                 *reinterpret_cast<uint4*>(sb + 16 * k) = __ldg(reinterpret_cast<const uint4*>(bytes + a));
@@ -69,36 +83,41 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
             }
         }
         __syncwarp();
-        if (gv) {
-            const uint64_t s0 = g << 5;
-            uint64_t next = slot_off[j + 1];
-            uint32_t w0 = 0, w1 = 0, tw = 0, nw5 = 0;
-            const int cnt = (int)min((uint64_t)32, n_slots - s0);
-            for (int t = 0; t < cnt; ++t) {
-                const uint64_t s = s0 + t;
-                while (s >= next && j + 1 < m) {
-                    ++j;
-                    next = slot_off[j + 1];
-                }
-                uint32_t code = 0;
-                if (s == next - 1) {
-                    tw |= 1u << (31 - t);
-                } else {
-                    const uint64_t bp = s - j;  // byte position: slots minus terminators before
-                    const uint64_t li = bp - al;
-                    if (bp < n_bytes && li < 1024 + 80) {
-                        const uint8_t c = code_of[sb[li]];
-                        if (c > maxc) atomicMin(err_pos, (unsigned long long)bp);
-                        else if (c == 4) nw5 |= 1u << (31 - t);
-                        else code = c;
-                    }
-                }
-                if (t < 16) w0 |= code << (30 - 2 * t); else w1 |= code << (30 - 2 * (t - 16));
+        uint32_t my_w0 = 0, my_w1 = 0, my_nb = 0;
+        // window index of slot (q, lane) = its byte position - al, where the
+        // byte position is slot - j0 - terminators before it; 32-bit bounds:
+        // slots below n_slots, bytes below n_bytes and inside the window
+        const uint32_t l0 = (uint32_t)(bp_first - al) + lane;
+        const uint32_t slot_lim = (uint32_t)min(n_slots - min(n_slots, wbase), (uint64_t)1024);
+        const uint32_t win_lim = (uint32_t)min(n_bytes - min(n_bytes, al), (uint64_t)kWin);
+#pragma unroll 4
+        for (uint32_t q = 0; q < 32; ++q) {
+            const uint32_t twq = __shfl_sync(0xFFFFFFFFu, tw, q);
+            const uint32_t relq = __shfl_sync(0xFFFFFFFFu, rel, q);
+            const uint32_t before = lane ? __popc(twq >> (32 - lane)) : 0u;
+            const uint32_t li = l0 + 32u * q - relq - before;
+            const bool is_t = (twq >> (31 - lane)) & 1u;
+            uint32_t code = 0;
+            bool n5 = false;
+            if (!is_t && 32u * q + lane < slot_lim && li < win_lim) {
+                const uint32_t c = code_of[sb[li]];
+                if (c > maxc) atomicMin(err_pos, (unsigned long long)(al + li));
+                else if (c == 4) n5 = true;
+                else code = c;
             }
-            text[2 * g] = w0;
-            text[2 * g + 1] = w1;
-            term[g] = tw;
-            if (nbit) nbit[g] = nw5;
+            const uint32_t v = code << (30 - 2 * (lane & 15));
+            const uint32_t w0 = __reduce_or_sync(0xFFFFFFFFu, lane < 16 ? v : 0u);
+            const uint32_t w1 = __reduce_or_sync(0xFFFFFFFFu, lane < 16 ? 0u : v);
+            const uint32_t nb = __brev(__ballot_sync(0xFFFFFFFFu, n5));
+            if (lane == q) {
+                my_w0 = w0;
+                my_w1 = w1;
+                my_nb = nb;
+            }
+        }
+        if (gv) {
+            reinterpret_cast<uint2*>(text)[g] = make_uint2(my_w0, my_w1);
+            if (nbit) nbit[g] = my_nb;
         }
         __syncwarp();
     }
@@ -106,14 +125,15 @@ __global__ void __launch_bounds__(kPackWarps * 32) pack_kernel(
 
 cudaError_t launch_pack_prepare(Profiler& prof, cudaStream_t s, const uint64_t* d_off, uint64_t m,
                                 uint64_t n_bytes, Packed pk, int* d_bad_offsets) {
-    SB_LAUNCH(prof, s, "slot_offsets", 16.0 * (m + 1), m + 1,
-              slot_off_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(d_off, m, n_bytes, pk.slot_off,
-                                                                   pk.gfirst, d_bad_offsets));
-    SB_CHECK(cudaGetLastError());
     const uint64_t n_groups = (pk.n_slots + 31) >> 5;
+    // the terminator bitmap (and its zero padding) is written here, by bit
+    SB_CHECK(cudaMemsetAsync(pk.term, 0, (n_groups + 4) * sizeof(uint32_t), s));
+    SB_LAUNCH(prof, s, "slot_offsets", 16.0 * (m + 1), m + 1,
+              slot_off_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(
+                  d_off, m, n_bytes, pk.n_slots, pk.slot_off, pk.gfirst, pk.term, d_bad_offsets));
+    SB_CHECK(cudaGetLastError());
     // padding words past the end must read as zero
     SB_CHECK(cudaMemsetAsync(pk.text + 2 * n_groups, 0, 4 * sizeof(uint32_t), s));
-    SB_CHECK(cudaMemsetAsync(pk.term + n_groups, 0, 4 * sizeof(uint32_t), s));
     if (pk.nbit) SB_CHECK(cudaMemsetAsync(pk.nbit + n_groups, 0, 4 * sizeof(uint32_t), s));
     return cudaSuccess;
 }
@@ -127,8 +147,8 @@ cudaError_t launch_pack_range(Profiler& prof, cudaStream_t s, const uint8_t* d_b
     const uint64_t n_warps = ((g_end - g_begin) + 31) >> 5;
     SB_LAUNCH(prof, s, "pack", 1.375 * (double)slots, slots,
               pack_kernel<<<grid_for(n_warps, kPackWarps, 148u * 16u), kPackWarps * 32, 0, s>>>(
-                  d_bytes, n_bytes, pk.slot_off, pk.gfirst, m, pk.n_slots, d_code_of, pk.text,
-                  pk.term, pk.nbit, d_err_pos, g_begin, g_end));
+                  d_bytes, n_bytes, pk.gfirst, m, pk.n_slots, d_code_of, pk.text, pk.term,
+                  pk.nbit, d_err_pos, g_begin, g_end));
     return cudaGetLastError();
 }
 
