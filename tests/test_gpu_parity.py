@@ -814,3 +814,68 @@ def test_third_level_counting_path(SetBWTE):
     idx = SetBWTE(A, block_suffixes=1 << 26)
     idx.append(d, o)
     assert idx.bwt() == want
+
+
+# --- pack (pack.cu): string boundaries against 32-slot groups and 1024-slot
+# warp windows, runs of empty / one-symbol strings, long strings -------------
+
+def _pack_layout(kind, rng):
+    if kind == "short":       # 0..2 symbols: up to 32 terminators per group
+        lens = rng.integers(0, 3, size=3000)
+    elif kind == "edges":     # lengths 31, 32, 33, 1023, 1024, 1025 (slot = len + 1)
+        lens = rng.choice([30, 31, 32, 1022, 1023, 1024], size=300)
+    elif kind == "long":      # few long strings: groups with no terminator
+        lens = rng.integers(2000, 6000, size=12)
+    else:                     # mixed
+        lens = np.concatenate([rng.integers(0, 3, size=500), rng.integers(90, 110, size=300),
+                               rng.integers(1000, 3000, size=5)])
+        rng.shuffle(lens)
+    return ["".join("ACGT"[c] for c in rng.integers(0, 4, size=int(n))) for n in lens]
+
+
+@pytest.mark.parametrize("kind", ["short", "edges", "long", "mixed"])
+@pytest.mark.parametrize("lanes", [0, 3])
+def test_pack_layouts(SetBWTE, kind, lanes):
+    rng = np.random.default_rng(["short", "edges", "long", "mixed"].index(kind))
+    d, o = synth.from_strings(_pack_layout(kind, rng))
+    # small blocks: several pack ranges, each starting mid-group
+    M = max(64, int(o[-1] + len(o) - 1) // 5 + 1)
+    idx = SetBWTE(A, block_suffixes=M)
+    idx.set_option("sort_lanes", lanes)
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt(A, d, o)
+
+
+@pytest.mark.parametrize("where", ["first", "window_edge", "last", "two"])
+def test_pack_invalid_byte_position(SetBWTE, where):
+    """The first invalid byte is reported, wherever it falls against the
+    pack's groups and warp windows (the index stays as it was)."""
+    from paper_1410_0562_b200 import SetBWTEError
+    rng = np.random.default_rng(7)
+    d, o = synth.from_strings(_pack_layout("mixed", rng))
+    n = int(o[-1])
+    pos = {"first": [0], "window_edge": [1023 - 40, 2047 - 77], "last": [n - 1],
+           "two": [n // 2, n // 3]}[where]
+    bad = d.copy()
+    for p in pos:
+        bad[p] = ord("#")
+    idx = SetBWTE(A, block_suffixes=max(64, (n + len(o)) // 4))
+    idx.append_strings(["ACGT"])
+    with pytest.raises(SetBWTEError) as e:
+        idx.append(bad, o)
+    assert e.value.name == "E_INVALID_CHAR"
+    assert idx.last_error() == (min(pos), ord("#"))
+    assert idx.bwt() == oracle.bwt(A, *synth.from_strings(["ACGT"]))
+
+
+@pytest.mark.parametrize("kind", ["short", "edges", "mixed"])
+def test_pack_layouts_sigma5(SetBWTE, kind):
+    rng = np.random.default_rng(11 + len(kind))
+    strs = _pack_layout(kind, rng)
+    # an N in about every tenth string
+    strs = [s[:len(s) // 2] + "N" + s[len(s) // 2 + 1:] if s and i % 10 == 0 else s
+            for i, s in enumerate(strs)]
+    d, o = synth.from_strings(strs)
+    idx = SetBWTE("ACGTN", block_suffixes=max(64, int(o[-1] + len(o) - 1) // 3 + 1))
+    idx.append(d, o)
+    assert idx.bwt() == oracle.bwt("ACGTN", d, o)
