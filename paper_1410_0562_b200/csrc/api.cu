@@ -560,6 +560,8 @@ setbwte_status host_reserve(setbwte_t h, uint64_t nblk, const Blk* src, bool src
         h->hdict = nullptr;
         h->hdict_bytes = 0;
         h->hdict_cap = 0;
+        // a grown mapping took the dictionary's content with it
+        if (keep_blks && !src_dev) h->failed = true;
         return from_cuda(h, e);
     }
     void* pd = nullptr;
