@@ -209,13 +209,21 @@ def cpu_count():
 # ---------------------------------------------------------------------------
 # reference arm: the oracle (the slow CPU program) on the box's host cores
 # ---------------------------------------------------------------------------
+def sample_reads(offsets, max_reads, max_bases):
+    """The oracle's bounded sample: the longest prefix of the workload's reads
+    with at most max_reads reads and max_bases bases (at least one read)."""
+    m = len(offsets) - 1
+    k = int(np.searchsorted(np.asarray(offsets, dtype=np.uint64), np.uint64(max_bases), side="right")) - 1
+    return max(1, min(max_reads, m, k))
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return 0
     import oracle
     wl = args.workload
     data, offsets = gen(wl)
-    m_sample = min(args.ref_sample_reads, len(offsets) - 1)
+    m_sample = sample_reads(offsets, args.ref_sample_reads, args.ref_sample_bases)
     o = offsets[: m_sample + 1]
     d = data[: int(o[-1])]
     bases = float(o[-1])
@@ -472,7 +480,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and base is None:
         import oracle
         cores = cpu_count()
-        m_s = min(args.cpu_sample_reads, m)
+        m_s = sample_reads(offsets, args.cpu_sample_reads, args.cpu_sample_bases)
         o_s = offsets[: m_s + 1]
         d_s = data[: int(o_s[-1])]
         t0 = time.perf_counter()
@@ -536,7 +544,9 @@ def main():
     ap.add_argument("--block-suffixes", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-reads", type=int, default=1_000_000)
+    ap.add_argument("--cpu-sample-bases", type=int, default=100_000_000)
     ap.add_argument("--ref-sample-reads", type=int, default=100_000)
+    ap.add_argument("--ref-sample-bases", type=int, default=10_000_000)
     ap.add_argument("--option", action="append", default=[],
                     help="library option key=value (setbwte_set_option), repeatable")
     args = ap.parse_args()
