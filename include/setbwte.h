@@ -246,7 +246,9 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value);
 
 /* Kernel timing for setbwte_stats: mode 0 = off, 1 = every launch, 2 = only
  * launches of the kernel named `kernel` (CUDA events on the launching stream
- * around each timed launch; fewer events perturb the pipeline less). */
+ * around each timed launch; fewer events perturb the pipeline less), 3 =
+ * every launch plus a timeline ("timeline": [kernel, stream, start ms, end
+ * ms] per launch of the last append, from its start: which stages overlap). */
 setbwte_status setbwte_set_profile(setbwte_t h, int mode, const char* kernel);
 
 /* Use cuda_stream (a cudaStream_t on the handle's device) for all further

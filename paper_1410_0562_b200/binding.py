@@ -165,7 +165,9 @@ class SetBWTE:
         self._check(self._lib.setbwte_set_option(self._h, key.encode(), int(value)), "set_option")
 
     def set_profile(self, mode: int, kernel: str | None = None):
-        """0 off, 1 time every launch, 2 time only launches of `kernel`."""
+        """0 off, 1 time every launch, 2 time only launches of `kernel`, 3 every
+        launch plus a timeline (stats()["timeline"]: [kernel, stream, start ms,
+        end ms] per launch, from the append's start)."""
         self._check(self._lib.setbwte_set_profile(self._h, mode,
                                                   kernel.encode() if kernel else None),
                     "set_profile")

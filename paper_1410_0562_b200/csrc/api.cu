@@ -137,7 +137,7 @@ void Profiler::end(const char* name, cudaStream_t s, cudaEvent_t a) {
     if (on && a) {
         cudaEvent_t b = get_event();
         cudaEventRecord(b, s);
-        pending.push_back(Rec{name, a, b});
+        pending.push_back(Rec{name, a, b, s});
     }
 }
 
@@ -147,6 +147,12 @@ cudaError_t Profiler::resolve() {
         float ms = 0.f;
         cudaError_t e = cudaEventElapsedTime(&ms, r.a, r.b);
         if (e == cudaSuccess) k[r.name].ms += ms; else err = e;
+        if (tl && ref && e == cudaSuccess) {
+            float t0 = 0.f, t1 = 0.f;
+            if (cudaEventElapsedTime(&t0, ref, r.a) == cudaSuccess &&
+                cudaEventElapsedTime(&t1, ref, r.b) == cudaSuccess)
+                timeline.push_back(TL{r.name, (uint64_t)(uintptr_t)r.s, t0, t1});
+        }
         pool.push_back(r.a);
         pool.push_back(r.b);
     }
@@ -161,6 +167,7 @@ void Profiler::reset() {
     }
     pending.clear();
     k.clear();
+    timeline.clear();
     total_launches = 0;
 }
 
@@ -999,6 +1006,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         lanes[l].ev_sorted = h->ev_sorted[l];
         lanes[l].prof.on = h->prof.on;
         lanes[l].prof.only = h->prof.only;
+        lanes[l].prof.tl = h->prof.tl;
+        lanes[l].prof.ref = h->prof.ref;
     }
     if (h->sort_lanes == 0) {
         // no pipelining: every stage of every block in order on the calling
@@ -1129,6 +1138,8 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
             d.units += kv.second.units;
         }
         h->prof.total_launches += lanes[l].prof.total_launches;
+        h->prof.timeline.insert(h->prof.timeline.end(), lanes[l].prof.timeline.begin(),
+                                lanes[l].prof.timeline.end());
         h->sstats.digit_passes += lanes[l].st.digit_passes;
         h->sstats.rounds += lanes[l].st.rounds;
         h->sstats.replayed += lanes[l].st.replayed;
@@ -1172,7 +1183,19 @@ void build_stats(setbwte_t h) {
                  kv.second.bytes, (unsigned long long)kv.second.units);
         s += buf;
     }
-    s += "}}";
+    s += "}";
+    if (h->prof.tl) {
+        // mode 3: [kernel, stream, start ms, end ms] per launch, from the append's start
+        s += ", \"timeline\": [";
+        for (size_t i = 0; i < h->prof.timeline.size(); ++i) {
+            const Profiler::TL& t = h->prof.timeline[i];
+            snprintf(buf, sizeof(buf), "%s[\"%s\", %llu, %.4f, %.4f]", i ? ", " : "",
+                     t.name.c_str(), (unsigned long long)t.stream, t.t0, t.t1);
+            s += buf;
+        }
+        s += "]";
+    }
+    s += "}";
     h->stats_json = s;
 }
 
@@ -1185,6 +1208,7 @@ setbwte_status append_impl(setbwte_t h, const uint8_t* host_bytes, const uint64_
                            const uint8_t* d_bytes, const uint64_t* d_off, uint64_t m,
                            uint64_t n_bytes, bool prepend = false) {
     h->prof.reset();
+    if (h->prof.tl && h->prof.ref) API_CHECK(h, cudaEventRecord(h->prof.ref, h->stream));
     h->sstats = SortStats();
     h->last_blocks = 0;
     h->last_bases = 0;
@@ -1524,6 +1548,7 @@ void setbwte_destroy(setbwte_t h) {
         cudaStreamDestroy(h->copy_stream);
     }
     for (cudaEvent_t ev : h->ev_packed) cudaEventDestroy(ev);
+    if (h->prof.ref) cudaEventDestroy(h->prof.ref);
     if (h->derr_host) cudaFreeHost(h->derr_host);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
@@ -1874,9 +1899,11 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
 }
 
 setbwte_status setbwte_set_profile(setbwte_t h, int mode, const char* kernel) {
-    if (!h || mode < 0 || mode > 2 || (mode == 2 && !kernel)) return SETBWTE_E_INVALID_ARG;
+    if (!h || mode < 0 || mode > 3 || (mode == 2 && !kernel)) return SETBWTE_E_INVALID_ARG;
     h->prof.on = mode != 0;
     h->prof.only = mode == 2 ? std::string(kernel) : std::string();
+    h->prof.tl = mode == 3;
+    if (h->prof.tl && !h->prof.ref) API_CHECK(h, cudaEventCreate(&h->prof.ref));
     return SETBWTE_OK;
 }
 

@@ -56,8 +56,19 @@ struct Profiler {
     struct Rec {
         std::string name;
         cudaEvent_t a, b;
+        cudaStream_t s;
     };
     std::vector<Rec> pending;
+    // mode 3 (timeline): every launch's start and end, ms after `ref` (an
+    // event the append records on the main stream first; not owned here)
+    bool tl = false;
+    cudaEvent_t ref = nullptr;
+    struct TL {
+        std::string name;
+        uint64_t stream;
+        float t0, t1;
+    };
+    std::vector<TL> timeline;
     std::vector<cudaEvent_t> pool;
     std::map<std::string, KStat> k;
     uint64_t total_launches = 0;
