@@ -879,3 +879,24 @@ def test_pack_layouts_sigma5(SetBWTE, kind):
     idx = SetBWTE("ACGTN", block_suffixes=max(64, int(o[-1] + len(o) - 1) // 3 + 1))
     idx.append(d, o)
     assert idx.bwt() == oracle.bwt("ACGTN", d, o)
+
+
+def test_profile_timeline(SetBWTE, c1):
+    """Profile mode 3: every launch of the last append with its stream and
+    start / end (ms from the append's start); results unchanged."""
+    d, o, want = c1
+    idx = SetBWTE(A, block_suffixes=25250)
+    idx.set_profile(3)
+    idx.append(d, o)
+    st = idx.stats()
+    tl = st["timeline"]
+    assert len(tl) == st["launches"] > 0
+    names = {n for n, _, _, _ in tl}
+    assert {"compute_ranks", "gather", "insert", "pack"} <= names
+    assert all(t1 >= t0 >= -0.01 for _, _, t0, t1 in tl)
+    assert sum(k["launches"] for k in st["kernels"].values()) == len(tl)
+    assert idx.bwt() == want
+    idx.set_profile(0)
+    idx.clear()
+    idx.append(d, o)
+    assert "timeline" not in idx.stats()
