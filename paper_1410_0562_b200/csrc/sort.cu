@@ -902,6 +902,9 @@ __global__ void __launch_bounds__(256, SB_TINY_MINB) tiny_kernel(Lists in, Bufs 
 // others become child segments, keyed on the next digit (or the next word
 // at shift 0).
 // ---------------------------------------------------------------------------
+#ifndef SB_LD_MINB
+#define SB_LD_MINB 4  // resident CTAs per SM of local_digit_kernel<256>
+#endif
 constexpr int kLocIpt = 8;
 
 template <int NT>
@@ -912,7 +915,7 @@ constexpr size_t local_digit_smem() {
 
 // NT = 512: LOCALD (tile 4096); NT = 256: LOCALD2 (tile 2048)
 template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) local_digit_kernel(Lists in, Lists out, Bufs B,
+__global__ void __launch_bounds__(NT, NT == 256 ? SB_LD_MINB : 1024 / NT) local_digit_kernel(Lists in, Lists out, Bufs B,
                                                                    uint32_t* misc) {
     constexpr int kLocNt = NT;
     constexpr uint32_t kTileL = NT * kLocIpt;
