@@ -198,9 +198,11 @@ setbwte_status setbwte_compute_ranks(setbwte_t h, const uint8_t* strings, const 
  *   "sort_lanes"      host threads (each with its own CUDA stream) running
  *                     ConstructSA of upcoming blocks ahead of the in-order
  *                     rank/insert stage (the stage pipeline of P:190-191):
- *                     1..4 (default 3; fewer when the lanes' sort scratch,
- *                     ~30 B per suffix each, would exceed half the free device
- *                     memory), or 0 = every stage in order on the main stream.
+ *                     1..4, 0 = every stage in order on the main stream, or
+ *                     255 = automatic (the default: 3 lanes while the
+ *                     append's largest block has < 2^26 suffixes, else 2);
+ *                     fewer when the lanes' sort scratch, ~30 B per suffix
+ *                     each, would exceed half the free device memory.
  *   "hbm_budget_bytes" largest B_ext dictionary kept in HBM; beyond it B_ext
  *                     moves to pinned, mapped host memory ("host tier", P:12,
  *                     <= 3 n log(sigma) bits of system

@@ -263,7 +263,8 @@ struct setbwte_s {
 
     // options
     uint64_t M = 1ull << 24;
-    int sort_lanes = 3;    // host sort lanes; 0 = no pipelining (every stage on the main stream)
+    int sort_lanes = -1;   // host sort lanes; 0 = no pipelining (every stage on the main stream);
+                           // -1 = automatic (lanes_for)
     uint64_t lanes_checked_suf = 0;  // largest block the lane count was checked against free memory
     int lanes_checked_nl = 0;        // ... and the lane count that fitted
     uint64_t hbm_budget = ~0ull;  // max bytes of B_ext dictionary kept in HBM
@@ -958,6 +959,17 @@ void fail_partial(setbwte_t h) {
     h->failed = true;
 }
 
+// Sort lanes of an append whose largest block has max_suf suffixes: the
+// option's value, or automatically 3 for blocks below 2^26 suffixes and 2
+// from there (measured, alternated runs: c2's 2^24-suffix blocks 6.25 vs
+// 6.64 ms per step with 3 vs 2 lanes; c3's 2^27 185.1 vs 186.0 ms and c4's
+// 2^30 795 vs 871 ms with 2 vs 3 -- three large sorts at once contend more
+// than they overlap).
+int lanes_for(setbwte_t h, uint64_t max_suf) {
+    if (h->sort_lanes >= 0) return h->sort_lanes;
+    return max_suf >= (1ull << 26) ? 2 : 3;
+}
+
 // validate(): called on the main thread before the first Insert (the index is
 // untouched until then); a non-OK status aborts the append.
 setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<BlockDesc>& blocks,
@@ -969,7 +981,7 @@ setbwte_status run_blocks(setbwte_t h, const Packed& pk, const std::vector<Block
         max_suf = std::max(max_suf, b.S1 - b.S0);
         total += b.S1 - b.S0;
     }
-    int NL = std::max(1, std::min<int>({h->sort_lanes, (int)K, setbwte_s::kMaxLanes}));
+    int NL = std::max(1, std::min<int>({lanes_for(h, max_suf), (int)K, setbwte_s::kMaxLanes}));
     if (NL > 1 && (max_suf > h->lanes_checked_suf || NL > h->lanes_checked_nl)) {
         // each lane owns a sort scratch (~30 B per suffix of the largest
         // block): keep the lanes within half of the free device memory.
@@ -1882,8 +1894,12 @@ setbwte_status setbwte_set_option(setbwte_t h, const char* key, uint64_t value) 
         if (value > 1) return SETBWTE_E_INVALID_ARG;
         h->insert_split = value != 0;
     } else if (!strcmp(key, "sort_lanes")) {
-        if (value > (uint64_t)setbwte_s::kMaxLanes) return SETBWTE_E_INVALID_ARG;
-        h->sort_lanes = (int)value;
+        if (value == 255) {
+            h->sort_lanes = -1;  // automatic (the default)
+        } else {
+            if (value > (uint64_t)setbwte_s::kMaxLanes) return SETBWTE_E_INVALID_ARG;
+            h->sort_lanes = (int)value;
+        }
     } else if (!strcmp(key, "gather_buckets")) {
         if (value > 2) return SETBWTE_E_INVALID_ARG;
         h->gather_mode = (int)value;
