@@ -245,15 +245,30 @@ __global__ void __launch_bounds__(kInsNt) insert_kernel(
                 if (N5) on = (uint64_t)oo[0][3] | ((uint64_t)oo[1][3] << 32);
             }
             const uint64_t V = lim == 64 ? ~0ull : ((1ull << lim) - 1ull);  // real positions
-#pragma unroll
-            for (int c = 0; c < 4; ++c) c4[c] = __popcll(match_plane(c, ol, oh, od) & V);
+            // per code (match_plane): 1 = lo & ~hi, 2 = ~lo & hi, 3 = lo & hi,
+            // 0 = neither, over the non-'$' positions
+            const uint64_t nd = ~od & V;
+            const uint32_t nl = __popcll(ol & nd), nh = __popcll(oh & nd);
+            const uint32_t n3 = __popcll(ol & oh & nd), na = __popcll(nd);
+            c4[0] = na - nl - nh + n3;
+            c4[1] = nl - n3;
+            c4[2] = nh - n3;
+            c4[3] = n3;
             if (N5) c4[4] = __popcll(on & V);
         }
-        // in-superblock exclusive prefix of the per-word counts (4 codes, + N)
+        // in-superblock exclusive prefix of the per-word counts (4 codes, + N);
+        // codes in 16-bit pairs (a warp's 32 words hold <= 2048 of each)
         constexpr int NC = N5 ? 5 : 4;
         uint32_t inc[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) inc[c] = warp_incl(c4[c], lane);
+        {
+            const uint32_t i01 = warp_incl(c4[0] | (c4[1] << 16), lane);
+            const uint32_t i23 = warp_incl(c4[2] | (c4[3] << 16), lane);
+            inc[0] = i01 & 0xFFFFu;
+            inc[1] = i01 >> 16;
+            inc[2] = i23 & 0xFFFFu;
+            inc[3] = i23 >> 16;
+            if (N5) inc[NC - 1] = warp_incl(c4[4], lane);
+        }
         if (lane == 31) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) wsum[c][warp] = inc[c];
